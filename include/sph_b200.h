@@ -1,0 +1,237 @@
+/* sph_b200.h -- C ABI of the B200-native SPH particle-step library
+ * (libsphb200.so, built for sm_100a).
+ *
+ * Drop-in boundary for the reference's hot path (reference package `minisph`,
+ * /root/reference/pkg/src/minisph).  The reference crosses from Python into
+ * native code at exactly two call sites: `kernel.driver()(range_size, args)`
+ * (execution.py:129, particle_for) and the reduce driver (execution.py:206,
+ * particle_reduce); plus the CLL build and sort drivers it calls from the
+ * step (neighborhood.py:149-173, sorting.py:46-70).  Each entry point below
+ * names the reference interface it replaces.
+ *
+ * Conventions
+ *  - extern "C", plain pointers + sizes; every pointer marked (dev) is device
+ *    memory, everything else host memory.
+ *  - Every call enqueues work on the caller's stream and returns an int
+ *    status (SPH_OK == 0); it never throws and never allocates persistent
+ *    memory.  Scratch comes from the caller, sized by the *_bytes queries.
+ *  - `_f32` entry points implement the reference's precision="f32" run
+ *    (binary32 storage with the binary64 temporaries numba infers, no FMA);
+ *    `_f64` ones the precision="f64" run.  Results are bit-identical to the
+ *    reference on the same inputs.
+ */
+#ifndef SPH_B200_H
+#define SPH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPH_ABI_VERSION 1
+#define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
+
+/* status codes; mapped to the reference's exception classes by the host */
+enum {
+    SPH_OK = 0,
+    SPH_ERR_INVALID = 1,        /* bad argument (TypeError/ValueError)       */
+    SPH_ERR_CUDA = 2,           /* CUDA launch/runtime error                  */
+    SPH_ERR_NEGATIVE_KEY = 3,   /* ValueError, sorting.py:52-53               */
+    SPH_ERR_WORKSPACE = 4,      /* workspace smaller than *_bytes query       */
+    SPH_ERR_UNSUPPORTED = 5     /* grid too large for 32-bit cell keys, ...   */
+};
+
+int sph_abi_version(void);
+const char* sph_last_error(void);
+/* kernels launched by this library since load (bench gpu_launches) */
+long long sph_kernel_launches(void);
+
+/* ---------------------------------------------------------------------------
+ * Generic kernel-dispatch boundary: particle_for(policy, n, KERNEL, args)
+ * with args == force_args(registry, cll) (physics.py:315-330), arrays in the
+ * reference layout (vectors (n, d) row-major, index fields uint32) and the
+ * caller's CellLinkedList (offsets int64[C+1], particle_ids int64[n]).
+ * -------------------------------------------------------------------------*/
+typedef struct {
+    /* per-particle (dev) */
+    const float* x; const float* v; float* rho; float* p; const float* m;
+    const uint32_t* wall; const uint32_t* ids;
+    const int64_t* offsets; const int64_t* pids;
+    float* drho; float* dvdt; uint32_t* nnb; uint32_t* oflow;
+    float* rho_new;                 /* Shepard target, physics.py:222 */
+    /* host values */
+    float g[3]; float origin[3]; int64_t shape[3];
+    float cell_size, cutoff, h, alpha_d, c0, rho0, alpha_visc, eps_h2;
+    int64_t n; int32_t dim; int32_t reserved;
+} SphSweepArgs_f32;
+
+typedef struct {
+    const double* x; const double* v; double* rho; double* p; const double* m;
+    const uint32_t* wall; const uint32_t* ids;
+    const int64_t* offsets; const int64_t* pids;
+    double* drho; double* dvdt; uint32_t* nnb; uint32_t* oflow;
+    double* rho_new;
+    double g[3]; double origin[3]; int64_t shape[3];
+    double cell_size, cutoff, h, alpha_d, c0, rho0, alpha_visc, eps_h2;
+    int64_t n; int32_t dim; int32_t reserved;
+} SphSweepArgs_f64;
+
+/* scratch for the ordered neighbour lists the sweeps build */
+size_t sph_sweep_workspace_bytes(int64_t n);
+
+/* physics.py:94-119 CONTINUITY / :122-158 MOMENTUM / :161-194 WALL_PRESSURE /
+ * :197-217 DENSITY_SUMMATION / :220-247 SHEPARD, each over i in [0, n) */
+int sph_continuity_f32(const SphSweepArgs_f32* a, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_momentum_f32(const SphSweepArgs_f32* a, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_wall_pressure_f32(const SphSweepArgs_f32* a, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_density_summation_f32(const SphSweepArgs_f32* a, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_shepard_f32(const SphSweepArgs_f32* a, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_continuity_f64(const SphSweepArgs_f64* a, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_momentum_f64(const SphSweepArgs_f64* a, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_wall_pressure_f64(const SphSweepArgs_f64* a, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_density_summation_f64(const SphSweepArgs_f64* a, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_shepard_f64(const SphSweepArgs_f64* a, void* ws, size_t ws_bytes, cudaStream_t s);
+
+/* neighborhood.py:176-227 collect_neighbors for particles i0..i0+count-1:
+ * out_lists (dev, count x 256 int32) = physical j in ascending-id order,
+ * out_counts (dev, count) = count or -1 on overflow. */
+int sph_neighbors_f32(const SphSweepArgs_f32* a, int64_t i0, int64_t count,
+                      int32_t* out_lists, int32_t* out_counts, cudaStream_t s);
+int sph_neighbors_f64(const SphSweepArgs_f64* a, int64_t i0, int64_t count,
+                      int32_t* out_lists, int32_t* out_counts, cudaStream_t s);
+
+/* physics.py:250-256 KICK, :259-265 DRIFT, :268-274 DENSITY_UPDATE,
+ * :277-280 COPY_SCALAR (all dev arrays, reference layout) */
+int sph_kick_f32(float* v, const float* dvdt, const uint32_t* wall, int64_t n, int dim, float half_dt, cudaStream_t s);
+int sph_drift_f32(float* x, const float* v, const uint32_t* wall, int64_t n, int dim, float dt, cudaStream_t s);
+int sph_density_update_f32(float* rho, float* p, const float* drho, const uint32_t* wall, int64_t n,
+                           float dt, float c0, float rho0, cudaStream_t s);
+int sph_kick_f64(double* v, const double* dvdt, const uint32_t* wall, int64_t n, int dim, double half_dt, cudaStream_t s);
+int sph_drift_f64(double* x, const double* v, const uint32_t* wall, int64_t n, int dim, double dt, cudaStream_t s);
+int sph_density_update_f64(double* rho, double* p, const double* drho, const uint32_t* wall, int64_t n,
+                           double dt, double c0, double rho0, cudaStream_t s);
+int sph_copy(void* dst, const void* src, int64_t nbytes, cudaStream_t s);
+
+/* physics.py:296-310 VMAX_SPEC through particle_reduce (execution.py:191-209):
+ * *out (dev double) = max_i sqrt(sum_k f64(v_ik*v_ik)), identity 0.0 */
+int sph_vmax_f32(const float* v, int64_t n, int dim, double* out, cudaStream_t s);
+int sph_vmax_f64(const double* v, int64_t n, int dim, double* out, cudaStream_t s);
+
+/* ---------------------------------------------------------------------------
+ * Cell linked list and sort (neighborhood.py:105-173, sorting.py:46-81)
+ * -------------------------------------------------------------------------*/
+/* neighborhood.py:137-146 compute_cell_keys: keys (dev int64[n]) and the
+ * clamp count (*oob_count, dev uint32) */
+int sph_cell_keys_f32(const float* x, int64_t n, int dim, const float* origin, float cell_size,
+                      const int64_t* shape, int64_t* keys, uint32_t* oob_count, cudaStream_t s);
+int sph_cell_keys_f64(const double* x, int64_t n, int dim, const double* origin, double cell_size,
+                      const int64_t* shape, int64_t* keys, uint32_t* oob_count, cudaStream_t s);
+
+/* neighborhood.py:149-173 build_cell_linked_list: offsets (dev int64[C+1]),
+ * particle_ids (dev int64[n]) == argsort(keys, kind="stable"). */
+size_t sph_cll_workspace_bytes(int64_t n, int64_t ncells);
+int sph_cll_build_f32(const float* x, int64_t n, int dim, const float* origin, float cell_size,
+                      const int64_t* shape, int64_t* offsets, int64_t* particle_ids,
+                      uint32_t* oob_count, void* ws, size_t ws_bytes, cudaStream_t s);
+int sph_cll_build_f64(const double* x, int64_t n, int dim, const double* origin, double cell_size,
+                      const int64_t* shape, int64_t* offsets, int64_t* particle_ids,
+                      uint32_t* oob_count, void* ws, size_t ws_bytes, cudaStream_t s);
+
+/* sorting.py:46-70 radix_sort_permutation: stable LSD radix (8-bit digits)
+ * of non-negative int64 keys; perm (dev int64[n]).  *max_key_out (host) may
+ * be NULL.  Returns SPH_ERR_NEGATIVE_KEY on a negative key. */
+size_t sph_sort_workspace_bytes(int64_t n);
+int sph_radix_sort_perm(const int64_t* keys, int64_t n, int64_t* perm,
+                        void* ws, size_t ws_bytes, cudaStream_t s);
+
+/* variables.py:132-145 apply_permutation: dst[k] = src[perm[k]] for
+ * elements of elem_bytes (4, 8, 12, 16, 24 or 32). */
+int sph_gather(void* dst, const void* src, const int64_t* perm, int64_t n, int elem_bytes,
+               cudaStream_t s);
+
+/* ---------------------------------------------------------------------------
+ * Device-resident step engine: the B200 restatement of Simulation.advance
+ * (physics.py:489-552).  Particles live in two segments -- fluid [0, nf),
+ * walls [nf, n) -- each ordered by grid cell; the fluid segment is re-sorted
+ * by cell every advective step, the static walls once.  All accumulation
+ * runs in ascending original-id order, so every field is bit-identical to
+ * the reference for any physical order.
+ * -------------------------------------------------------------------------*/
+typedef struct {
+    unsigned long long vmax_bits;     /* exact max |v|   (f64 bits)            */
+    unsigned long long amax_bits;     /* exact max |dvdt| (f64 bits)           */
+    unsigned long long interactions;  /* report.py:20-21 directed visits       */
+    unsigned long long rho_min_key;   /* order-preserving key of min rho (f64) */
+    unsigned long long v2max_key;     /* key of max run-precision |v|^2        */
+    unsigned int overflow;            /* particles over NEIGHBOR_CAPACITY      */
+    unsigned int oob;                 /* fluid out-of-bounds clamps            */
+    unsigned int oob_walls;           /* wall clamps (counted once, at push)   */
+    unsigned int nfix;                /* skin-list fallbacks                   */
+    unsigned int nan_flags;           /* bit0: a NaN rho, bit1: a NaN |v|^2    */
+    unsigned int reserved;
+} SphStepStats;
+
+typedef struct {
+    /* sizes */
+    int64_t n, nf, ncells; int32_t dim; int32_t key_bits;
+    /* per-particle SoA, physical order (dev).  f32 run: float4/float2,
+     * f64 run: double4/double2 (reinterpret). pos.w == m. */
+    void* pos; void* vel[2]; void* rp[2]; void* dvdt; void* drho;
+    uint32_t* id; uint32_t* nnb; uint32_t* refpos;
+    /* by-id cold fields (dev) */
+    void* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; void* vol_id;
+    /* cell offsets into each segment (dev, ncells+1 each) */
+    uint32_t* offs_f; uint32_t* offs_w;
+    /* ordered neighbour lists: tile-ELL [n_slots/32][256][32] int32 + counts */
+    int32_t* lists; int32_t* lcount;
+    /* scratch (dev): keys/values x2 for the radix sort + gather staging */
+    void* ws; size_t ws_bytes;
+    SphStepStats* stats;              /* dev */
+    /* physics scalars (run precision, passed as double for both runs) */
+    double g[3]; double origin[3]; int64_t shape[3];
+    double cell_size, cutoff, h, alpha_d, c0, rho0, alpha_visc, eps_h2;
+    /* double-buffer selectors, maintained by the library */
+    int32_t cur_v, cur_rp;
+    int32_t f64;                      /* 0: f32 run, 1: f64 run */
+    int32_t reserved;
+} SphEngine;
+
+size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64);
+/* Registry-order (n,d)/(n,) device arrays <-> engine SoA.  push lays the
+ * particles out (fluid/wall split, cell order) and records refpos. */
+int sph_engine_push(SphEngine* e, const void* x, const void* v, const void* rho, const void* p,
+                    const void* m, const void* vol, const void* drho, const void* dvdt,
+                    const void* rho_scratch, const uint32_t* id, const uint32_t* wall,
+                    const uint32_t* nnb, const uint32_t* oflow, cudaStream_t s);
+int sph_engine_pull(const SphEngine* e, void* x, void* v, void* rho, void* p, void* m, void* vol,
+                    void* drho, void* dvdt, void* rho_scratch, uint32_t* id, uint32_t* wall,
+                    uint32_t* nnb, uint32_t* oflow, cudaStream_t s);
+/* physics.py:446-449 _rebuild_cll on the engine layout: re-sort the fluid
+ * segment by cell, rebuild the segment offsets; counts clamps into stats. */
+int sph_engine_rebuild_cll(SphEngine* e, cudaStream_t s);
+/* sorting.py:84-87 sort_particles_by_cell, tracked for the registry mirror */
+int sph_engine_ref_sort(SphEngine* e, cudaStream_t s);
+/* physics.py:460-467 initialize: wall pressure + momentum + counts */
+int sph_engine_initialize(SphEngine* e, cudaStream_t s);
+/* physics.py:469-487 _shepard_filter (SHEPARD, COPY_SCALAR, DENSITY_UPDATE) */
+int sph_engine_shepard(SphEngine* e, cudaStream_t s);
+/* physics.py:522-548 one acoustic sub-step: KICK, DRIFT, CONTINUITY,
+ * DENSITY_UPDATE, WALL_PRESSURE, MOMENTUM, KICK (fused) */
+int sph_engine_substep(SphEngine* e, double half_dt, double full_dt, cudaStream_t s);
+/* the same sub-step, synchronised, with CUDA-event times (ms) of its five
+ * kernels: kick+drift, neighbour lists, continuity+density update, wall
+ * pressure, momentum+kick (bench.py per-kernel roofline) */
+int sph_engine_substep_timed(SphEngine* e, double half_dt, double full_dt, float* ms_out,
+                             cudaStream_t s);
+/* flags & 1: reset the per-step counters (interactions, overflow, oob, nfix);
+ * flags & 2: recompute the exact vmax/amax (physics.py:390-391) and the
+ * stability inputs (physics.py:554-564) into e->stats */
+int sph_engine_stats(SphEngine* e, int flags, cudaStream_t s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPH_B200_H */

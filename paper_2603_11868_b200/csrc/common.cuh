@@ -1,0 +1,165 @@
+// common.cuh -- shared device helpers for the B200 SPH hot path (sm_100a).
+//
+// Exact-arithmetic contract: the reference's f32 run
+// evaluates array/f32-scalar operations in binary32 and anything touching a
+// Python float literal in binary64, with no FMA contraction, IEEE division
+// and square root.  Every floating-point operation on the hot path goes
+// through the explicit round-to-nearest intrinsics below, which nvcc never
+// contracts or reorders; the library is also built with --fmad=false.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/sph_b200.h"
+
+namespace sph {
+
+constexpr int kWarp = 32;
+constexpr int kCap = SPH_NEIGHBOR_CAPACITY;   // neighborhood.py:30
+
+// ---- exact scalar ops, T = run precision ------------------------------------
+template <class T> struct RN;
+template <> struct RN<float> {
+    static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+    static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
+    static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+    static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+    static __device__ __forceinline__ float sqrt(float a) { return __fsqrt_rn(a); }
+    static __device__ __forceinline__ float from_d(double a) { return __double2float_rn(a); }
+};
+template <> struct RN<double> {
+    static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+    static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+    static __device__ __forceinline__ double sqrt(double a) { return __dsqrt_rn(a); }
+    static __device__ __forceinline__ double from_d(double a) { return a; }
+};
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// ---- packed vectors ---------------------------------------------------------
+template <class T> struct V4;
+template <> struct V4<float> { using type = float4; };
+template <> struct V4<double> { using type = double4; };
+template <class T> struct V2;
+template <> struct V2<float> { using type = float2; };
+template <> struct V2<double> { using type = double2; };
+template <class T> using vec4 = typename V4<T>::type;
+template <class T> using vec2 = typename V2<T>::type;
+
+template <class T> __device__ __forceinline__ T comp(const vec4<T>& v, int k)
+{
+    return k == 0 ? v.x : (k == 1 ? v.y : v.z);
+}
+
+// ---- grid cell coordinate (neighborhood.py:76-84) ----------------------------
+// c = int(floor(f(f(x - origin) / cell_size))), clamped to [0, ncells-1].
+template <class T>
+__device__ __forceinline__ int cell_coord(T x, T origin, T cell_size, int ncells,
+                                          int& clamped)
+{
+    T t = RN<T>::div(RN<T>::sub(x, origin), cell_size);
+    T f = floor(t);
+    // int(floor(t)) on x86 maps NaN and |t| >= 2^63 to INT64_MIN, which the
+    // reference then clamps to cell 0; mirror that.
+    if (!(f >= T(0)) || f >= T(9.2233720368547758e18)) { clamped = 1; return 0; }
+    if (!(f < T(ncells))) { clamped = 1; return ncells - 1; }
+    return int(f);
+}
+
+// ---- Wendland C2 factors (physics.py:113-117, 184-186), binary64 ------------
+// fac = gw / r with gw = -5.0*alpha_d*q*tq*tq*tq/h, tq = 1.0 - 0.5*q.
+template <class T>
+__device__ __forceinline__ double grad_fac(T r, T q, T h, T alpha_d)
+{
+    double tq = dsub(1.0, dmul(0.5, double(q)));
+    double gw = dmul(-5.0, double(alpha_d));
+    gw = dmul(gw, double(q));
+    gw = dmul(gw, tq);
+    gw = dmul(gw, tq);
+    gw = dmul(gw, tq);
+    gw = ddiv(gw, double(h));
+    return ddiv(gw, double(r));
+}
+
+// w = alpha_d*tq*tq*tq*tq*(2.0*q + 1.0)
+template <class T>
+__device__ __forceinline__ double kernel_w(T q, T alpha_d)
+{
+    double tq = dsub(1.0, dmul(0.5, double(q)));
+    double w = dmul(double(alpha_d), tq);
+    w = dmul(w, tq);
+    w = dmul(w, tq);
+    w = dmul(w, tq);
+    return dmul(w, dadd(dmul(2.0, double(q)), 1.0));
+}
+
+// ---- warp helpers -----------------------------------------------------------
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt()
+{
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <class U>
+__device__ __forceinline__ U warp_sum(U v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w > v ? w : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ unsigned warp_min_u32(unsigned v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Order-preserving maps so exact max/min reductions can use integer atomics.
+// Non-negative doubles order like their bit patterns.
+__device__ __forceinline__ unsigned long long dbits(double v)
+{
+    return (unsigned long long)__double_as_longlong(v);
+}
+// float -> monotone u32 key (total order, -0 < +0)
+__device__ __forceinline__ unsigned fkey(float f)
+{
+    unsigned u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ unsigned long long dkey(double f)
+{
+    unsigned long long u = (unsigned long long)__double_as_longlong(f);
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// process-wide count of kernel launches issued by this library (bench.py
+// reports it as gpu_launches); defined in sort.cu
+void note_launch();
+
+inline int grid_for(int64_t n, int threads, int cap = 1 << 30)
+{
+    int64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return int(g);
+}
+
+}  // namespace sph

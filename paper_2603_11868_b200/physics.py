@@ -1,0 +1,756 @@
+"""Weakly-compressible SPH on B200: kernel objects, bindings and the
+device-resident step driver.
+
+Mirror of ``minisph/physics.py``.  Host-side formulas (Wendland alpha, EOS,
+``force_args`` scalars, time-step arithmetic) are the reference's own,
+evaluated with the same NumPy-2 scalar rules so the device receives the
+reference's exact binary32 scalars.  Every per-particle body runs in CUDA:
+``CONTINUITY`` ... ``COPY_SCALAR`` dispatch by identity to the C ABI
+(include/sph_b200.h), and :class:`Simulation` keeps the whole state in HBM
+and runs ``advance`` as the fused engine of csrc/engine.cu.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import struct
+import time
+
+import numpy as np
+
+from . import _native
+from . import variables as var
+from ._device import (Staging, device_of, is_tensor, ptr, stream_ptr,
+                      torch_mod, workspace)
+from .execution import (ExecutionPolicy, ParticleKernel, ReduceSpec,
+                        particle_for, particle_reduce)
+from .neighborhood import (NEIGHBOR_CAPACITY, NeighborOverflowError,
+                           build_cell_linked_list)
+
+
+class SimulationUnstableError(RuntimeError):
+    """physics.py:36-37"""
+
+
+# -- smoothing kernel and EOS (physics.py:42-73), host scalars ---------------
+
+def wendland_alpha(h, d):
+    if d == 2:
+        return 7.0 / (4.0 * math.pi * h * h)
+    return 21.0 / (16.0 * math.pi * h ** 3)
+
+
+def kernel_W(r, h, d):
+    q = r / h
+    if q >= 2.0:
+        return 0.0
+    t = 1.0 - 0.5 * q
+    return wendland_alpha(h, d) * t ** 4 * (2.0 * q + 1.0)
+
+
+def kernel_gradW(r, h, d):
+    q = r / h
+    if q >= 2.0:
+        return 0.0
+    t = 1.0 - 0.5 * q
+    return -5.0 * wendland_alpha(h, d) * q * t ** 3 / h
+
+
+def eos_pressure(rho, rho0, c0):
+    return c0 * c0 * (rho - rho0)
+
+
+def eos_density(p, rho0, c0):
+    return rho0 + p / (c0 * c0)
+
+
+# -- native kernel implementations (the particle_for boundary) ---------------
+
+def _dtype_of(a):
+    if is_tensor(a):
+        return np.dtype(str(a.dtype).replace("torch.", ""))
+    return np.asarray(a).dtype
+
+
+def _fill_common(a, dtype, n, dim, origin, shape, cell_size, cutoff, h, alpha_d):
+    dt = np.dtype(dtype).type
+    for k in range(3):
+        a.origin[k] = float(origin[k]) if k < dim else 0.0
+        a.shape[k] = int(shape[k]) if k < dim else 1
+    a.cell_size = dt(cell_size)
+    a.cutoff = dt(cutoff)
+    a.h = dt(h)
+    a.alpha_d = dt(alpha_d)
+    a.n = n
+    a.dim = dim
+
+
+def _run_sweep(entry, policy, n, fill):
+    """Stage arrays, fill the SphSweepArgs struct, call, write back."""
+    lib = _native.lib()
+    dev = device_of(policy)
+    with Staging(dev) as st:
+        a, dtype = fill(st)
+        ws_bytes = lib.sph_sweep_workspace_bytes(n)
+        ws = workspace(dev, ws_bytes)
+        fn = getattr(lib, f"sph_{entry}_{_native.sfx(dtype)}")
+        rc = fn(ctypes.byref(a), ptr(ws), ws_bytes, stream_ptr(dev))
+        _native.check(rc, entry)
+
+
+def _force_sweep(entry, writes):
+    """particle_for body for the force_args-bound sweeps (physics.py:94-194)."""
+
+    def native(policy, n, args):
+        (x, v, rho, p, m, wall, ids, g, offsets, pids, origin, shape,
+         drho, dvdt, nnb, oflow, cell_size, cutoff, h, alpha_d, c0, rho0,
+         avisc, eps_h2) = args
+        dtype = _dtype_of(x)
+        dim = int(np.asarray(shape).shape[0])
+
+        def fill(st):
+            a = _native.sweep_struct(dtype)()
+            dev_arrays = {}
+            for name, arr in (("x", x), ("v", v), ("rho", rho), ("p", p),
+                              ("m", m), ("wall", wall), ("ids", ids),
+                              ("offsets", offsets), ("pids", pids),
+                              ("drho", drho), ("dvdt", dvdt), ("nnb", nnb),
+                              ("oflow", oflow)):
+                dev_arrays[name] = st.to_dev(arr, writeback=name in writes)
+                setattr(a, name, ptr(dev_arrays[name]).value)
+            _fill_common(a, dtype, n, dim, np.asarray(origin), np.asarray(shape),
+                         cell_size, cutoff, h, alpha_d)
+            gg = np.asarray(g)
+            for k in range(3):
+                a.g[k] = float(gg[k]) if k < dim else 0.0
+            dt = np.dtype(dtype).type
+            a.c0, a.rho0 = dt(c0), dt(rho0)
+            a.alpha_visc, a.eps_h2 = dt(avisc), dt(eps_h2)
+            return a, dtype
+
+        _run_sweep(entry, policy, n, fill)
+
+    return native
+
+
+def _density_summation_native(policy, n, args):
+    """physics.py:197-217 via its kernel-shell argument tuple (:376-380)."""
+    (x, rho, m, ids, offsets, pids, origin, shape, cell_size, cutoff, h,
+     alpha_d) = args
+    dtype = _dtype_of(x)
+    dim = int(np.asarray(shape).shape[0])
+
+    def fill(st):
+        a = _native.sweep_struct(dtype)()
+        for name, arr, wb in (("x", x, False), ("rho", rho, True), ("m", m, False),
+                              ("ids", ids, False), ("offsets", offsets, False),
+                              ("pids", pids, False)):
+            setattr(a, name, ptr(st.to_dev(arr, writeback=wb)).value)
+        _fill_common(a, dtype, n, dim, np.asarray(origin), np.asarray(shape),
+                     cell_size, cutoff, h, alpha_d)
+        return a, dtype
+
+    _run_sweep("density_summation", policy, n, fill)
+
+
+def _shepard_native(policy, n, args):
+    """physics.py:220-247 via the _shepard_filter tuple (:473-478)."""
+    (x, rho, m, wall, ids, offsets, pids, origin, shape, rho_new, cell_size,
+     cutoff, h, alpha_d) = args
+    dtype = _dtype_of(x)
+    dim = int(np.asarray(shape).shape[0])
+
+    def fill(st):
+        a = _native.sweep_struct(dtype)()
+        for name, arr, wb in (("x", x, False), ("rho", rho, False), ("m", m, False),
+                              ("wall", wall, False), ("ids", ids, False),
+                              ("offsets", offsets, False), ("pids", pids, False),
+                              ("rho_new", rho_new, True)):
+            setattr(a, name, ptr(st.to_dev(arr, writeback=wb)).value)
+        _fill_common(a, dtype, n, dim, np.asarray(origin), np.asarray(shape),
+                     cell_size, cutoff, h, alpha_d)
+        return a, dtype
+
+    _run_sweep("shepard", policy, n, fill)
+
+
+def _dim_of(vec):
+    return int(vec.shape[1]) if len(vec.shape) == 2 else 1
+
+
+def _integ_native(entry):
+    def native(policy, n, args):
+        lib = _native.lib()
+        dev = device_of(policy)
+        if entry in ("kick", "drift"):
+            target, src, wall, scal = args
+            dtype = _dtype_of(target)
+            with Staging(dev) as st:
+                t = st.to_dev(target, writeback=True)
+                s_ = st.to_dev(src)
+                w = st.to_dev(wall)
+                fn = getattr(lib, f"sph_{entry}_{_native.sfx(dtype)}")
+                rc = fn(ptr(t), ptr(s_), ptr(w), n, _dim_of(target),
+                        np.dtype(dtype).type(scal), stream_ptr(dev))
+                _native.check(rc, entry)
+        elif entry == "density_update":
+            rho, p, drho, wall, dt_, c0, rho0 = args
+            dtype = _dtype_of(rho)
+            T = np.dtype(dtype).type
+            with Staging(dev) as st:
+                r = st.to_dev(rho, writeback=True)
+                pp = st.to_dev(p, writeback=True)
+                d = st.to_dev(drho)
+                w = st.to_dev(wall)
+                fn = getattr(lib, f"sph_density_update_{_native.sfx(dtype)}")
+                rc = fn(ptr(r), ptr(pp), ptr(d), ptr(w), n, T(dt_), T(c0), T(rho0),
+                        stream_ptr(dev))
+                _native.check(rc, entry)
+        else:   # copy_scalar: dst[i] = src[i] for i < n
+            dst, src = args
+            with Staging(dev) as st:
+                d = st.to_dev(dst, writeback=True)
+                s_ = st.to_dev(src)
+                nbytes = n * d.element_size() * (d[0].numel() if d.dim() > 1 else 1)
+                rc = lib.sph_copy(ptr(d), ptr(s_), nbytes, stream_ptr(dev))
+                _native.check(rc, entry)
+
+    return native
+
+
+def _vmax_native(policy, n, args):
+    """VMAX_SPEC (physics.py:296-310): exact max of |row|, a float64."""
+    (v,) = args
+    lib = _native.lib()
+    dev = device_of(policy)
+    torch = torch_mod()
+    dtype = _dtype_of(v)
+    with Staging(dev) as st:
+        vv = st.to_dev(v)
+        out = st.empty((1,), torch.float64)
+        fn = getattr(lib, f"sph_vmax_{_native.sfx(dtype)}")
+        rc = fn(ptr(vv), n, _dim_of(v), ptr(out), stream_ptr(dev))
+        _native.check(rc, "vmax")
+        return np.float64(out.cpu().item())
+
+
+def _body_doc(name):
+    def body(i, args):   # pragma: no cover - documentation stub
+        raise NotImplementedError(f"{name} runs on the GPU")
+    body.__name__ = name
+    return body
+
+
+CONTINUITY = ParticleKernel(_body_doc("_continuity_body"), "continuity",
+                            _force_sweep("continuity", {"drho", "oflow"}))
+MOMENTUM = ParticleKernel(_body_doc("_momentum_body"), "momentum",
+                          _force_sweep("momentum", {"dvdt", "nnb", "oflow"}))
+WALL_PRESSURE = ParticleKernel(_body_doc("_wall_pressure_body"), "wall_pressure",
+                               _force_sweep("wall_pressure",
+                                            {"p", "rho", "nnb", "oflow"}))
+DENSITY_SUMMATION = ParticleKernel(_body_doc("_density_summation_body"),
+                                   "density_summation", _density_summation_native)
+SHEPARD = ParticleKernel(_body_doc("_shepard_body"), "shepard", _shepard_native)
+KICK = ParticleKernel(_body_doc("_kick_body"), "kick", _integ_native("kick"))
+DRIFT = ParticleKernel(_body_doc("_drift_body"), "drift", _integ_native("drift"))
+DENSITY_UPDATE = ParticleKernel(_body_doc("_density_update_body"), "density_update",
+                                _integ_native("density_update"))
+COPY_SCALAR = ParticleKernel(_body_doc("_copy_scalar_body"), "copy_scalar",
+                             _integ_native("copy"))
+
+
+def _vnorm_transform(i, args):   # pragma: no cover - documentation stub
+    raise NotImplementedError("VMAX_SPEC runs on the GPU")
+
+
+def _fmax(a, b):
+    return max(a, b)
+
+
+VMAX_SPEC = ReduceSpec(0.0, _vnorm_transform, _fmax, native=_vmax_native)
+
+
+# -- kernel-shell layer (physics.py:315-381) ----------------------------------
+
+def force_scalars(registry, grid):
+    """The scalar tail of force_args with NumPy-2 scalar semantics
+    (physics.py:327-330)."""
+    dt = registry.dtype.type
+    h = registry.singular("h")
+    return (dt(grid.cell_size), dt(2.0 * h), dt(h),
+            dt(wendland_alpha(h, registry.dim)),
+            dt(registry.singular("c0")), dt(registry.singular("rho0")),
+            dt(registry.singular("alpha_visc")), dt(0.01 * h * h))
+
+
+def force_args(registry, cll):
+    """The shared neighbour-sweep argument tuple (physics.py:315-330)."""
+    return ((registry.view("x"), registry.view("v"), registry.view("rho"),
+             registry.view("p"), registry.view("m"), registry.view("wall"),
+             registry.view("id"), registry.singular("g"),
+             cll.offsets, cll.particle_ids,
+             cll.grid.origin.astype(registry.dtype),
+             cll.grid.shape_array(),
+             registry.view("drho"), registry.view("dvdt"),
+             registry.view("nnb"), registry.view("oflow"))
+            + force_scalars(registry, cll.grid))
+
+
+def evaluate_forces(policy, registry, cll):
+    evaluate_continuity(policy, registry, cll)
+    evaluate_momentum(policy, registry, cll)
+
+
+def evaluate_continuity(policy, registry, cll):
+    particle_for(policy, registry.particle_count, CONTINUITY,
+                 force_args(registry, cll))
+    _check_overflow(registry)
+
+
+def evaluate_momentum(policy, registry, cll):
+    particle_for(policy, registry.particle_count, MOMENTUM,
+                 force_args(registry, cll))
+    _check_overflow(registry)
+
+
+def extrapolate_wall_pressure(policy, registry, cll):
+    particle_for(policy, registry.particle_count, WALL_PRESSURE,
+                 force_args(registry, cll))
+    _check_overflow(registry)
+
+
+def _check_overflow(registry):
+    if registry.view("oflow").any():
+        raise NeighborOverflowError(
+            f"neighbor buffer capacity {NEIGHBOR_CAPACITY} exceeded")
+
+
+class DensitySummationDynamics:
+    """rho_i = sum_j m_j W_ij including self (physics.py:363-381)."""
+
+    kernel = DENSITY_SUMMATION
+
+    def __init__(self, registry, cll):
+        self.registry = registry
+        self.cll = cll
+
+    def setup(self):
+        reg, cll = self.registry, self.cll
+        dt = reg.dtype.type
+        h = reg.singular("h")
+        args = (reg.view("x"), reg.view("rho"), reg.view("m"), reg.view("id"),
+                cll.offsets, cll.particle_ids,
+                cll.grid.origin.astype(reg.dtype), cll.grid.shape_array(),
+                dt(cll.grid.cell_size), dt(2.0 * h), dt(h),
+                dt(wendland_alpha(h, reg.dim)))
+        return reg.particle_count, args
+
+
+# -- time stepping (physics.py:386-413) --------------------------------------
+
+def timestep_formula(vmax, amax, h, c0, dt_max, cfl_acoustic=0.6,
+                     cfl_advective=0.25):
+    """The host arithmetic of compute_timestep (physics.py:392-400)."""
+    dt_acoustic = cfl_acoustic * h / (c0 + vmax)
+    dt_advective = dt_max
+    if vmax > 0.0:
+        dt_advective = min(dt_advective, cfl_advective * h / vmax)
+    if amax > 0.0:
+        dt_advective = min(dt_advective, cfl_advective * math.sqrt(h / amax))
+    return dt_acoustic, dt_advective
+
+
+def compute_timestep(policy, registry, dt_max, cfl_acoustic=0.6,
+                     cfl_advective=0.25):
+    """Dual criteria from exact device max-reductions (physics.py:386-400)."""
+    n = registry.particle_count
+    vmax = float(particle_reduce(policy, n, VMAX_SPEC, (registry.view("v"),)))
+    amax = float(particle_reduce(policy, n, VMAX_SPEC, (registry.view("dvdt"),)))
+    return timestep_formula(vmax, amax, float(registry.singular("h")),
+                            float(registry.singular("c0")), dt_max,
+                            cfl_acoustic, cfl_advective)
+
+
+def setup_state_variables(registry):
+    """physics.py:403-413"""
+    for name, kind in (("x", var.VECTOR), ("v", var.VECTOR),
+                       ("rho", var.SCALAR), ("p", var.SCALAR),
+                       ("m", var.SCALAR), ("Vol", var.SCALAR),
+                       ("drho", var.SCALAR), ("dvdt", var.VECTOR),
+                       ("rho_scratch", var.SCALAR)):
+        registry.register_discrete(name, kind)
+    registry.register_discrete("wall", var.INDEX)
+    registry.register_discrete("nnb", var.INDEX)
+    registry.register_discrete("oflow", var.INDEX)
+
+
+# -- device-resident driver ----------------------------------------------------
+
+SUBSTEP_KERNELS = ("kick_drift", "build_lists", "continuity_du", "wall_pressure",
+                   "momentum_kick")
+
+_ENGINE_FIELDS = ("x", "v", "rho", "p", "m", "Vol", "drho", "dvdt",
+                  "rho_scratch", "id", "wall", "nnb", "oflow")
+
+
+def _key_to_double(k):
+    """Inverse of the kernels' order-preserving double -> u64 key."""
+    if k & (1 << 63):
+        u = k & ~(1 << 63)
+    else:
+        u = ~k & 0xFFFFFFFFFFFFFFFF
+    return struct.unpack("<d", struct.pack("<Q", u))[0]
+
+
+def _bits_to_double(b):
+    return struct.unpack("<d", struct.pack("<Q", b))[0]
+
+
+class Simulation:
+    """Advective-step driver (physics.py:416-564) with the state in HBM.
+
+    Constructor, attributes and methods follow the reference.  The registry
+    stays the user-facing owner: the first ``initialize``/``advance`` pushes
+    it to the device; ``registry.view(...)`` pulls the device state back into
+    the registry's arrays in the reference's physical order (the engine tracks
+    the reference's sort_every permutation), after which the host copy is
+    authoritative again for the next step.
+    """
+
+    def __init__(self, registry, grid, policy, dt_max=1e-3, sort_every=100,
+                 shepard_every=200, fixed_dt=None, cfl_acoustic=0.6,
+                 cfl_advective=0.25):
+        self.registry = registry
+        self.grid = grid
+        self.policy = policy
+        self.dt_max = dt_max
+        self.sort_every = sort_every
+        self.shepard_every = shepard_every
+        self.fixed_dt = fixed_dt
+        self.cfl_acoustic = cfl_acoustic
+        self.cfl_advective = cfl_advective
+        self.step_count = 0
+        self.time = 0.0
+        self.interaction_count = 0
+        self.phase_seconds = {"cll": 0.0, "interactions": 0.0,
+                              "integration": 0.0, "sorting": 0.0}
+        self.out_of_bounds = 0
+        self.last_nsub = 0
+        self._dev = None
+        self._host_dirty = True     # host registry is authoritative
+        self._host_stale = False    # device is ahead of the host registry
+        self._norms = None          # (vmax, amax) valid for the device state
+        self._oob_walls = 0
+        self.kernel_times = None    # dict name -> [ms per launch] when profiling
+        registry.attach_engine(self)
+
+    # -- registry coupling ----------------------------------------------------
+
+    def host_modified(self):
+        self._host_dirty = True
+        self._norms = None
+
+    def pull_to_host(self):
+        """Write the device state into the registry (reference order)."""
+        if self._dev is None or not self._host_stale:
+            return
+        self._host_stale = False
+        d = self._dev
+        torch = torch_mod()
+        reg = self.registry
+        outs = {}
+        for f in _ENGINE_FIELDS:
+            host = reg.raw_view(f)
+            tdt = torch.int32 if host.dtype == np.uint32 else d["tdtype"]
+            outs[f] = torch.empty(host.shape, dtype=tdt, device=d["device"])
+        rc = _native.lib().sph_engine_pull(
+            ctypes.byref(d["E"]), *[ptr(outs[f]) for f in _ENGINE_FIELDS],
+            d["stream"])
+        _native.check(rc, "engine_pull")
+        for f in _ENGINE_FIELDS:
+            host = reg.raw_view(f)
+            hv = host.view(np.int32) if host.dtype == np.uint32 else host
+            torch.from_numpy(hv).copy_(outs[f])
+        # the caller may now modify the host arrays in place
+        self._host_dirty = True
+        self._norms = None
+
+    @property
+    def cll(self):
+        """A reference CellLinkedList of the current positions (diagnostic)."""
+        return build_cell_linked_list(self.policy, self.registry.view("x"),
+                                      self.grid)
+
+    # -- device state ---------------------------------------------------------
+
+    def _alloc(self):
+        torch = torch_mod()
+        reg = self.registry
+        dev = device_of(self.policy)
+        n, d = reg.particle_count, reg.dim
+        f64 = reg.dtype == np.float64
+        tdt = torch.float64 if f64 else torch.float32
+        ncells = self.grid.cell_count
+        if self.grid.dim != d:
+            raise ValueError("grid and registry dimensions differ")
+        key_bits = max(1, int(ncells - 1).bit_length())
+        lib = _native.lib()
+        wall = reg.raw_view("wall")
+        nf = int((wall == 0).sum())
+        nw = n - nf
+        tiles = (nf + 31) // 32 + (nw + 31) // 32
+        i32 = torch.int32
+        T = {}
+        T["pos"] = torch.empty((n, 4), dtype=tdt, device=dev)
+        T["vel0"] = torch.empty((n, 4), dtype=tdt, device=dev)
+        T["vel1"] = torch.empty((n, 4), dtype=tdt, device=dev)
+        T["rp0"] = torch.empty((n, 2), dtype=tdt, device=dev)
+        T["rp1"] = torch.empty((n, 2), dtype=tdt, device=dev)
+        T["dvdt"] = torch.empty((n, 4), dtype=tdt, device=dev)
+        T["drho"] = torch.empty((n,), dtype=tdt, device=dev)
+        for k in ("id", "nnb", "refpos", "oflow_id", "wall_id"):
+            T[k] = torch.empty((n,), dtype=i32, device=dev)
+        T["rho_scratch_id"] = torch.empty((n,), dtype=tdt, device=dev)
+        T["vol_id"] = torch.empty((n,), dtype=tdt, device=dev)
+        T["offs_f"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
+        T["offs_w"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
+        T["lists"] = torch.empty((max(tiles, 1), NEIGHBOR_CAPACITY, 32), dtype=i32,
+                                 device=dev)
+        T["lcount"] = torch.empty((max(tiles, 1) * 32,), dtype=i32, device=dev)
+        ws_bytes = lib.sph_engine_workspace_bytes(n, ncells, int(f64))
+        T["ws"] = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
+        T["stats"] = torch.zeros((ctypes.sizeof(_native.SphStepStats),),
+                                 dtype=torch.uint8, device=dev)
+        E = _native.SphEngine()
+        E.n, E.nf, E.ncells, E.dim, E.key_bits = n, nf, ncells, d, key_bits
+        E.pos = T["pos"].data_ptr()
+        E.vel[0], E.vel[1] = T["vel0"].data_ptr(), T["vel1"].data_ptr()
+        E.rp[0], E.rp[1] = T["rp0"].data_ptr(), T["rp1"].data_ptr()
+        for k in ("dvdt", "drho", "id", "nnb", "refpos", "rho_scratch_id",
+                  "oflow_id", "wall_id", "vol_id", "offs_f", "offs_w", "lists",
+                  "lcount", "ws", "stats"):
+            setattr(E, k, T[k].data_ptr())
+        E.ws_bytes = ws_bytes
+        (cs, cutoff, h, alpha_d, c0, rho0, avisc, eps_h2) = force_scalars(reg, self.grid)
+        g = np.asarray(reg.singular("g"))
+        origin = self.grid.origin.astype(reg.dtype)
+        for k in range(3):
+            E.g[k] = float(g[k]) if k < d else 0.0
+            E.origin[k] = float(origin[k]) if k < d else 0.0
+            E.shape[k] = int(self.grid.shape[k]) if k < d else 1
+        E.cell_size, E.cutoff, E.h, E.alpha_d = (float(cs), float(cutoff),
+                                                 float(h), float(alpha_d))
+        E.c0, E.rho0, E.alpha_visc, E.eps_h2 = (float(c0), float(rho0),
+                                                float(avisc), float(eps_h2))
+        E.f64 = int(f64)
+        self._dev = {"device": dev, "E": E, "T": T, "tdtype": tdt,
+                     "stream": stream_ptr(dev),
+                     "stats_host": torch.empty(T["stats"].shape, dtype=torch.uint8,
+                                               pin_memory=True)}
+
+    def _push(self):
+        """Registry -> device SoA (physics layout, cell order)."""
+        torch = torch_mod()
+        reg = self.registry
+        ids = reg.raw_view("id")
+        n = reg.particle_count
+        if n and (ids.min() != 0 or ids.max() != n - 1
+                  or np.bincount(ids.astype(np.int64), minlength=n).max() != 1):
+            raise ValueError("registry ids must be a permutation of 0..N-1")
+        if self._dev is None or int((reg.raw_view("wall") == 0).sum()) != self._dev["E"].nf:
+            self._alloc()
+        d = self._dev
+        st = Staging(d["device"])
+        devs = [st.to_dev(reg.raw_view(f)) for f in _ENGINE_FIELDS]
+        rc = _native.lib().sph_engine_push(ctypes.byref(d["E"]),
+                                           *[ptr(t) for t in devs], d["stream"])
+        _native.check(rc, "engine_push")
+        stats = self._read_stats()
+        self._oob_walls = stats.oob_walls
+        del devs, st
+        self._host_dirty = False
+        self._host_stale = False
+        self._norms = None
+
+    def _ensure_device(self):
+        if self._host_dirty:
+            self._push()
+
+    def _call(self, name, *args):
+        d = self._dev
+        rc = getattr(_native.lib(), name)(ctypes.byref(d["E"]), *args, d["stream"])
+        _native.check(rc, name)
+
+    def _read_stats(self):
+        d = self._dev
+        d["stats_host"].copy_(d["T"]["stats"], non_blocking=True)
+        torch_mod().cuda.current_stream(d["device"]).synchronize()
+        return _native.SphStepStats.from_buffer_copy(d["stats_host"].numpy().tobytes())
+
+    def _finish_counts(self, stats, check):
+        if stats.overflow and check:
+            raise NeighborOverflowError(
+                f"neighbor buffer capacity {NEIGHBOR_CAPACITY} exceeded")
+        self._norms = (_bits_to_double(stats.vmax_bits),
+                       _bits_to_double(stats.amax_bits))
+
+    # -- reference API ---------------------------------------------------------
+
+    def _rebuild_cll(self):
+        """physics.py:446-449 on the engine layout."""
+        t0 = time.perf_counter()
+        self._call("sph_engine_rebuild_cll")
+        self.phase_seconds["cll"] += time.perf_counter() - t0
+
+    def initialize(self):
+        """physics.py:460-467: CLL, wall pressure, momentum, counts."""
+        self._ensure_device()
+        self._call("sph_engine_stats", ctypes.c_int32(_native.STATS_RESET))
+        self._rebuild_cll()
+        t0 = time.perf_counter()
+        self._call("sph_engine_initialize")
+        self._call("sph_engine_stats", ctypes.c_int32(_native.STATS_NORMS))
+        stats = self._read_stats()
+        self.phase_seconds["interactions"] += time.perf_counter() - t0
+        self._host_stale = True
+        self.out_of_bounds += stats.oob + self._oob_walls
+        self._finish_counts(stats, check=True)
+        self.interaction_count += int(stats.interactions)
+
+    def _shepard_filter(self):
+        """physics.py:469-487 (SHEPARD, COPY_SCALAR, DENSITY_UPDATE(0))."""
+        self._ensure_device()
+        self._call("sph_engine_shepard")
+        self._host_stale = True
+
+    def advance(self, end_time=None):
+        """One advective step (physics.py:489-552); returns the dt taken."""
+        self._ensure_device()
+        d = self._dev
+        L = _native.lib()
+        if self.sort_every and self.step_count > 0 \
+                and self.step_count % self.sort_every == 0:
+            t0 = time.perf_counter()
+            self._call("sph_engine_ref_sort")
+            self.phase_seconds["sorting"] += time.perf_counter() - t0
+        flags = _native.STATS_RESET | (0 if self._norms else _native.STATS_NORMS)
+        self._call("sph_engine_stats", ctypes.c_int32(flags))
+        self._rebuild_cll()
+        if self.shepard_every and self.step_count > 0 \
+                and self.step_count % self.shepard_every == 0:
+            t0 = time.perf_counter()
+            self._call("sph_engine_shepard")
+            self.phase_seconds["interactions"] += time.perf_counter() - t0
+        if self.fixed_dt is not None:
+            dt_ac = dt_adv = self.fixed_dt
+        else:
+            t0 = time.perf_counter()
+            if self._norms is None:
+                s = self._read_stats()
+                self._norms = (_bits_to_double(s.vmax_bits),
+                               _bits_to_double(s.amax_bits))
+            vmax, amax = self._norms
+            dt_ac, dt_adv = timestep_formula(
+                vmax, amax, float(self.registry.singular("h")),
+                float(self.registry.singular("c0")), self.dt_max,
+                self.cfl_acoustic, self.cfl_advective)
+            self.phase_seconds["integration"] += time.perf_counter() - t0
+        dt = dt_adv
+        if end_time is not None:
+            dt = min(dt, end_time - self.time)
+        nsub = max(1, int(math.ceil(dt / dt_ac)))
+        dts = dt / nsub
+        dtype = self.registry.dtype.type
+        half = float(dtype(0.5 * dts))
+        full = float(dtype(dts))
+        t0 = time.perf_counter()
+        E = ctypes.byref(d["E"])
+        if self.kernel_times is None:
+            for _ in range(nsub):
+                rc = L.sph_engine_substep(E, half, full, d["stream"])
+                if rc:
+                    _native.check(rc, "engine_substep")
+        else:   # per-kernel CUDA-event timing (bench.py roofline pass)
+            ms = (ctypes.c_float * 5)()
+            for _ in range(nsub):
+                rc = L.sph_engine_substep_timed(E, half, full, ms, d["stream"])
+                _native.check(rc, "engine_substep_timed")
+                for k, name in enumerate(SUBSTEP_KERNELS):
+                    self.kernel_times.setdefault(name, []).append(ms[k])
+        self._call("sph_engine_stats", ctypes.c_int32(_native.STATS_NORMS))
+        stats = self._read_stats()
+        self.phase_seconds["interactions"] += time.perf_counter() - t0
+        self._host_stale = True
+        self.last_nsub = nsub
+        self.out_of_bounds += stats.oob + self._oob_walls
+        self._finish_counts(stats, check=True)
+        self.interaction_count += int(stats.interactions)
+        self.step_count += 1
+        self.time += dt
+        c0 = float(self.registry.singular("c0"))
+        # physics.py:554-564 with numpy's NaN-propagating min/max
+        rho_min = (math.nan if stats.nan_flags & 1
+                   else _key_to_double(stats.rho_min_key))
+        if self.registry.particle_count and rho_min <= 0.0:
+            raise SimulationUnstableError(
+                f"non-positive density at step {self.step_count}")
+        v2 = _key_to_double(stats.v2max_key) if self.registry.particle_count else 0.0
+        if stats.nan_flags & 2:
+            v2 = math.nan
+        vmax_f = float(np.sqrt(self.registry.dtype.type(v2)))
+        if self.registry.particle_count and vmax_f > 10.0 * c0:
+            raise SimulationUnstableError(
+                f"runaway velocity {vmax_f:.3g} at step {self.step_count}")
+        return dt
+
+    def _stability_check(self, c0):
+        """physics.py:554-564 on the registry state."""
+        rho = self.registry.view("rho")
+        if rho.size and float(rho.min()) <= 0.0:
+            raise SimulationUnstableError(
+                f"non-positive density at step {self.step_count}")
+        v = self.registry.view("v")
+        if v.size:
+            vmax = float(np.sqrt((v * v).sum(axis=1).max()))
+            if vmax > 10.0 * c0:
+                raise SimulationUnstableError(
+                    f"runaway velocity {vmax:.3g} at step {self.step_count}")
+
+
+# -- diagnostics (physics.py:569-606; host-side helpers) ----------------------
+
+def total_energy(registry):
+    m = registry.view("m")
+    v = registry.view("v")
+    x = registry.view("x")
+    rho = registry.view("rho")
+    wall = registry.view("wall")
+    g = np.asarray(registry.singular("g"), dtype=np.float64)
+    c0 = float(registry.singular("c0"))
+    rho0 = float(registry.singular("rho0"))
+    fluid = wall == 0
+    ke = 0.5 * float((m[fluid] * (v[fluid] ** 2).sum(axis=1)).sum())
+    pe = -float((m[fluid] * (x[fluid] @ g)).sum())
+    dr = rho[fluid].astype(np.float64) - rho0
+    ce = float((m[fluid] * c0 * c0 * dr * dr / (2.0 * rho0 * rho[fluid])).sum())
+    return ke + pe + ce
+
+
+def sample_pressure(registry, location):
+    x = registry.view("x")
+    wall = registry.view("wall")
+    h = float(registry.singular("h"))
+    d = registry.dim
+    loc = np.asarray(location, dtype=np.float64)
+    diff = x.astype(np.float64) - loc
+    r = np.sqrt((diff * diff).sum(axis=1))
+    mask = (r < 2.0 * h) & (wall == 0)
+    if not mask.any():
+        return 0.0
+    w = np.array([kernel_W(ri, h, d) for ri in r[mask]])
+    vol = (registry.view("m")[mask] / registry.view("rho")[mask]).astype(np.float64)
+    den = float((w * vol).sum())
+    if den == 0.0:
+        return 0.0
+    return float((registry.view("p")[mask] * w * vol).sum() / den)

@@ -1,0 +1,195 @@
+"""The device-resident step engine (physics.Simulation) vs the reference.
+
+Whole-step trajectories against the reference's own fixtures (every discrete
+variable by id AND in the registry's physical order, dt, nsub, interaction
+and clamp counts), and against the CPU oracle on larger cases and on
+configurations the fixtures do not cover.
+"""
+
+import numpy as np
+import pytest
+
+from _util import FIELDS, TRAJ, by_id, case, golden, mismatched, sha
+
+import paper_2603_11868_b200 as P
+from paper_2603_11868_b200 import cases
+from paper_2603_11868_b200.physics import (Simulation, SimulationUnstableError,
+                                           compute_timestep)
+from paper_2603_11868_b200.neighborhood import NeighborOverflowError
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+CUDA = P.ExecutionPolicy.cuda()
+
+
+def _engine_fields(reg):
+    return {f: reg.view(f) for f in FIELDS}
+
+
+@pytest.mark.parametrize("tag", sorted(TRAJ))
+def test_engine_trajectory_bitwise_vs_reference(tag):
+    z = golden(f"traj_{tag}.npz")
+    reg, grid = case(tag)
+    sim = Simulation(reg, grid, CUDA)
+    sim.initialize()
+    assert sim.interaction_count == z["interactions"][0]
+    ids = lambda: reg.view("id")
+    assert not mismatched(lambda f: by_id(reg.view(f), ids()), z, 0)
+    steps = len(z["dt"]) - 1
+    check_every = 1 if steps <= 250 else 10
+    for step in range(1, steps + 1):
+        dt = sim.advance()
+        assert dt == z["dt"][step], step
+        assert sim.last_nsub == z["nsub"][step], step
+        assert sim.interaction_count == z["interactions"][step], step
+        assert sim.out_of_bounds == z["out_of_bounds"][step], step
+        if step % check_every == 0 or step == steps:
+            bad = mismatched(lambda f: by_id(reg.view(f), ids()), z, step,
+                             lambda f: reg.view(f))
+            assert not bad, (step, bad)
+    for s in z["full_steps"]:
+        if s == steps:
+            for f in FIELDS:
+                assert np.array_equal(by_id(reg.view(f), ids()), z[f"s{s}_{f}"]), f
+
+
+def test_engine_device_resident_run_matches_golden_without_pulls():
+    """No host pulls between steps: the device layout (fluid re-sorted every
+    step) is never re-pushed, yet every field matches at the end."""
+    tag = "dambreak2d_f32"
+    z = golden(f"traj_{tag}.npz")
+    reg, grid = case(tag)
+    sim = Simulation(reg, grid, CUDA)
+    sim.initialize()
+    for _ in range(201):
+        sim.advance()
+    bad = mismatched(lambda f: by_id(reg.view(f), reg.view("id")), z, 201,
+                     lambda f: reg.view(f))
+    assert not bad
+
+
+def _oracle_vs_engine(reg, grid, steps, **kw):
+    osim = O.OracleSim.from_registry(reg, grid, **kw)
+    sim = Simulation(reg, grid, CUDA, **kw)
+    osim.initialize()
+    sim.initialize()
+    assert sim.interaction_count == osim.interaction_count
+    for step in range(steps):
+        dt_o = osim.advance()
+        dt_g = sim.advance()
+        assert dt_g == dt_o, step
+        assert sim.last_nsub == osim.last_nsub
+        assert sim.interaction_count == osim.interaction_count
+        assert sim.out_of_bounds == osim.out_of_bounds
+    for f in FIELDS:
+        assert reg.view(f).tobytes() == osim.f[f].tobytes(), f
+
+
+def test_engine_vs_oracle_2d_fine():
+    cfg = cases.CaseConfig(case="dambreak2d", dp=0.008, precision="f32")
+    reg, grid = cases.build_case(cfg)
+    _oracle_vs_engine(reg, grid, 6)
+
+
+def test_engine_vs_oracle_3d_medium():
+    cfg = cases.kleefsman_config(dp=0.02, precision="f32")
+    reg, grid = cases.build_case(cfg)
+    _oracle_vs_engine(reg, grid, 3)
+
+
+def test_engine_vs_oracle_sort_and_shepard_cadence():
+    cfg = cases.CaseConfig(case="dambreak2d", dp=0.05, precision="f32")
+    reg, grid = cases.build_case(cfg)
+    _oracle_vs_engine(reg, grid, 25, sort_every=3, shepard_every=4)
+
+
+def test_engine_vs_oracle_hydrostatic_f64_fixed_dt():
+    cfg = cases.CaseConfig(case="hydrostatic", tank=(0.5, 0.6), column=(0.5, 0.5),
+                           dp=0.02, hydrostatic_init=True, precision="f64")
+    reg, grid = cases.build_case(cfg)
+    _oracle_vs_engine(reg, grid, 20, fixed_dt=2e-4)
+
+
+def test_engine_free_cloud_no_walls_and_clamped_particles():
+    """A wall-free cloud partly outside the grid (clamped, counted)."""
+    from paper_2603_11868_b200.neighborhood import UniformGrid
+    from paper_2603_11868_b200.physics import setup_state_variables
+    from paper_2603_11868_b200.variables import VariableRegistry
+    rng = np.random.default_rng(5)
+    n = 3000
+    reg = VariableRegistry(n, 2, dtype=np.float32)
+    setup_state_variables(reg)
+    reg.raw_view("x")[:] = rng.random((n, 2)) * 1.0
+    reg.raw_view("v")[:] = rng.normal(0, 0.3, (n, 2))
+    reg.raw_view("rho")[:] = 1000.0
+    reg.raw_view("m")[:] = 1000.0 * 0.02 ** 2
+    for k, val in (("rho0", 1000.0), ("c0", 20.0), ("h", 0.026), ("dp", 0.02),
+                   ("alpha_visc", 0.02)):
+        reg.register_singular(k, val)
+    reg.register_singular("g", np.array([0.0, -9.81]))
+    grid = UniformGrid.from_bounds((0.1, 0.1), (0.9, 0.9), 0.052)
+    _oracle_vs_engine(reg, grid, 5)
+
+
+def test_engine_stability_and_overflow_errors():
+    from paper_2603_11868_b200.neighborhood import UniformGrid
+    from paper_2603_11868_b200.physics import setup_state_variables
+    from paper_2603_11868_b200.variables import VariableRegistry
+    rng = np.random.default_rng(8)
+    n = 300
+    reg = VariableRegistry(n, 2, dtype=np.float32)
+    setup_state_variables(reg)
+    reg.raw_view("x")[:] = 0.5 + rng.random((n, 2)) * 1e-4
+    reg.raw_view("rho")[:] = 1000.0
+    reg.raw_view("m")[:] = 1.0
+    for k, val in (("rho0", 1000.0), ("c0", 20.0), ("h", 0.065), ("dp", 0.05),
+                   ("alpha_visc", 0.02)):
+        reg.register_singular(k, val)
+    reg.register_singular("g", np.array([0.0, 0.0]))
+    grid = UniformGrid.from_bounds((0.3, 0.3), (0.7, 0.7), 0.13)
+    sim = Simulation(reg, grid, CUDA)
+    with pytest.raises(NeighborOverflowError):
+        sim.initialize()
+    # absurd fixed dt -> instability (tests/test_harness.py:178-185 analogue)
+    cfg = cases.CaseConfig(case="dambreak2d", dp=0.05, precision="f32",
+                           fixed_dt=5.0)
+    reg2, grid2 = cases.build_case(cfg)
+    sim2 = Simulation(reg2, grid2, CUDA, fixed_dt=5.0)
+    sim2.initialize()
+    with pytest.raises(SimulationUnstableError):
+        for _ in range(5):
+            sim2.advance()
+
+
+def test_host_modification_between_steps_is_honoured():
+    cfg = cases.CaseConfig(case="dambreak2d", dp=0.05, precision="f32")
+    reg, grid = cases.build_case(cfg)
+    reg_o, _ = cases.build_case(cfg)
+    sim = Simulation(reg, grid, CUDA)
+    sim.initialize()
+    sim.advance()
+    reg.view("v")[:5] += np.float32(0.25)       # in-place host edit
+    osim = O.OracleSim.from_registry(reg, grid)
+    osim.st.step_count = sim.step_count
+    osim.st.time = sim.time
+    dt_g = sim.advance()
+    dt_o = osim.advance()
+    assert dt_g == dt_o
+    for f in ("x", "v", "rho", "p", "dvdt", "drho"):
+        assert reg.view(f).tobytes() == osim.f[f].tobytes(), f
+
+
+def test_compute_timestep_across_policies():
+    rng = np.random.default_rng(11)
+    cfg = cases.CaseConfig(case="dambreak2d", dp=0.05, precision="f64")
+    reg, grid = cases.build_case(cfg)
+    reg.view("v")[:] = rng.normal(0.0, 1.0, reg.view("v").shape)
+    reg.view("dvdt")[:] = rng.normal(0.0, 10.0, reg.view("dvdt").shape)
+    vals = {compute_timestep(p, reg, dt_max=1e-3)
+            for p in (P.ExecutionPolicy.sequenced(), P.ExecutionPolicy.parallel(4), CUDA)}
+    assert len(vals) == 1
+    vm = O.vmax(reg.view("v"))
+    am = O.vmax(reg.view("dvdt"))
+    from paper_2603_11868_b200.physics import timestep_formula
+    assert vals.pop() == timestep_formula(vm, am, float(reg.singular("h")),
+                                          float(reg.singular("c0")), 1e-3)
