@@ -251,7 +251,7 @@ __global__ void k_ref_assign(const uint32_t* __restrict__ phys_sorted, int64_t n
 
 // fused gather of every per-particle field of the fluid segment by perm
 template <class T>
-__global__ void k_fluid_gather(const uint32_t* __restrict__ perm, int64_t nf,
+__global__ void k_fluid_gather(const uint32_t* __restrict__ perm, int64_t nf, int64_t n,
                                const vec4<T>* __restrict__ pos, vec4<T>* __restrict__ pos_o,
                                const vec4<T>* __restrict__ vel, vec4<T>* __restrict__ vel_o,
                                const vec2<T>* __restrict__ rp, vec2<T>* __restrict__ rp_o,
@@ -263,7 +263,12 @@ __global__ void k_fluid_gather(const uint32_t* __restrict__ perm, int64_t nf,
                                const uint32_t* __restrict__ nnb, uint32_t* __restrict__ nnb_o)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nf) return;
+    if (i >= nf) {
+        // walls: the (rho, p) buffer becoming current must carry the walls'
+        // latest wall-pressure values (velocity buffers agree on walls)
+        if (i < n) rp_o[i] = rp[i];
+        return;
+    }
     uint32_t r = perm[i];
     pos_o[i] = pos[r];
     vel_o[i] = vel[r];
@@ -691,8 +696,8 @@ static int rebuild_impl(SphEngine* e, cudaStream_t s)
     const uint32_t* sk = which ? sb.k1 : sb.k0;
     const uint32_t* perm = which ? sb.v1 : sb.v0;
     const int cv = e->cur_v, crp = e->cur_rp;
-    note_launch(), k_fluid_gather<T><<<grid_for(nf, 256), 256, 0, s>>>(
-        perm, nf, E.pos, pos_o, E.vel[cv], E.vel[cv ^ 1], E.rp[crp], E.rp[crp ^ 1], E.dvdt,
+    note_launch(), k_fluid_gather<T><<<grid_for(e->n, 256), 256, 0, s>>>(
+        perm, nf, e->n, E.pos, pos_o, E.vel[cv], E.vel[cv ^ 1], E.rp[crp], E.rp[crp ^ 1], E.dvdt,
         dvdt_o, E.drho, drho_o, E.id, id_o, E.refpos, ref_o, E.nnb, nnb_o);
     // the gathered fluid prefix goes back into the primary arrays; the wall
     // suffix there is untouched (walls never move)
@@ -703,7 +708,7 @@ static int rebuild_impl(SphEngine* e, cudaStream_t s)
     cudaMemcpyAsync(e->id, id_o, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(e->refpos, ref_o, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(e->nnb, nnb_o, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, s);
-    // walls of the other vel/rp buffers already equal the current ones
+    // velocity buffers agree on the (never moving) walls
     e->cur_v = cv ^ 1;
     e->cur_rp = crp ^ 1;
     note_launch(), k_seg_offsets<<<grid_for(e->ncells + 1, 256), 256, 0, s>>>(sk, nf, e->ncells, 0u, e->offs_f);

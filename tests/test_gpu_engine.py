@@ -150,15 +150,28 @@ def test_engine_stability_and_overflow_errors():
     sim = Simulation(reg, grid, CUDA)
     with pytest.raises(NeighborOverflowError):
         sim.initialize()
-    # absurd fixed dt -> instability (tests/test_harness.py:178-185 analogue)
-    cfg = cases.CaseConfig(case="dambreak2d", dp=0.05, precision="f32",
-                           fixed_dt=5.0)
+    # absurd fixed dt -> instability (tests/test_harness.py:178-185): the
+    # engine aborts at the same step, with the same check, as the oracle
+    cfg = cases.CaseConfig(case="dambreak2d", dp=0.05, precision="f32")
     reg2, grid2 = cases.build_case(cfg)
-    sim2 = Simulation(reg2, grid2, CUDA, fixed_dt=5.0)
+    osim = O.OracleSim.from_registry(reg2, grid2, fixed_dt=0.05)
+    sim2 = Simulation(reg2, grid2, CUDA, fixed_dt=0.05)
+    osim.initialize()
     sim2.initialize()
-    with pytest.raises(SimulationUnstableError):
-        for _ in range(5):
+    o_fail = g_fail = None
+    for step in range(20):
+        try:
+            osim.advance()
+        except O.OracleError as exc:
+            o_fail = (step, exc.code)
+        try:
             sim2.advance()
+        except SimulationUnstableError as exc:
+            g_fail = (step, 2 if "density" in str(exc) else 3)
+        assert (o_fail is None) == (g_fail is None), (o_fail, g_fail)
+        if o_fail:
+            break
+    assert o_fail == g_fail and o_fail is not None
 
 
 def test_host_modification_between_steps_is_honoured():
