@@ -41,7 +41,7 @@ CONFIGS = {
 }
 METRIC = "particle-updates/sec (full time step)"
 UNIT = "particle-updates/s"
-SUBSTEP_KERNELS = ("kick_drift", "build_lists", "continuity_du", "wall_pressure",
+SUBSTEP_KERNELS = ("kick_drift", "list_filter", "continuity_du", "wall_pressure",
                    "momentum_kick")
 
 
@@ -71,8 +71,8 @@ def kernel_bytes(name, d, nf, nw, nnb_f, nnb_w, nnb_wf):
     neighbour data is assumed cache-resident (SURVEY.md section 8d model)."""
     if name == "kick_drift":       # read x v a, write x v
         return nf * 20 * d
-    if name == "build_lists":      # read x,id of i; write 4 B per entry + count
-        return (nf + nw) * (4 * d + 8) + 4 * (nnb_f + nnb_wf)
+    if name == "list_filter":      # read x, cell0, disp, counts, list; write mask, count
+        return (nf + nw) * (4 * d + 4 + 4 + 4 + 4 + 4 + 4) + 4 * (nnb_f + nnb_wf)
     if name == "continuity_du":    # read x v rho m + list, write drho rho p
         return nf * (8 * d + 8 + 4 + 12) + 4 * nnb_f
     if name == "wall_pressure":    # read x + list, write rho p nnb drho

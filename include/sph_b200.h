@@ -166,10 +166,11 @@ typedef struct {
     unsigned long long interactions;  /* report.py:20-21 directed visits       */
     unsigned long long rho_min_key;   /* order-preserving key of min rho (f64) */
     unsigned long long v2max_key;     /* key of max run-precision |v|^2        */
+    unsigned long long dmax_bits;     /* max path length since the skin build  */
     unsigned int overflow;            /* particles over NEIGHBOR_CAPACITY      */
     unsigned int oob;                 /* fluid out-of-bounds clamps            */
     unsigned int oob_walls;           /* wall clamps (counted once, at push)   */
-    unsigned int nfix;                /* skin-list fallbacks                   */
+    unsigned int nfix;                /* exact list rebuilds (skin fallbacks)  */
     unsigned int nan_flags;           /* bit0: a NaN rho, bit1: a NaN |v|^2    */
     unsigned int reserved;
 } SphStepStats;
@@ -185,18 +186,24 @@ typedef struct {
     void* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; void* vol_id;
     /* cell offsets into each segment (dev, ncells+1 each) */
     uint32_t* offs_f; uint32_t* offs_w;
-    /* ordered neighbour lists: tile-ELL [n_slots/32][256][32] int32 + counts */
-    int32_t* lists; int32_t* lcount;
+    /* ascending-id neighbour lists, tile-ELL [slots/32][256][32] int32, and
+     * per slot: entries (lcount), exact accepted count this sub-step or -1
+     * (acount), static wall-wall count of walls (nww); 256-bit exact-filter
+     * masks [slots/32][8][32]; per particle: list cell (cell0) and path
+     * length since the list build (disp, run precision); fix-up queue */
+    int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; uint32_t* mask;
+    uint32_t* cell0; void* disp; uint32_t* queue; uint32_t* qcount;
     /* scratch (dev): keys/values x2 for the radix sort + gather staging */
     void* ws; size_t ws_bytes;
     SphStepStats* stats;              /* dev */
     /* physics scalars (run precision, passed as double for both runs) */
     double g[3]; double origin[3]; int64_t shape[3];
     double cell_size, cutoff, h, alpha_d, c0, rho0, alpha_visc, eps_h2;
-    /* double-buffer selectors, maintained by the library */
+    double skin;                      /* Verlet skin of the current lists    */
+    /* double-buffer selectors and list state, maintained by the library */
     int32_t cur_v, cur_rp;
     int32_t f64;                      /* 0: f32 run, 1: f64 run */
-    int32_t reserved;
+    int32_t lists_ready;
 } SphEngine;
 
 size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64);
@@ -214,6 +221,13 @@ int sph_engine_pull(const SphEngine* e, void* x, void* v, void* rho, void* p, vo
 int sph_engine_rebuild_cll(SphEngine* e, cudaStream_t s);
 /* sorting.py:84-87 sort_particles_by_cell, tracked for the registry mirror */
 int sph_engine_ref_sort(SphEngine* e, cudaStream_t s);
+/* Verlet skin lists for the step (after every rebuild): for each particle the
+ * ascending-id list of CLL-block neighbours within cutoff + skin of its
+ * current position; resets the displacement bounds.  Every later sweep
+ * filters them exactly (0 < r2 < cutoff^2 on current positions) and falls
+ * back to an exact rebuild for a particle whose cell changed or whose
+ * displacement bound exceeds the skin, so results are the reference's. */
+int sph_engine_build_lists(SphEngine* e, double skin, cudaStream_t s);
 /* physics.py:460-467 initialize: wall pressure + momentum + counts */
 int sph_engine_initialize(SphEngine* e, cudaStream_t s);
 /* physics.py:469-487 _shepard_filter (SHEPARD, COPY_SCALAR, DENSITY_UPDATE) */

@@ -62,7 +62,7 @@ class SphStepStats(C.Structure):
     _fields_ = [
         ("vmax_bits", C.c_uint64), ("amax_bits", C.c_uint64),
         ("interactions", C.c_uint64), ("rho_min_key", C.c_uint64),
-        ("v2max_key", C.c_uint64),
+        ("v2max_key", C.c_uint64), ("dmax_bits", C.c_uint64),
         ("overflow", C.c_uint32), ("oob", C.c_uint32),
         ("oob_walls", C.c_uint32), ("nfix", C.c_uint32),
         ("nan_flags", C.c_uint32), ("reserved", C.c_uint32),
@@ -78,13 +78,15 @@ class SphEngine(C.Structure):
         ("id", P), ("nnb", P), ("refpos", P),
         ("rho_scratch_id", P), ("oflow_id", P), ("wall_id", P), ("vol_id", P),
         ("offs_f", P), ("offs_w", P),
-        ("lists", P), ("lcount", P),
+        ("lists", P), ("lcount", P), ("acount", P), ("nww", P), ("mask", P),
+        ("cell0", P), ("disp", P), ("queue", P), ("qcount", P),
         ("ws", P), ("ws_bytes", c_size),
         ("stats", P),
         ("g", c_f64 * 3), ("origin", c_f64 * 3), ("shape", c_i64 * 3),
         ("cell_size", c_f64), ("cutoff", c_f64), ("h", c_f64), ("alpha_d", c_f64),
         ("c0", c_f64), ("rho0", c_f64), ("alpha_visc", c_f64), ("eps_h2", c_f64),
-        ("cur_v", c_i32), ("cur_rp", c_i32), ("f64", c_i32), ("reserved", c_i32),
+        ("skin", c_f64),
+        ("cur_v", c_i32), ("cur_rp", c_i32), ("f64", c_i32), ("lists_ready", c_i32),
     ]
 
 
@@ -109,6 +111,7 @@ _PROTOS = {
     "sph_engine_rebuild_cll": (c_i32, [_P, _P]),
     "sph_engine_ref_sort": (c_i32, [_P, _P]),
     "sph_engine_initialize": (c_i32, [_P, _P]),
+    "sph_engine_build_lists": (c_i32, [_P, c_f64, _P]),
     "sph_engine_shepard": (c_i32, [_P, _P]),
     "sph_engine_substep": (c_i32, [_P, c_f64, c_f64, _P]),
     "sph_engine_substep_timed": (c_i32, [_P, c_f64, c_f64, _P, _P]),

@@ -1,0 +1,125 @@
+// engine.cuh -- shared view of the device-resident engine state (SphEngine).
+//
+// Layout in HBM: particles in two segments, fluid [0, nf) and walls [nf, n),
+// each ordered by grid cell.  Structure of arrays with packed vectors so a
+// neighbour costs three 16/8-byte loads:
+//   pos  vec4 (x, y, z, m)          -- drift updates x in place
+//   vel  vec4 x2 (double buffer)    -- kick2 writes the other buffer
+//   rp   vec2 (rho, p) x2           -- continuity+density update writes the
+//                                      other buffer, walls follow
+//   dvdt vec4, drho, id, nnb, refpos (registry position of each particle)
+// Cold per-particle fields no kernel reads per pair (rho_scratch, oflow,
+// wall, Vol) are stored BY ORIGINAL ID, so re-sorting never moves them.
+#pragma once
+
+#include "common.cuh"
+#include "internal.cuh"
+#include "nlist.cuh"
+#include "physics.cuh"
+
+namespace sph {
+
+constexpr int kSweepThreads = 128;
+constexpr uint32_t kInvalidCell = 0xffffffffu;   // list is not a valid skin list
+
+template <class T>
+struct Eng {
+    int64_t n, nf, nw, nf_pad;
+    vec4<T>* pos; vec4<T>* vel[2]; vec2<T>* rp[2]; vec4<T>* dvdt; T* drho;
+    uint32_t* id; uint32_t* nnb; uint32_t* refpos;
+    T* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; T* vol_id;
+    uint32_t* offs_f; uint32_t* offs_w;
+    int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; uint32_t* mask;
+    uint32_t* cell0; T* disp; uint32_t* queue; uint32_t* qcount;
+    SphStepStats* stats;
+};
+
+template <class T>
+inline Eng<T> eng_of(const SphEngine* e)
+{
+    Eng<T> g;
+    g.n = e->n; g.nf = e->nf; g.nw = e->n - e->nf; g.nf_pad = (e->nf + 31) / 32 * 32;
+    g.pos = (vec4<T>*)e->pos;
+    g.vel[0] = (vec4<T>*)e->vel[0]; g.vel[1] = (vec4<T>*)e->vel[1];
+    g.rp[0] = (vec2<T>*)e->rp[0]; g.rp[1] = (vec2<T>*)e->rp[1];
+    g.dvdt = (vec4<T>*)e->dvdt; g.drho = (T*)e->drho;
+    g.id = e->id; g.nnb = e->nnb; g.refpos = e->refpos;
+    g.rho_scratch_id = (T*)e->rho_scratch_id; g.oflow_id = e->oflow_id;
+    g.wall_id = e->wall_id; g.vol_id = (T*)e->vol_id;
+    g.offs_f = e->offs_f; g.offs_w = e->offs_w;
+    g.lists = e->lists; g.lcount = e->lcount; g.acount = e->acount; g.nww = e->nww;
+    g.mask = e->mask; g.cell0 = e->cell0; g.disp = (T*)e->disp; g.queue = e->queue;
+    g.qcount = e->qcount; g.stats = e->stats;
+    return g;
+}
+
+inline PhysP phys_of_engine(const SphEngine* e)
+{
+    PhysP P;
+    P.cell_size = e->cell_size; P.cutoff = e->cutoff; P.h = e->h; P.alpha_d = e->alpha_d;
+    P.c0 = e->c0; P.rho0 = e->rho0; P.alpha_visc = e->alpha_visc; P.eps_h2 = e->eps_h2;
+    P.g[0] = e->g[0]; P.g[1] = e->g[1]; P.g[2] = e->dim == 3 ? e->g[2] : 0.0;
+    return P;
+}
+
+template <class T>
+inline GridP<T> grid_of_engine(const SphEngine* e)
+{
+    GridP<T> g;
+    for (int k = 0; k < 3; k++) {
+        g.o[k] = k < e->dim ? T(e->origin[k]) : T(0);
+        g.s[k] = k < e->dim ? (int)e->shape[k] : 1;
+    }
+    g.cs = T(e->cell_size);
+    const T c = T(e->cutoff);
+    g.c2 = c * c;   // binary32 product in the f32 run (neighborhood.py:185)
+    return g;
+}
+
+template <class T>
+inline EngAcc<T> acc_of_engine(const SphEngine* e)
+{
+    EngAcc<T> acc;
+    acc.pos = (const vec4<T>*)e->pos;
+    acc.id = e->id;
+    acc.offs_f = e->offs_f;
+    acc.offs_w = e->offs_w;
+    acc.nf = e->nf;
+    return acc;
+}
+
+// list slot of particle i (walls start on a fresh 32-particle tile)
+template <class T>
+__device__ __forceinline__ int64_t slot_of(const Eng<T>& E, int64_t i)
+{
+    return i < E.nf ? i : E.nf_pad + (i - E.nf);
+}
+
+template <class T>
+__device__ __forceinline__ void to3(const vec4<T>& v, T (&o)[3])
+{
+    o[0] = v.x; o[1] = v.y; o[2] = v.z;
+}
+
+__device__ __forceinline__ void add_interactions(SphStepStats* st, unsigned long long c)
+{
+    c = warp_sum(c);
+    if (lane_id() == 0 && c) atomicAdd(&st->interactions, c);
+}
+
+inline int engine_validate(const SphEngine* e)
+{
+    if (!e || (e->dim != 2 && e->dim != 3) || e->n < 0 || e->nf < 0 || e->nf > e->n)
+        return SPH_ERR_INVALID;
+    if (e->ncells + 1 >= (int64_t)INT32_MAX || e->key_bits > 30 || e->n >= (int64_t)INT32_MAX) {
+        set_error("engine: grid or particle count too large for 32-bit keys");
+        return SPH_ERR_UNSUPPORTED;
+    }
+    return SPH_OK;
+}
+
+#define SPH_DISPATCH(e, FN, ...)                                                              \
+    ((e)->f64 ? ((e)->dim == 3 ? FN<double, 3>(__VA_ARGS__) : FN<double, 2>(__VA_ARGS__))     \
+              : ((e)->dim == 3 ? FN<float, 3>(__VA_ARGS__) : FN<float, 2>(__VA_ARGS__)))
+
+}  // namespace sph

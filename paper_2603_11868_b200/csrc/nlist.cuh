@@ -6,15 +6,21 @@
 // with 0 < r2 < cutoff^2, and visits them in ascending ORIGINAL id.  That
 // order fixes every floating-point accumulation, so it is reproduced exactly.
 //
-// B200 mapping: one warp per particle.  The block's row-major cell keys make
-// each (ax, ay) column of the block one contiguous key range (3 ranges in
-// 2D, 9 in 3D), i.e. one contiguous run of the cell-sorted particle array
-// per segment; lanes test 32 candidates per step, survivors are compacted by
-// ballot into a per-warp shared buffer of packed (id << 32 | j), sorted by a
-// warp bitonic network (registers for <= 32 survivors, shared memory above),
-// then staged so the block writes its 32-particle tile of lists coalesced in
-// a tile-ELL layout: lists[tile][t][lane].  The thread-per-particle sweeps
-// then read entry t of 32 consecutive particles as one 128-byte line.
+// B200 mapping: one warp per particle.  Row-major cell keys make each (ax,
+// ay) column of the block one contiguous key range (3 in 2D, 9 in 3D), i.e.
+// one contiguous run of the cell-sorted particle array per segment.  All
+// run bounds are fetched in one round trip (one lane per run), a warp scan
+// flattens the runs into one candidate index space, and every 32-candidate
+// step finds its run with a 5-step shuffle binary search -- so a particle
+// costs two dependent memory round trips plus one per 32 candidates, not two
+// per run.  Survivors are compacted by ballot into a per-warp shared buffer
+// of packed (id << 32 | j) and sorted by a warp bitonic network (registers
+// for <= 32 survivors, shared memory above).
+//
+// Two acceptance modes:
+//   exact: 0 < r2 < cutoff^2 (the reference's test), and
+//   skin:  r2 < (cutoff + skin)^2 -- a Verlet superset built once per
+//          advective step; engine.cu filters it exactly every sub-step.
 #pragma once
 
 #include "common.cuh"
@@ -26,19 +32,26 @@ constexpr int kNlWarps = 8;
 constexpr int kNlThreads = kNlWarps * 32;
 constexpr int kStagePitch = 33;   // conflict-free transposition
 constexpr size_t kNlSmem = sizeof(int32_t) * kCap * kStagePitch +
-                           sizeof(unsigned long long) * kNlWarps * kCap + sizeof(int) * 32;
+                           sizeof(unsigned long long) * kNlWarps * kCap + sizeof(int) * 64;
+constexpr int kMaskWords = kCap / 32;   // 256-bit filter mask per particle
 
 template <class T>
 struct GridP {
     T o[3]; T cs; T c2; int s[3];
 };
 
+// tile-ELL: entry t of slot s at [s/32][t][s%32]
 __device__ __forceinline__ size_t ell_index(int64_t slot, int t)
 {
     return (size_t)(slot >> 5) * (kCap * 32) + (size_t)t * 32 + (size_t)(slot & 31);
 }
+// filter-mask word w of slot s at [s/32][w][s%32]
+__device__ __forceinline__ size_t mask_index(int64_t slot, int w)
+{
+    return (size_t)(slot >> 5) * (kMaskWords * 32) + (size_t)w * 32 + (size_t)(slot & 31);
+}
 
-// ascending bitonic sort of sb[0..np), np a power of two in [32, 256]
+// ascending bitonic sort of sb[0..np), np a power of two in [64, 256]
 __device__ __forceinline__ void warp_bitonic_smem(unsigned long long* sb, int np, unsigned lane)
 {
     for (int k = 2; k <= np; k <<= 1) {
@@ -66,12 +79,30 @@ __device__ __forceinline__ unsigned long long warp_bitonic_reg(unsigned long lon
             unsigned long long o = __shfl_xor_sync(0xffffffffu, v, j);
             bool up = (lane & k) == 0;
             bool lower = (lane & j) == 0;
-            bool take_min = (lower == up);
             unsigned long long mn = o < v ? o : v, mx = o < v ? v : o;
-            v = take_min ? mn : mx;
+            v = (lower == up) ? mn : mx;
         }
     }
     return v;
+}
+
+// Sort sb[0..n) ascending (n <= kCap) in place; the warp must be converged.
+__device__ __forceinline__ void warp_sort_packed(unsigned long long* sb, int n, unsigned lane)
+{
+    __syncwarp();
+    if (n <= 32) {
+        unsigned long long v = lane < (unsigned)n ? sb[lane] : ~0ull;
+        v = warp_bitonic_reg(v, lane);
+        __syncwarp();
+        if (lane < (unsigned)n) sb[lane] = v;
+    } else {
+        int np = 64;
+        while (np < n) np <<= 1;
+        for (int k = n + lane; k < np; k += 32) sb[k] = ~0ull;
+        __syncwarp();
+        warp_bitonic_smem(sb, np, lane);
+    }
+    __syncwarp();
 }
 
 // Engine layout: segment 0 = fluid [0, nf), segment 1 = walls [nf, n); each
@@ -84,7 +115,6 @@ struct EngAcc {
     const uint32_t* __restrict__ offs_f;
     const uint32_t* __restrict__ offs_w;
     int64_t nf;
-    bool store_walls;   // walls' own lists keep fluid neighbours only
     __device__ __forceinline__ void position(int64_t j, T (&x)[3]) const
     {
         vec4<T> p = pos[j];
@@ -97,7 +127,6 @@ struct EngAcc {
         if (seg == 0) { s0 = offs_f[klo]; s1 = offs_f[khi + 1]; }
         else { s0 = nf + offs_w[klo]; s1 = nf + offs_w[khi + 1]; }
     }
-    __device__ __forceinline__ bool store(int seg) const { return seg == 0 || store_walls; }
     __device__ __forceinline__ int64_t cand(int64_t s) const { return s; }
 };
 
@@ -119,12 +148,126 @@ struct GenAcc {
     {
         s0 = offsets[klo]; s1 = offsets[khi + 1];
     }
-    __device__ __forceinline__ bool store(int) const { return true; }
     __device__ __forceinline__ int64_t cand(int64_t s) const { return pids[s]; }
 };
 
-// Build the ordered lists of particles first .. first+count-1 into slots
-// slot_first .. (slot_first % 32 == 0).  lcount[slot] = stored count, or -1
+// cell of a position and its row-major key (neighborhood.py:76-84, 112-116)
+template <class T, int D>
+__device__ __forceinline__ uint32_t cell_key_of(const T (&x)[3], const GridP<T>& g, int (&c)[3])
+{
+    int cl = 0;
+    c[0] = cell_coord<T>(x[0], g.o[0], g.cs, g.s[0], cl);
+    c[1] = cell_coord<T>(x[1], g.o[1], g.cs, g.s[1], cl);
+    c[2] = D == 3 ? cell_coord<T>(x[2], g.o[2], g.cs, g.s[2], cl) : 0;
+    uint32_t k = (uint32_t)c[0] * g.s[1] + c[1];
+    if (D == 3) k = k * g.s[2] + c[2];
+    return k;
+}
+
+struct CollectCounts {
+    int stored;     // packed entries written to sb (may exceed kCap: overflow)
+    int accepted;   // exact-test accepted neighbours over ALL segments
+};
+
+// Collect the neighbours of particle i (position xi) into sb.
+//   SKIN == false: store j of storing segments with 0 < r2 < c2;
+//   SKIN == true : store j of storing segments with r2 < cs2 (a superset).
+// `accepted` counts exact-test neighbours of every segment (the reference's
+// capacity count); with SKIN it counts only the non-storing segments.
+// store_mask bit s: segment s is stored.
+template <class T, int D, bool SKIN, class Acc>
+__device__ __forceinline__ CollectCounts warp_collect(const Acc& acc, const GridP<T>& g,
+                                                      int64_t i, const T (&xi)[3], T cs2,
+                                                      unsigned store_mask,
+                                                      unsigned long long* sb)
+{
+    const unsigned lane = lane_id();
+    const unsigned lt = lanemask_lt();
+    int c[3];
+    cell_key_of<T, D>(xi, g, c);
+    const int xlo = max(c[0] - 1, 0), xhi = min(c[0] + 1, g.s[0] - 1);
+    const int ylo = max(c[1] - 1, 0), yhi = min(c[1] + 1, g.s[1] - 1);
+    const int zlo = D == 3 ? max(c[2] - 1, 0) : 0, zhi = D == 3 ? min(c[2] + 1, g.s[2] - 1) : 0;
+    const int nxr = xhi - xlo + 1;
+    const int nyr = D == 3 ? (yhi - ylo + 1) : 1;
+    const int runs_per_seg = nxr * nyr;
+    const int nruns = runs_per_seg * Acc::kSegs;
+    // lane r < nruns owns run r: (seg, ax, ay) -> candidate range [s0, s1)
+    int64_t s0 = 0, s1 = 0;
+    int seg = 0;
+    if ((int)lane < nruns) {
+        seg = (int)lane / runs_per_seg;
+        const int rr = (int)lane - seg * runs_per_seg;
+        const int ax = xlo + rr / nyr, ay = ylo + rr % nyr;
+        uint32_t klo, khi;
+        if (D == 3) {
+            const uint32_t rowk = ((uint32_t)ax * g.s[1] + ay) * g.s[2];
+            klo = rowk + zlo;
+            khi = rowk + zhi;
+        } else {
+            klo = (uint32_t)ax * g.s[1] + ylo;
+            khi = (uint32_t)ax * g.s[1] + yhi;
+        }
+        acc.run(seg, klo, khi, s0, s1);
+    }
+    // flatten: exclusive prefix of run lengths
+    uint32_t len = (uint32_t)(s1 - s0);
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += t;
+    }
+    const uint32_t start = incl - len;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    CollectCounts out{0, 0};
+    for (uint32_t base = 0; base < total; base += 32) {
+        const uint32_t idx = base + lane;
+        // largest run r with start_r <= idx (empty runs tie to the later run)
+        int r = 0;
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const int cand = r + step;
+            const uint32_t sv = __shfl_sync(0xffffffffu, start, cand & 31);
+            if (cand < nruns && sv <= idx) r = cand;
+        }
+        const int64_t rs0 = __shfl_sync(0xffffffffu, s0, r);
+        const uint32_t rstart = __shfl_sync(0xffffffffu, start, r);
+        const int rseg = __shfl_sync(0xffffffffu, seg, r);
+        bool ok_store = false, ok_count = false;
+        int64_t j = 0;
+        if (idx < total) {
+            j = acc.cand(rs0 + (idx - rstart));
+            if (j != i) {
+                T xj[3];
+                acc.position(j, xj);
+                const T r2 = accept_r2<T, D>(xi, xj);
+                const bool exact = (r2 < g.c2) && (r2 > T(0));
+                const bool stores = (store_mask >> rseg) & 1u;
+                if (SKIN) {
+                    ok_store = stores && (r2 < cs2);
+                    ok_count = !stores && exact;
+                } else {
+                    ok_store = stores && exact;
+                    ok_count = exact;
+                }
+            }
+        }
+        const unsigned bs = __ballot_sync(0xffffffffu, ok_store);
+        if (ok_store) {
+            const int p = out.stored + __popc(bs & lt);
+            if (p < kCap)
+                sb[p] = ((unsigned long long)acc.idof(j) << 32) | (unsigned long long)(uint32_t)j;
+        }
+        out.stored += __popc(bs);
+        out.accepted += __popc(__ballot_sync(0xffffffffu, ok_count));
+    }
+    return out;
+}
+
+// Build exact ordered lists of particles first .. first+count-1 into slots
+// slot_first .. (slot_first % 32 == 0), staged per 32-particle tile so the
+// block writes lists[tile][t][lane] coalesced.  lcount[slot] = count, or -1
 // when more than kCap neighbours qualify (neighborhood.py:200-202).
 template <class T, int D, class Acc>
 __global__ void __launch_bounds__(kNlThreads)
@@ -138,7 +281,6 @@ k_build_lists(const Acc acc, const GridP<T> g, int64_t first, int64_t count,
     int* scnt = reinterpret_cast<int*>(sbuf_all + kNlWarps * kCap);
 
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    const unsigned lt = lanemask_lt();
     unsigned long long* sb = sbuf_all + warp * kCap;
     const int64_t t0 = (int64_t)blockIdx.x * 32;
 
@@ -151,83 +293,16 @@ k_build_lists(const Acc acc, const GridP<T> g, int64_t first, int64_t count,
         const int64_t i = first + t;
         T xi[3];
         acc.position(i, xi);
-        int cl = 0;
-        const int cx = cell_coord<T>(xi[0], g.o[0], g.cs, g.s[0], cl);
-        const int cy = cell_coord<T>(xi[1], g.o[1], g.cs, g.s[1], cl);
-        const int xlo = max(cx - 1, 0), xhi = min(cx + 1, g.s[0] - 1);
-        const int ylo = max(cy - 1, 0), yhi = min(cy + 1, g.s[1] - 1);
-        int zlo = 0, zhi = 0;
-        if (D == 3) {
-            const int cz = cell_coord<T>(xi[2], g.o[2], g.cs, g.s[2], cl);
-            zlo = max(cz - 1, 0);
-            zhi = min(cz + 1, g.s[2] - 1);
-        }
-        int n_tot = 0, n_st = 0;
-        for (int ax = xlo; ax <= xhi; ax++) {
-            const int ay_end = D == 3 ? yhi : ylo;   // 2D: one key range per ax
-            for (int ay = ylo; ay <= ay_end; ay++) {
-                uint32_t klo, khi;
-                if (D == 3) {
-                    uint32_t rowk = ((uint32_t)ax * g.s[1] + ay) * g.s[2];
-                    klo = rowk + zlo;
-                    khi = rowk + zhi;
-                } else {
-                    klo = (uint32_t)ax * g.s[1] + ylo;
-                    khi = (uint32_t)ax * g.s[1] + yhi;
-                }
-#pragma unroll
-                for (int seg = 0; seg < Acc::kSegs; seg++) {
-                    int64_t s0, s1;
-                    acc.run(seg, klo, khi, s0, s1);
-                    const bool st = acc.store(seg);
-                    for (int64_t sbase = s0; sbase < s1; sbase += 32) {
-                        const int64_t sidx = sbase + lane;
-                        bool ok = false;
-                        int64_t j = 0;
-                        if (sidx < s1) {
-                            j = acc.cand(sidx);
-                            if (j != i) {
-                                T xj[3];
-                                acc.position(j, xj);
-                                T r2 = accept_r2<T, D>(xi, xj);
-                                ok = (r2 < g.c2) && (r2 > T(0));
-                            }
-                        }
-                        const unsigned b = __ballot_sync(0xffffffffu, ok);
-                        if (st) {
-                            if (ok) {
-                                int pos = n_st + __popc(b & lt);
-                                if (pos < kCap)
-                                    sb[pos] = ((unsigned long long)acc.idof(j) << 32) |
-                                              (unsigned long long)(uint32_t)j;
-                            }
-                            n_st += __popc(b);
-                        }
-                        n_tot += __popc(b);
-                    }
-                }
-            }
-        }
-        if (n_tot > kCap) {
+        CollectCounts cc = warp_collect<T, D, false>(acc, g, i, xi, T(0), 1u, sb);
+        if (cc.accepted > kCap) {
             if (lane == 0) scnt[p] = -1;
             __syncwarp();
             continue;
         }
-        __syncwarp();
-        if (n_st <= 32) {
-            unsigned long long v = lane < (unsigned)n_st ? sb[lane] : ~0ull;
-            v = warp_bitonic_reg(v, lane);
-            if (lane < (unsigned)n_st) stage[lane * kStagePitch + p] = (int32_t)(uint32_t)v;
-        } else {
-            int np = 64;
-            while (np < n_st) np <<= 1;
-            for (int k = n_st + lane; k < np; k += 32) sb[k] = ~0ull;
-            __syncwarp();
-            warp_bitonic_smem(sb, np, lane);
-            for (int k = lane; k < n_st; k += 32)
-                stage[k * kStagePitch + p] = (int32_t)(uint32_t)sb[k];
-        }
-        if (lane == 0) scnt[p] = n_st;
+        warp_sort_packed(sb, cc.stored, lane);
+        for (int k = lane; k < cc.stored; k += 32)
+            stage[k * kStagePitch + p] = (int32_t)(uint32_t)sb[k];
+        if (lane == 0) scnt[p] = cc.stored;
         __syncwarp();
     }
     __syncthreads();
@@ -247,16 +322,11 @@ inline int launch_build_lists(const Acc& acc, const GridP<T>& g, int64_t first, 
                               cudaStream_t s)
 {
     if (count <= 0) return 0;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_build_lists<T, D, Acc>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kNlSmem);
-        attr_set = true;
-    }
+    cudaFuncSetAttribute(k_build_lists<T, D, Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kNlSmem);
     int64_t tiles = (count + 31) / 32;
-    note_launch(), k_build_lists<T, D, Acc><<<(unsigned)tiles, kNlThreads, kNlSmem, s>>>(acc, g, first, count,
-                                                                          slot_first, lists,
-                                                                          lcount);
+    note_launch(), k_build_lists<T, D, Acc><<<(unsigned)tiles, kNlThreads, kNlSmem, s>>>(
+        acc, g, first, count, slot_first, lists, lcount);
     return 0;
 }
 

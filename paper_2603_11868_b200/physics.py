@@ -387,7 +387,7 @@ def setup_state_variables(registry):
 
 # -- device-resident driver ----------------------------------------------------
 
-SUBSTEP_KERNELS = ("kick_drift", "build_lists", "continuity_du", "wall_pressure",
+SUBSTEP_KERNELS = ("kick_drift", "list_filter", "continuity_du", "wall_pressure",
                    "momentum_kick")
 
 _ENGINE_FIELDS = ("x", "v", "rho", "p", "m", "Vol", "drho", "dvdt",
@@ -443,6 +443,8 @@ class Simulation:
         self._norms = None          # (vmax, amax) valid for the device state
         self._oob_walls = 0
         self.kernel_times = None    # dict name -> [ms per launch] when profiling
+        self._skin_factor = 3.0
+        self.last_nfix = 0
         registry.attach_engine(self)
 
     # -- registry coupling ----------------------------------------------------
@@ -517,7 +519,16 @@ class Simulation:
         T["offs_w"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
         T["lists"] = torch.empty((max(tiles, 1), NEIGHBOR_CAPACITY, 32), dtype=i32,
                                  device=dev)
-        T["lcount"] = torch.empty((max(tiles, 1) * 32,), dtype=i32, device=dev)
+        slots = max(tiles, 1) * 32
+        T["lcount"] = torch.empty((slots,), dtype=i32, device=dev)
+        T["acount"] = torch.empty((slots,), dtype=i32, device=dev)
+        T["nww"] = torch.empty((slots,), dtype=i32, device=dev)
+        T["mask"] = torch.empty((max(tiles, 1), NEIGHBOR_CAPACITY // 32, 32), dtype=i32,
+                                device=dev)
+        T["cell0"] = torch.empty((max(n, 1),), dtype=i32, device=dev)
+        T["disp"] = torch.empty((max(n, 1),), dtype=tdt, device=dev)
+        T["queue"] = torch.empty((max(n, 1),), dtype=i32, device=dev)
+        T["qcount"] = torch.zeros((4,), dtype=i32, device=dev)
         ws_bytes = lib.sph_engine_workspace_bytes(n, ncells, int(f64))
         T["ws"] = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
         T["stats"] = torch.zeros((ctypes.sizeof(_native.SphStepStats),),
@@ -529,7 +540,8 @@ class Simulation:
         E.rp[0], E.rp[1] = T["rp0"].data_ptr(), T["rp1"].data_ptr()
         for k in ("dvdt", "drho", "id", "nnb", "refpos", "rho_scratch_id",
                   "oflow_id", "wall_id", "vol_id", "offs_f", "offs_w", "lists",
-                  "lcount", "ws", "stats"):
+                  "lcount", "acount", "nww", "mask", "cell0", "disp", "queue",
+                  "qcount", "ws", "stats"):
             setattr(E, k, T[k].data_ptr())
         E.ws_bytes = ws_bytes
         (cs, cutoff, h, alpha_d, c0, rho0, avisc, eps_h2) = force_scalars(reg, self.grid)
@@ -609,6 +621,7 @@ class Simulation:
         self._call("sph_engine_stats", ctypes.c_int32(_native.STATS_RESET))
         self._rebuild_cll()
         t0 = time.perf_counter()
+        self._build_lists(0.0)
         self._call("sph_engine_initialize")
         self._call("sph_engine_stats", ctypes.c_int32(_native.STATS_NORMS))
         stats = self._read_stats()
@@ -621,8 +634,30 @@ class Simulation:
     def _shepard_filter(self):
         """physics.py:469-487 (SHEPARD, COPY_SCALAR, DENSITY_UPDATE(0))."""
         self._ensure_device()
+        self._build_lists(0.0)
         self._call("sph_engine_shepard")
         self._host_stale = True
+
+    def _build_lists(self, skin):
+        """Ascending-id Verlet lists within cutoff + skin (csrc/engine.cu)."""
+        self._call("sph_engine_build_lists", ctypes.c_double(skin))
+
+    def _choose_skin(self, vmax, amax, dt):
+        """Skin for this step's lists: a multiple of the displacement the
+        step's own dt allows; any particle that outruns it is rebuilt exactly
+        on the device, so the choice affects speed only."""
+        cutoff = float(self._dev["E"].cutoff)
+        est = vmax * dt + amax * dt * dt
+        cap = (0.45 if self.registry.dim == 3 else 1.0) * cutoff
+        return min(self._skin_factor * est + 0.02 * cutoff, cap)
+
+    def _adapt_skin(self, nfix, nsub):
+        n = max(1, self.registry.particle_count)
+        frac = nfix / (n * max(1, nsub))
+        if frac > 2e-3:
+            self._skin_factor = min(self._skin_factor * 1.5, 16.0)
+        elif frac < 5e-4:
+            self._skin_factor = max(2.0, self._skin_factor * 0.95)
 
     def advance(self, end_time=None):
         """One advective step (physics.py:489-552); returns the dt taken."""
@@ -637,28 +672,33 @@ class Simulation:
         flags = _native.STATS_RESET | (0 if self._norms else _native.STATS_NORMS)
         self._call("sph_engine_stats", ctypes.c_int32(flags))
         self._rebuild_cll()
+        # compute_timestep (physics.py:502-511) reads only v and dvdt, which the
+        # Shepard filter does not touch, so the step's dt is known before the
+        # lists are built and sizes their skin
+        t0 = time.perf_counter()
+        if self._norms is None:
+            s = self._read_stats()
+            self._norms = (_bits_to_double(s.vmax_bits), _bits_to_double(s.amax_bits))
+        vmax, amax = self._norms
+        if self.fixed_dt is not None:
+            dt_ac = dt_adv = self.fixed_dt
+        else:
+            dt_ac, dt_adv = timestep_formula(
+                vmax, amax, float(self.registry.singular("h")),
+                float(self.registry.singular("c0")), self.dt_max,
+                self.cfl_acoustic, self.cfl_advective)
+        self.phase_seconds["integration"] += time.perf_counter() - t0
+        dt = dt_adv
+        if end_time is not None:
+            dt = min(dt, end_time - self.time)
+        t0 = time.perf_counter()
+        self._build_lists(self._choose_skin(vmax, amax, dt))
+        self.phase_seconds["cll"] += time.perf_counter() - t0
         if self.shepard_every and self.step_count > 0 \
                 and self.step_count % self.shepard_every == 0:
             t0 = time.perf_counter()
             self._call("sph_engine_shepard")
             self.phase_seconds["interactions"] += time.perf_counter() - t0
-        if self.fixed_dt is not None:
-            dt_ac = dt_adv = self.fixed_dt
-        else:
-            t0 = time.perf_counter()
-            if self._norms is None:
-                s = self._read_stats()
-                self._norms = (_bits_to_double(s.vmax_bits),
-                               _bits_to_double(s.amax_bits))
-            vmax, amax = self._norms
-            dt_ac, dt_adv = timestep_formula(
-                vmax, amax, float(self.registry.singular("h")),
-                float(self.registry.singular("c0")), self.dt_max,
-                self.cfl_acoustic, self.cfl_advective)
-            self.phase_seconds["integration"] += time.perf_counter() - t0
-        dt = dt_adv
-        if end_time is not None:
-            dt = min(dt, end_time - self.time)
         nsub = max(1, int(math.ceil(dt / dt_ac)))
         dts = dt / nsub
         dtype = self.registry.dtype.type
@@ -683,6 +723,8 @@ class Simulation:
         self.phase_seconds["interactions"] += time.perf_counter() - t0
         self._host_stale = True
         self.last_nsub = nsub
+        self.last_nfix = int(stats.nfix)
+        self._adapt_skin(stats.nfix, nsub)
         self.out_of_bounds += stats.oob + self._oob_walls
         self._finish_counts(stats, check=True)
         self.interaction_count += int(stats.interactions)

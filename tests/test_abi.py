@@ -34,7 +34,7 @@ def test_struct_layouts_match_header():
     # 14 pointers, 6 reals, 3 int64, 8 reals, int64, 2 int32
     assert ctypes.sizeof(_native.SphSweepArgs_f32) == 14 * 8 + 6 * 4 + 24 + 8 * 4 + 16
     assert ctypes.sizeof(_native.SphSweepArgs_f64) == 14 * 8 + 6 * 8 + 24 + 8 * 8 + 16
-    assert ctypes.sizeof(_native.SphStepStats) == 5 * 8 + 6 * 4
+    assert ctypes.sizeof(_native.SphStepStats) == 6 * 8 + 6 * 4
 
 
 def test_workspace_queries_need_no_gpu():
