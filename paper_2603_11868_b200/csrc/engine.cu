@@ -39,6 +39,52 @@ namespace sph {
         }                                                                                    \
     }
 
+// Software-pipelined walk over the accepted neighbours of slot in ascending
+// original id: the list entry two pairs ahead and the neighbour data one
+// pair ahead are in flight while the current pair is computed (the sweeps
+// are latency bound on these dependent gathers otherwise).
+template <class T, class Load, class Body>
+__device__ __forceinline__ void sweep_accepted(const Eng<T>& E, int64_t slot, int nl,
+                                               Load load, Body body)
+{
+    const int32_t* __restrict__ lp = E.lists + ell_index(slot, 0);
+    const int nwords = (nl + 31) >> 5;
+    int w = 0;
+    uint32_t m = nwords > 0 ? E.mask[mask_index(slot, 0)] : 0u;
+    auto next_pos = [&]() -> int {
+        while (m == 0) {
+            if (++w >= nwords) return -1;
+            m = E.mask[mask_index(slot, w)];
+        }
+        const int u = __ffs(m) - 1;
+        m &= m - 1;
+        return (w << 5) + u;
+    };
+    const int p0 = next_pos();
+    if (p0 < 0) return;
+    const int j0 = lp[p0 * 32];
+    int p1 = next_pos();
+    int j1 = p1 >= 0 ? lp[p1 * 32] : 0;
+    auto nxt = load(j0);
+    while (true) {
+        const auto cur = nxt;
+        const bool more = p1 >= 0;
+        int p2 = -1, j2 = 0;
+        if (more) {
+            nxt = load(j1);
+            p2 = next_pos();
+            if (p2 >= 0) j2 = lp[p2 * 32];
+        }
+        body(cur);
+        if (!more) break;
+        p1 = p2;
+        j1 = j2;
+    }
+}
+
+template <class T> struct NbrPVR { vec4<T> p; vec4<T> v; vec2<T> rp; };
+template <class T> struct NbrPR { vec4<T> p; vec2<T> rp; };
+
 __device__ __forceinline__ void enqueue(uint32_t* queue, uint32_t* qcount, bool need,
                                         uint32_t value)
 {
@@ -56,27 +102,20 @@ __device__ __forceinline__ void enqueue(uint32_t* queue, uint32_t* qcount, bool 
 // skin lists (one per advective step)
 // ---------------------------------------------------------------------------
 template <class T, int D>
-__global__ void __launch_bounds__(kNlThreads)
+__global__ void __launch_bounds__(kNlThreads, 4)
 k_skin_build(const EngAcc<T> acc, const GridP<T> g, T cs2, int64_t first, int64_t count,
              int64_t slot_first, unsigned store_mask, Eng<T> E)
 {
-    extern __shared__ __align__(16) unsigned char nl_smem[];
-    int32_t* stage = reinterpret_cast<int32_t*>(nl_smem);
-    unsigned long long* sbuf_all =
-        reinterpret_cast<unsigned long long*>(nl_smem + sizeof(int32_t) * kCap * kStagePitch);
-    int* scnt = reinterpret_cast<int*>(sbuf_all + kNlWarps * kCap);
-
+    // one warp per particle, grid-stride; lists written straight into the
+    // tile-ELL slot (L2 merges the 4-byte column writes of a tile's warps),
+    // which keeps shared memory at 16 KB per block and occupancy at 64 warps
+    __shared__ WarpBuf bufs[kNlWarps];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    unsigned long long* sb = sbuf_all + warp * kCap;
-    const int64_t t0 = (int64_t)blockIdx.x * 32;
-
-    for (int p = warp; p < 32; p += kNlWarps) {
-        const int64_t t = t0 + p;
-        if (t >= count) {
-            if (lane == 0) scnt[p] = 0;
-            continue;
-        }
+    WarpBuf& sb = bufs[warp];
+    for (int64_t t = (int64_t)blockIdx.x * kNlWarps + warp; t < count;
+         t += (int64_t)gridDim.x * kNlWarps) {
         const int64_t i = first + t;
+        const int64_t slot = slot_first + t;
         T xi[3];
         acc.position(i, xi);
         CollectCounts cc = warp_collect<T, D, true>(acc, g, i, xi, cs2, store_mask, sb);
@@ -85,29 +124,19 @@ k_skin_build(const EngAcc<T> acc, const GridP<T> g, T cs2, int64_t first, int64_
         int stored = cc.stored;
         if (stored > kCap) {   // list storage exhausted: exact rebuilds instead
             stored = 0;
-            if (lane == 0) E.cell0[i] = kInvalidCell;
         } else {
-            warp_sort_packed(sb, stored, lane);
-            for (int k = lane; k < stored; k += 32)
-                stage[k * kStagePitch + p] = (int32_t)(uint32_t)sb[k];
-            if (lane == 0) E.cell0[i] = key0;
+            warp_emit_sorted(sb, stored, lane, [&](int pos, uint32_t j) {
+                E.lists[ell_index(slot, pos)] = (int32_t)j;
+            });
         }
         if (lane == 0) {
-            scnt[p] = stored;
-            E.nww[slot_first + t] = cc.accepted;   // walls: static wall-wall count
+            E.cell0[i] = cc.stored > kCap ? kInvalidCell : key0;
+            E.lcount[slot] = stored;
+            E.nww[slot] = cc.accepted;   // walls: static wall-wall count
             E.disp[i] = T(0);
         }
         __syncwarp();
     }
-    __syncthreads();
-    int mc = 0;
-#pragma unroll 4
-    for (int q = 0; q < 32; q++) mc = max(mc, scnt[q]);
-    int32_t* dst = E.lists + (size_t)((slot_first + t0) >> 5) * (kCap * 32);
-    for (int idx = threadIdx.x; idx < mc * 32; idx += kNlThreads)
-        dst[idx] = stage[(idx >> 5) * kStagePitch + (idx & 31)];
-    if (threadIdx.x < 32 && t0 + threadIdx.x < count)
-        E.lcount[slot_first + t0 + threadIdx.x] = scnt[threadIdx.x];
 }
 
 // ---------------------------------------------------------------------------
@@ -177,11 +206,23 @@ k_mask(Eng<T> E, GridP<T> g, T s_eff)
                 const int32_t* lp = E.lists + ell_index(slot, w * 32);
                 const int ne = min(32, nl - w * 32);
                 uint32_t m = 0;
-                for (int u = 0; u < ne; ++u) {
-                    T xj[3];
-                    to3<T>(E.pos[lp[u * 32]], xj);
-                    const T r2 = accept_r2<T, D>(xi, xj);
-                    if ((r2 < g.c2) && (r2 > T(0))) m |= 1u << u;
+                // 4 independent list entries + positions in flight per trip
+                for (int u0 = 0; u0 < ne; u0 += 4) {
+                    int jj[4];
+#pragma unroll
+                    for (int k = 0; k < 4; k++) jj[k] = u0 + k < ne ? lp[(u0 + k) * 32] : -1;
+                    vec4<T> pj[4];
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        if (jj[k] >= 0) pj[k] = E.pos[jj[k]];
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        if (jj[k] < 0) continue;
+                        T xj[3];
+                        to3<T>(pj[k], xj);
+                        const T r2 = accept_r2<T, D>(xi, xj);
+                        if ((r2 < g.c2) && (r2 > T(0))) m |= 1u << (u0 + k);
+                    }
                 }
                 E.mask[mask_index(slot, w)] = m;
                 acc += __popc(m);
@@ -196,13 +237,13 @@ k_mask(Eng<T> E, GridP<T> g, T s_eff)
 // exact ordered lists (neighborhood.py:176-227) for the queued particles;
 // one warp per entry, grid-stride over the device-side queue length
 template <class T, int D>
-__global__ void __launch_bounds__(kNlThreads)
+__global__ void __launch_bounds__(kNlThreads, 4)
 k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E)
 {
-    __shared__ unsigned long long sbuf[kNlWarps][kCap];
+    __shared__ WarpBuf bufs[kNlWarps];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     const uint32_t qn = *(volatile uint32_t*)E.qcount;
-    unsigned long long* sb = sbuf[warp];
+    WarpBuf& sb = bufs[warp];
     for (uint32_t q = blockIdx.x * kNlWarps + warp; q < qn; q += gridDim.x * kNlWarps) {
         const int64_t i = E.queue[q];
         const int64_t slot = slot_of(E, i);
@@ -213,9 +254,9 @@ k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E)
         if (cc.accepted > kCap) {
             if (lane == 0) { E.acount[slot] = -1; E.lcount[slot] = 0; }
         } else {
-            warp_sort_packed(sb, cc.stored, lane);
-            for (int k = lane; k < cc.stored; k += 32)
-                E.lists[ell_index(slot, k)] = (int32_t)(uint32_t)sb[k];
+            warp_emit_sorted(sb, cc.stored, lane, [&](int pos, uint32_t j) {
+                E.lists[ell_index(slot, pos)] = (int32_t)j;
+            });
             for (int w = lane; w * 32 < cc.stored; w += 32) {
                 const int rem = cc.stored - w * 32;
                 E.mask[mask_index(slot, w)] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
@@ -259,14 +300,15 @@ k_cont_du(Eng<T> E, PhysP pp, int cv, int crp, T full)
     const T rho_i = rp[i].x;
     double acc = double(RN<T>::sub(rho_i, rho_i));
     const int nl = E.lcount[i];
-    SPH_FOR_EACH_ACCEPTED(E, i, nl, j, {
-        const vec4<T> PJ = pos[j];
-        T xj[3], vj[3], dx[3], r2, vx;
-        to3<T>(PJ, xj);
-        to3<T>(vel[j], vj);
-        pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-        acc = dadd(acc, continuity_term<T>(r2, vx, PJ.w, rp[j].x, P));
-    })
+    sweep_accepted<T>(E, i, nl,
+        [&](int j) { return NbrPVR<T>{pos[j], vel[j], rp[j]}; },
+        [&](const NbrPVR<T>& nb) {
+            T xj[3], vj[3], dx[3], r2, vx;
+            to3<T>(nb.p, xj);
+            to3<T>(nb.v, vj);
+            pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
+            acc = dadd(acc, continuity_term<T>(r2, vx, nb.p.w, nb.rp.x, P));
+        });
     const T dr = RN<T>::from_d(dmul(double(rho_i), acc));
     E.drho[i] = dr;
     vec2<T> out;
@@ -299,13 +341,15 @@ k_wall(Eng<T> E, PhysP pp, int b, int zero_drho, int count_factor)
             double num = double(RN<T>::sub(rho_i, rho_i));
             double den = num;
             const int nl = E.lcount[slot];
-            SPH_FOR_EACH_ACCEPTED(E, slot, nl, j, {
-                T xj[3];
-                to3<T>(E.pos[j], xj);
-                const double w = wall_weight<T>(pair_r2<T, D>(xi, xj), P);
-                num = dadd(num, dmul(double(rp[j].y), w));
-                den = dadd(den, w);
-            })
+            sweep_accepted<T>(E, slot, nl,
+                [&](int j) { return NbrPR<T>{E.pos[j], rp[j]}; },
+                [&](const NbrPR<T>& nb) {
+                    T xj[3];
+                    to3<T>(nb.p, xj);
+                    const double w = wall_weight<T>(pair_r2<T, D>(xi, xj), P);
+                    num = dadd(num, dmul(double(nb.rp.y), w));
+                    den = dadd(den, w);
+                });
             vec2<T> out;
             out.y = den > 0.0 ? RN<T>::from_d(ddiv(num, den)) : T(0);
             out.x = RN<T>::add(P.rho0, RN<T>::div(out.y, P.c0c0));
@@ -344,15 +388,16 @@ k_mom(Eng<T> E, PhysP pp, int cv, int brp, int kick, T half, int count_factor)
             const T pi_rr = RN<T>::div(RPI.y, RN<T>::mul(rho_i, rho_i));
             T a[3] = {P.g[0], P.g[1], P.g[2]};
             const int nl = E.lcount[i];
-            SPH_FOR_EACH_ACCEPTED(E, i, nl, j, {
-                const vec4<T> PJ = pos[j];
-                const vec2<T> RPJ = rp[j];
-                T xj[3], vj[3], dx[3], r2, vx;
-                to3<T>(PJ, xj);
-                to3<T>(vel[j], vj);
-                pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-                momentum_pair<T, D>(r2, vx, dx, rho_i, pi_rr, RPJ.x, RPJ.y, PJ.w, P, a);
-            })
+            sweep_accepted<T>(E, i, nl,
+                [&](int j) { return NbrPVR<T>{pos[j], vel[j], rp[j]}; },
+                [&](const NbrPVR<T>& nb) {
+                    T xj[3], vj[3], dx[3], r2, vx;
+                    to3<T>(nb.p, xj);
+                    to3<T>(nb.v, vj);
+                    pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
+                    momentum_pair<T, D>(r2, vx, dx, rho_i, pi_rr, nb.rp.x, nb.rp.y, nb.p.w, P,
+                                        a);
+                });
             vec4<T> A4;
             A4.x = a[0]; A4.y = a[1]; A4.z = D == 3 ? a[2] : T(0); A4.w = T(0);
             E.dvdt[i] = A4;
@@ -445,15 +490,17 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
     EngAcc<T> acc = acc_of_engine<T>(e);
     Eng<T> E = eng_of<T>(e);
     const T cs2 = skin_cs2<T>(e);
-    cudaFuncSetAttribute(k_skin_build<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kNlSmem);
+    auto blocks = [](int64_t cnt) {
+        const int64_t want = (cnt + kNlWarps - 1) / kNlWarps;
+        return (unsigned)(want < 148 * 32 ? want : 148 * 32);
+    };
     if (e->nf > 0)
-        note_launch(), k_skin_build<T, D><<<(unsigned)((e->nf + 31) / 32), kNlThreads, kNlSmem,
-                                            s>>>(acc, g, cs2, 0, e->nf, 0, 3u, E);
+        note_launch(), k_skin_build<T, D><<<blocks(e->nf), kNlThreads, 0, s>>>(
+            acc, g, cs2, 0, e->nf, 0, 3u, E);
     const int64_t nw = e->n - e->nf;
     if (nw > 0)
-        note_launch(), k_skin_build<T, D><<<(unsigned)((nw + 31) / 32), kNlThreads, kNlSmem,
-                                            s>>>(acc, g, cs2, e->nf, nw, E.nf_pad, 1u, E);
+        note_launch(), k_skin_build<T, D><<<blocks(nw), kNlThreads, 0, s>>>(
+            acc, g, cs2, e->nf, nw, E.nf_pad, 1u, E);
     e->lists_ready = 1;
     return check_launch("engine_build_lists");
 }

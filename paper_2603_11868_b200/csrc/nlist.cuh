@@ -31,8 +31,10 @@ namespace sph {
 constexpr int kNlWarps = 8;
 constexpr int kNlThreads = kNlWarps * 32;
 constexpr int kStagePitch = 33;   // conflict-free transposition
-constexpr size_t kNlSmem = sizeof(int32_t) * kCap * kStagePitch +
-                           sizeof(unsigned long long) * kNlWarps * kCap + sizeof(int) * 64;
+struct WarpBuf;
+constexpr size_t kWarpBufBytes = sizeof(uint32_t) * (2 * kCap + 4);
+constexpr size_t kNlSmem = sizeof(int32_t) * kCap * kStagePitch + kWarpBufBytes * kNlWarps +
+                           sizeof(int) * 64;
 constexpr int kMaskWords = kCap / 32;   // 256-bit filter mask per particle
 
 template <class T>
@@ -86,21 +88,123 @@ __device__ __forceinline__ unsigned long long warp_bitonic_reg(unsigned long lon
     return v;
 }
 
-// Sort sb[0..n) ascending (n <= kCap) in place; the warp must be converged.
-__device__ __forceinline__ void warp_sort_packed(unsigned long long* sb, int n, unsigned lane)
+// Register bitonic sort of 32*PER values held blocked (lane owns elements
+// lane*PER .. lane*PER+PER-1): partners closer than PER are exchanged inside
+// a lane, farther ones through shuffles.  Fully unrolled; ~5x cheaper than a
+// shared-memory network for 128 elements.
+template <int PER>
+__device__ __forceinline__ void warp_bitonic_blocked(unsigned long long (&v)[PER], unsigned lane)
+{
+    constexpr int N = 32 * PER;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= PER) {
+#pragma unroll
+                for (int r = 0; r < PER; r++) {
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, v[r], j / PER);
+                    const int e = (int)lane * PER + r;
+                    const bool up = (e & k) == 0, lower = (e & j) == 0;
+                    const unsigned long long mn = o < v[r] ? o : v[r];
+                    const unsigned long long mx = o < v[r] ? v[r] : o;
+                    v[r] = (lower == up) ? mn : mx;
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < PER; r++) {
+                    if (r & j) continue;
+                    const int e = (int)lane * PER + r;
+                    const bool up = (e & k) == 0;
+                    const unsigned long long a = v[r], b = v[r ^ j];
+                    const bool sw = (a > b) == up;
+                    v[r] = sw ? b : a;
+                    v[r ^ j] = sw ? a : b;
+                }
+            }
+        }
+    }
+}
+
+template <int PER>
+__device__ __forceinline__ void warp_sort_blocked_smem(unsigned long long* sb, int n,
+                                                       unsigned lane)
+{
+    unsigned long long v[PER];
+#pragma unroll
+    for (int r = 0; r < PER; r++) {
+        const int e = (int)lane * PER + r;
+        v[r] = e < n ? sb[e] : ~0ull;
+    }
+    warp_bitonic_blocked<PER>(v, lane);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < PER; r++) {
+        const int e = (int)lane * PER + r;
+        if (e < n) sb[e] = v[r];
+    }
+}
+
+// Per-warp survivor buffer: original ids and physical indices (compacted).
+struct __align__(16) WarpBuf {
+    uint32_t id[kCap + 4];   // +4: padding so 128-bit loads may read past n
+    uint32_t j[kCap];
+};
+
+// Rank by counting: survivor e goes to position #{f : id_f < id_e} (ids are
+// unique).  Each lane owns E survivors; the ids are streamed from shared
+// memory four at a time as broadcasts.  For n <= 128 this is cheaper than a
+// bitonic network (2 ALU ops per comparison, no data movement).
+template <int E, class Emit>
+__device__ __forceinline__ void rank_emit(WarpBuf& b, int n, unsigned lane, Emit emit)
+{
+    if (lane < 4) b.id[n + lane] = 0xffffffffu;
+    __syncwarp();
+    uint32_t my[E];
+    int rank[E];
+#pragma unroll
+    for (int k = 0; k < E; k++) {
+        const int e = (int)lane + 32 * k;
+        my[k] = e < n ? b.id[e] : 0xffffffffu;
+        rank[k] = 0;
+    }
+    const uint4* ids4 = reinterpret_cast<const uint4*>(b.id);
+    for (int f = 0; f < n; f += 4) {
+        const uint4 q = ids4[f >> 2];
+#pragma unroll
+        for (int k = 0; k < E; k++)
+            rank[k] += (int)(q.x < my[k]) + (int)(q.y < my[k]) + (int)(q.z < my[k]) +
+                       (int)(q.w < my[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < E; k++) {
+        const int e = (int)lane + 32 * k;
+        if (e < n) emit(rank[k], b.j[e]);
+    }
+}
+
+// Emit the n survivors of b in ascending original id: emit(position, j).
+template <class Emit>
+__device__ __forceinline__ void warp_emit_sorted(WarpBuf& b, int n, unsigned lane, Emit emit)
 {
     __syncwarp();
-    if (n <= 32) {
-        unsigned long long v = lane < (unsigned)n ? sb[lane] : ~0ull;
-        v = warp_bitonic_reg(v, lane);
-        __syncwarp();
-        if (lane < (unsigned)n) sb[lane] = v;
-    } else {
-        int np = 64;
-        while (np < n) np <<= 1;
-        for (int k = n + lane; k < np; k += 32) sb[k] = ~0ull;
-        __syncwarp();
-        warp_bitonic_smem(sb, np, lane);
+    if (n <= 32) rank_emit<1>(b, n, lane, emit);
+    else if (n <= 64) rank_emit<2>(b, n, lane, emit);
+    else if (n <= 96) rank_emit<3>(b, n, lane, emit);
+    else if (n <= 128) rank_emit<4>(b, n, lane, emit);
+    else {   // long skin lists: register bitonic network over (id, j) pairs
+        unsigned long long v[8];
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const int e = (int)lane * 8 + r;
+            v[r] = e < n ? (((unsigned long long)b.id[e] << 32) | b.j[e]) : ~0ull;
+        }
+        warp_bitonic_blocked<8>(v, lane);
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const int e = (int)lane * 8 + r;
+            if (e < n) emit(e, (uint32_t)v[r]);
+        }
     }
     __syncwarp();
 }
@@ -178,8 +282,7 @@ struct CollectCounts {
 template <class T, int D, bool SKIN, class Acc>
 __device__ __forceinline__ CollectCounts warp_collect(const Acc& acc, const GridP<T>& g,
                                                       int64_t i, const T (&xi)[3], T cs2,
-                                                      unsigned store_mask,
-                                                      unsigned long long* sb)
+                                                      unsigned store_mask, WarpBuf& buf)
 {
     const unsigned lane = lane_id();
     const unsigned lt = lanemask_lt();
@@ -211,7 +314,7 @@ __device__ __forceinline__ CollectCounts warp_collect(const Acc& acc, const Grid
         acc.run(seg, klo, khi, s0, s1);
     }
     // flatten: exclusive prefix of run lengths
-    uint32_t len = (uint32_t)(s1 - s0);
+    const uint32_t len = (uint32_t)(s1 - s0);
     uint32_t incl = len;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -220,30 +323,48 @@ __device__ __forceinline__ CollectCounts warp_collect(const Acc& acc, const Grid
     }
     const uint32_t start = incl - len;
     const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t seg_s0 = (uint32_t)s0 | ((uint32_t)seg << 31);   // index < 2^31
     CollectCounts out{0, 0};
-    for (uint32_t base = 0; base < total; base += 32) {
-        const uint32_t idx = base + lane;
-        // largest run r with start_r <= idx (empty runs tie to the later run)
-        int r = 0;
+    // each lane tracks the run of its candidate index; indices grow by 32
+    // per chunk, so the run only ever moves forward (usually 0-1 runs)
+    int r[2] = {0, 0};
+    for (uint32_t base = 0; base < total; base += 64) {
+        int64_t jj[2];
+        int sg[2];
+        bool valid[2];
 #pragma unroll
-        for (int step = 16; step >= 1; step >>= 1) {
-            const int cand = r + step;
-            const uint32_t sv = __shfl_sync(0xffffffffu, start, cand & 31);
-            if (cand < nruns && sv <= idx) r = cand;
+        for (int h = 0; h < 2; h++) {
+            const uint32_t idx = base + 32 * h + lane;
+            while (true) {
+                const int nr = r[h] + 1;
+                const uint32_t sv = __shfl_sync(0xffffffffu, start, nr & 31);
+                const bool adv = nr < nruns && sv <= idx;
+                if (!__any_sync(0xffffffffu, adv)) break;
+                if (adv) r[h] = nr;
+            }
+            const uint32_t rss = __shfl_sync(0xffffffffu, seg_s0, r[h]);
+            const uint32_t rstart = __shfl_sync(0xffffffffu, start, r[h]);
+            sg[h] = (int)(rss >> 31);
+            valid[h] = idx < total;
+            jj[h] = valid[h] ? acc.cand((int64_t)(rss & 0x7fffffffu) + (idx - rstart)) : 0;
+            valid[h] = valid[h] && jj[h] != i;
         }
-        const int64_t rs0 = __shfl_sync(0xffffffffu, s0, r);
-        const uint32_t rstart = __shfl_sync(0xffffffffu, start, r);
-        const int rseg = __shfl_sync(0xffffffffu, seg, r);
-        bool ok_store = false, ok_count = false;
-        int64_t j = 0;
-        if (idx < total) {
-            j = acc.cand(rs0 + (idx - rstart));
-            if (j != i) {
-                T xj[3];
-                acc.position(j, xj);
-                const T r2 = accept_r2<T, D>(xi, xj);
+        T xj[2][3];
+        uint32_t idj[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            if (valid[h]) {
+                acc.position(jj[h], xj[h]);
+                idj[h] = acc.idof(jj[h]);
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            bool ok_store = false, ok_count = false;
+            if (valid[h]) {
+                const T r2 = accept_r2<T, D>(xi, xj[h]);
                 const bool exact = (r2 < g.c2) && (r2 > T(0));
-                const bool stores = (store_mask >> rseg) & 1u;
+                const bool stores = (store_mask >> sg[h]) & 1u;
                 if (SKIN) {
                     ok_store = stores && (r2 < cs2);
                     ok_count = !stores && exact;
@@ -252,15 +373,17 @@ __device__ __forceinline__ CollectCounts warp_collect(const Acc& acc, const Grid
                     ok_count = exact;
                 }
             }
+            const unsigned bs = __ballot_sync(0xffffffffu, ok_store);
+            if (ok_store) {
+                const int p = out.stored + __popc(bs & lt);
+                if (p < kCap) {
+                    buf.id[p] = idj[h];
+                    buf.j[p] = (uint32_t)jj[h];
+                }
+            }
+            out.stored += __popc(bs);
+            out.accepted += __popc(__ballot_sync(0xffffffffu, ok_count));
         }
-        const unsigned bs = __ballot_sync(0xffffffffu, ok_store);
-        if (ok_store) {
-            const int p = out.stored + __popc(bs & lt);
-            if (p < kCap)
-                sb[p] = ((unsigned long long)acc.idof(j) << 32) | (unsigned long long)(uint32_t)j;
-        }
-        out.stored += __popc(bs);
-        out.accepted += __popc(__ballot_sync(0xffffffffu, ok_count));
     }
     return out;
 }
@@ -270,18 +393,18 @@ __device__ __forceinline__ CollectCounts warp_collect(const Acc& acc, const Grid
 // block writes lists[tile][t][lane] coalesced.  lcount[slot] = count, or -1
 // when more than kCap neighbours qualify (neighborhood.py:200-202).
 template <class T, int D, class Acc>
-__global__ void __launch_bounds__(kNlThreads)
+__global__ void __launch_bounds__(kNlThreads, 4)
 k_build_lists(const Acc acc, const GridP<T> g, int64_t first, int64_t count,
               int64_t slot_first, int32_t* __restrict__ lists, int32_t* __restrict__ lcount)
 {
     extern __shared__ __align__(16) unsigned char nl_smem[];
     int32_t* stage = reinterpret_cast<int32_t*>(nl_smem);
-    unsigned long long* sbuf_all =
-        reinterpret_cast<unsigned long long*>(nl_smem + sizeof(int32_t) * kCap * kStagePitch);
-    int* scnt = reinterpret_cast<int*>(sbuf_all + kNlWarps * kCap);
+    WarpBuf* bufs =
+        reinterpret_cast<WarpBuf*>(nl_smem + sizeof(int32_t) * kCap * kStagePitch);
+    int* scnt = reinterpret_cast<int*>(bufs + kNlWarps);
 
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    unsigned long long* sb = sbuf_all + warp * kCap;
+    WarpBuf& sb = bufs[warp];
     const int64_t t0 = (int64_t)blockIdx.x * 32;
 
     for (int p = warp; p < 32; p += kNlWarps) {
@@ -299,9 +422,9 @@ k_build_lists(const Acc acc, const GridP<T> g, int64_t first, int64_t count,
             __syncwarp();
             continue;
         }
-        warp_sort_packed(sb, cc.stored, lane);
-        for (int k = lane; k < cc.stored; k += 32)
-            stage[k * kStagePitch + p] = (int32_t)(uint32_t)sb[k];
+        warp_emit_sorted(sb, cc.stored, lane, [&](int pos, uint32_t j) {
+            stage[pos * kStagePitch + p] = (int32_t)j;
+        });
         if (lane == 0) scnt[p] = cc.stored;
         __syncwarp();
     }
