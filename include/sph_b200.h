@@ -186,12 +186,12 @@ typedef struct {
     void* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; void* vol_id;
     /* cell offsets into each segment (dev, ncells+1 each) */
     uint32_t* offs_f; uint32_t* offs_w;
-    /* ascending-id neighbour lists, tile-ELL [slots/32][256][32] int32, and
-     * per slot: entries (lcount), exact accepted count this sub-step or -1
-     * (acount), static wall-wall count of walls (nww); 256-bit exact-filter
-     * masks [slots/32][8][32]; per particle: list cell (cell0) and path
-     * length since the list build (disp, run precision); fix-up queue */
-    int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; uint32_t* mask;
+    /* ascending-id Verlet (skin) lists and this sub-step's exact lists, both
+     * tile-ELL [slots/32][256][32] int32; per slot: skin entries (lcount),
+     * exact count or -1 on overflow (acount), static wall-wall count of walls
+     * (nww); per particle: list cell (cell0) and path length since the list
+     * build (disp, run precision); fix-up queue */
+    int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; int32_t* elist;
     uint32_t* cell0; void* disp; uint32_t* queue; uint32_t* qcount;
     /* scratch (dev): keys/values x2 for the radix sort + gather staging */
     void* ws; size_t ws_bytes;

@@ -78,7 +78,7 @@ class SphEngine(C.Structure):
         ("id", P), ("nnb", P), ("refpos", P),
         ("rho_scratch_id", P), ("oflow_id", P), ("wall_id", P), ("vol_id", P),
         ("offs_f", P), ("offs_w", P),
-        ("lists", P), ("lcount", P), ("acount", P), ("nww", P), ("mask", P),
+        ("lists", P), ("lcount", P), ("acount", P), ("nww", P), ("elist", P),
         ("cell0", P), ("disp", P), ("queue", P), ("qcount", P),
         ("ws", P), ("ws_bytes", c_size),
         ("stats", P),

@@ -7,7 +7,7 @@
 // step the reference recomputes neighbours at every sweep from CURRENT
 // positions with the stale CLL (neighborhood.py:188-213); the engine gets the
 // identical ordered set by filtering the skin list exactly (0 < r2 < c^2 in
-// binary32, the reference's test) into a 256-bit mask per particle, which is
+// binary32, the reference's test) into an exact list per sub-step, which is
 // exact as long as (a) the particle is still in the cell its list was built
 // for and (b) its displacement bound plus the largest displacement bound of
 // any particle stays below the skin (triangle inequality; bounds are
@@ -17,7 +17,7 @@
 //
 // One acoustic sub-step (physics.py:522-548):
 //   k_kick_drift  KICK + DRIFT, displacement bounds, cell-change marks
-//   k_mask        exact filter of the skin lists -> masks, accepted counts
+//   k_mask        exact filter of the skin lists -> exact lists + counts
 //   k_fix_build   exact ordered lists for the marked particles
 //   k_cont_du     CONTINUITY + DENSITY_UPDATE   (fluid)
 //   k_wall        WALL_PRESSURE                 (walls)
@@ -26,59 +26,22 @@
 
 namespace sph {
 
-// iterate the accepted neighbours j of slot in ascending original id
-#define SPH_FOR_EACH_ACCEPTED(E, slot, nlist, j, ...)                                        \
-    for (int w_ = 0; w_ * 32 < (nlist); ++w_) {                                             \
-        uint32_t m_ = (E).mask[mask_index((slot), w_)];                                     \
-        const int32_t* lp_ = (E).lists + ell_index((slot), w_ * 32);                        \
-        while (m_) {                                                                         \
-            const int u_ = __ffs(m_) - 1;                                                    \
-            m_ &= m_ - 1;                                                                    \
-            const int j = lp_[u_ * 32];                                                      \
-            __VA_ARGS__                                                                      \
-        }                                                                                    \
-    }
-
-// Software-pipelined walk over the accepted neighbours of slot in ascending
-// original id: the list entry two pairs ahead and the neighbour data one
-// pair ahead are in flight while the current pair is computed (the sweeps
-// are latency bound on these dependent gathers otherwise).
+// Software-pipelined walk over the exact list of slot (ascending original
+// id): the list entry two pairs ahead and the neighbour data one pair ahead
+// are in flight while the current pair is computed.
 template <class T, class Load, class Body>
-__device__ __forceinline__ void sweep_accepted(const Eng<T>& E, int64_t slot, int nl,
-                                               Load load, Body body)
+__device__ __forceinline__ void sweep_list(const Eng<T>& E, int64_t slot, int cnt, Load load,
+                                           Body body)
 {
-    const int32_t* __restrict__ lp = E.lists + ell_index(slot, 0);
-    const int nwords = (nl + 31) >> 5;
-    int w = 0;
-    uint32_t m = nwords > 0 ? E.mask[mask_index(slot, 0)] : 0u;
-    auto next_pos = [&]() -> int {
-        while (m == 0) {
-            if (++w >= nwords) return -1;
-            m = E.mask[mask_index(slot, w)];
-        }
-        const int u = __ffs(m) - 1;
-        m &= m - 1;
-        return (w << 5) + u;
-    };
-    const int p0 = next_pos();
-    if (p0 < 0) return;
-    const int j0 = lp[p0 * 32];
-    int p1 = next_pos();
-    int j1 = p1 >= 0 ? lp[p1 * 32] : 0;
-    auto nxt = load(j0);
-    while (true) {
+    if (cnt <= 0) return;
+    const int32_t* __restrict__ lp = E.elist + ell_index(slot, 0);
+    int j1 = cnt > 1 ? lp[32] : 0;
+    auto nxt = load(lp[0]);
+    for (int t = 0; t < cnt; ++t) {
         const auto cur = nxt;
-        const bool more = p1 >= 0;
-        int p2 = -1, j2 = 0;
-        if (more) {
-            nxt = load(j1);
-            p2 = next_pos();
-            if (p2 >= 0) j2 = lp[p2 * 32];
-        }
+        if (t + 1 < cnt) nxt = load(j1);
+        if (t + 2 < cnt) j1 = lp[(t + 2) * 32];
         body(cur);
-        if (!more) break;
-        p1 = p2;
-        j1 = j2;
     }
 }
 
@@ -180,7 +143,7 @@ k_kick_drift(Eng<T> E, int cv, GridP<T> g, T half, T full)
     if (lane_id() == 0 && b) atomicMax(&E.stats->dmax_bits, b);
 }
 
-// exact filter of every valid skin list on current positions -> masks and
+// exact filter of every valid skin list on current positions -> exact lists and
 // accepted counts; particles whose list is not valid go to the fix queue
 template <class T, int D>
 __global__ void __launch_bounds__(kSweepThreads)
@@ -202,30 +165,28 @@ k_mask(Eng<T> E, GridP<T> g, T s_eff)
             to3<T>(E.pos[i], xi);
             const int nl = E.lcount[slot];
             int acc = 0;
-            for (int w = 0; w * 32 < nl; ++w) {
-                const int32_t* lp = E.lists + ell_index(slot, w * 32);
-                const int ne = min(32, nl - w * 32);
-                uint32_t m = 0;
-                // 4 independent list entries + positions in flight per trip
-                for (int u0 = 0; u0 < ne; u0 += 4) {
-                    int jj[4];
+            const int32_t* lp = E.lists + ell_index(slot, 0);
+            int32_t* ep = E.elist + ell_index(slot, 0);
+            // 4 independent list entries + positions in flight per trip
+            for (int u0 = 0; u0 < nl; u0 += 4) {
+                int jj[4];
 #pragma unroll
-                    for (int k = 0; k < 4; k++) jj[k] = u0 + k < ne ? lp[(u0 + k) * 32] : -1;
-                    vec4<T> pj[4];
+                for (int k = 0; k < 4; k++) jj[k] = u0 + k < nl ? lp[(u0 + k) * 32] : -1;
+                vec4<T> pj[4];
 #pragma unroll
-                    for (int k = 0; k < 4; k++)
-                        if (jj[k] >= 0) pj[k] = E.pos[jj[k]];
+                for (int k = 0; k < 4; k++)
+                    if (jj[k] >= 0) pj[k] = E.pos[jj[k]];
 #pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        if (jj[k] < 0) continue;
-                        T xj[3];
-                        to3<T>(pj[k], xj);
-                        const T r2 = accept_r2<T, D>(xi, xj);
-                        if ((r2 < g.c2) && (r2 > T(0))) m |= 1u << (u0 + k);
+                for (int k = 0; k < 4; k++) {
+                    if (jj[k] < 0) continue;
+                    T xj[3];
+                    to3<T>(pj[k], xj);
+                    const T r2 = accept_r2<T, D>(xi, xj);
+                    if ((r2 < g.c2) && (r2 > T(0))) {
+                        if (acc < kCap) ep[acc * 32] = jj[k];
+                        acc++;
                     }
                 }
-                E.mask[mask_index(slot, w)] = m;
-                acc += __popc(m);
             }
             const int total = acc + (i >= E.nf ? E.nww[slot] : 0);
             E.acount[slot] = total > kCap ? -1 : acc;
@@ -252,19 +213,12 @@ k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E)
         acc.position(i, xi);
         CollectCounts cc = warp_collect<T, D, false>(acc, g, i, xi, T(0), fluid ? 3u : 1u, sb);
         if (cc.accepted > kCap) {
-            if (lane == 0) { E.acount[slot] = -1; E.lcount[slot] = 0; }
+            if (lane == 0) E.acount[slot] = -1;
         } else {
             warp_emit_sorted(sb, cc.stored, lane, [&](int pos, uint32_t j) {
-                E.lists[ell_index(slot, pos)] = (int32_t)j;
+                E.elist[ell_index(slot, pos)] = (int32_t)j;
             });
-            for (int w = lane; w * 32 < cc.stored; w += 32) {
-                const int rem = cc.stored - w * 32;
-                E.mask[mask_index(slot, w)] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
-            }
-            if (lane == 0) {
-                E.lcount[slot] = cc.stored;
-                E.acount[slot] = cc.stored;   // fluid: all; walls: fluid visits
-            }
+            if (lane == 0) E.acount[slot] = cc.stored;   // fluid: all; walls: fluid visits
         }
         if (lane == 0) atomicAdd(&E.stats->nfix, 1u);
         __syncwarp();
@@ -299,8 +253,7 @@ k_cont_du(Eng<T> E, PhysP pp, int cv, int crp, T full)
     to3<T>(vel[i], vi);
     const T rho_i = rp[i].x;
     double acc = double(RN<T>::sub(rho_i, rho_i));
-    const int nl = E.lcount[i];
-    sweep_accepted<T>(E, i, nl,
+    sweep_list<T>(E, i, acnt,
         [&](int j) { return NbrPVR<T>{pos[j], vel[j], rp[j]}; },
         [&](const NbrPVR<T>& nb) {
             T xj[3], vj[3], dx[3], r2, vx;
@@ -340,8 +293,7 @@ k_wall(Eng<T> E, PhysP pp, int b, int zero_drho, int count_factor)
             const T rho_i = rp[i].x;
             double num = double(RN<T>::sub(rho_i, rho_i));
             double den = num;
-            const int nl = E.lcount[slot];
-            sweep_accepted<T>(E, slot, nl,
+            sweep_list<T>(E, slot, acnt,
                 [&](int j) { return NbrPR<T>{E.pos[j], rp[j]}; },
                 [&](const NbrPR<T>& nb) {
                     T xj[3];
@@ -387,8 +339,7 @@ k_mom(Eng<T> E, PhysP pp, int cv, int brp, int kick, T half, int count_factor)
             const T rho_i = RPI.x;
             const T pi_rr = RN<T>::div(RPI.y, RN<T>::mul(rho_i, rho_i));
             T a[3] = {P.g[0], P.g[1], P.g[2]};
-            const int nl = E.lcount[i];
-            sweep_accepted<T>(E, i, nl,
+            sweep_list<T>(E, i, acnt,
                 [&](int j) { return NbrPVR<T>{pos[j], vel[j], rp[j]}; },
                 [&](const NbrPVR<T>& nb) {
                     T xj[3], vj[3], dx[3], r2, vx;
@@ -440,15 +391,15 @@ k_shepard(Eng<T> E, PhysP pp, int crp)
         const T m_i = PI.w;
         double num = double(RN<T>::mul(m_i, P.alpha_d));
         double den = double(RN<T>::mul(RN<T>::div(m_i, RPI.x), P.alpha_d));
-        const int nl = E.lcount[i];
-        SPH_FOR_EACH_ACCEPTED(E, i, nl, j, {
-            const vec4<T> PJ = E.pos[j];
-            T xj[3];
-            to3<T>(PJ, xj);
-            const double w = wall_weight<T>(pair_r2<T, D>(xi, xj), P);
-            num = dadd(num, dmul(double(PJ.w), w));
-            den = dadd(den, dmul(double(RN<T>::div(PJ.w, rp[j].x)), w));
-        })
+        sweep_list<T>(E, i, E.acount[i],
+            [&](int j) { return NbrPR<T>{E.pos[j], rp[j]}; },
+            [&](const NbrPR<T>& nb) {
+                T xj[3];
+                to3<T>(nb.p, xj);
+                const double w = wall_weight<T>(pair_r2<T, D>(xi, xj), P);
+                num = dadd(num, dmul(double(nb.p.w), w));
+                den = dadd(den, dmul(double(RN<T>::div(nb.p.w, nb.rp.x)), w));
+            });
         rho_new = RN<T>::from_d(ddiv(num, den));
     }
     E.rho_scratch_id[pid] = rho_new;
@@ -512,7 +463,7 @@ extern "C" int sph_engine_build_lists(SphEngine* e, double skin, cudaStream_t s)
     return SPH_DISPATCH(e, build_lists_impl, e, skin, s);
 }
 
-// masks for valid skin lists + exact rebuilds for the rest
+// exact lists: filtered skin lists, exact rebuilds for the rest
 template <class T, int D>
 static void prepare_lists(const SphEngine* e, cudaStream_t s)
 {

@@ -29,7 +29,7 @@ struct Eng {
     uint32_t* id; uint32_t* nnb; uint32_t* refpos;
     T* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; T* vol_id;
     uint32_t* offs_f; uint32_t* offs_w;
-    int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; uint32_t* mask;
+    int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; int32_t* elist;
     uint32_t* cell0; T* disp; uint32_t* queue; uint32_t* qcount;
     SphStepStats* stats;
 };
@@ -48,7 +48,7 @@ inline Eng<T> eng_of(const SphEngine* e)
     g.wall_id = e->wall_id; g.vol_id = (T*)e->vol_id;
     g.offs_f = e->offs_f; g.offs_w = e->offs_w;
     g.lists = e->lists; g.lcount = e->lcount; g.acount = e->acount; g.nww = e->nww;
-    g.mask = e->mask; g.cell0 = e->cell0; g.disp = (T*)e->disp; g.queue = e->queue;
+    g.elist = e->elist; g.cell0 = e->cell0; g.disp = (T*)e->disp; g.queue = e->queue;
     g.qcount = e->qcount; g.stats = e->stats;
     return g;
 }

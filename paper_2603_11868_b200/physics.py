@@ -523,8 +523,8 @@ class Simulation:
         T["lcount"] = torch.empty((slots,), dtype=i32, device=dev)
         T["acount"] = torch.empty((slots,), dtype=i32, device=dev)
         T["nww"] = torch.empty((slots,), dtype=i32, device=dev)
-        T["mask"] = torch.empty((max(tiles, 1), NEIGHBOR_CAPACITY // 32, 32), dtype=i32,
-                                device=dev)
+        T["elist"] = torch.empty((max(tiles, 1), NEIGHBOR_CAPACITY, 32), dtype=i32,
+                                 device=dev)
         T["cell0"] = torch.empty((max(n, 1),), dtype=i32, device=dev)
         T["disp"] = torch.empty((max(n, 1),), dtype=tdt, device=dev)
         T["queue"] = torch.empty((max(n, 1),), dtype=i32, device=dev)
@@ -540,7 +540,7 @@ class Simulation:
         E.rp[0], E.rp[1] = T["rp0"].data_ptr(), T["rp1"].data_ptr()
         for k in ("dvdt", "drho", "id", "nnb", "refpos", "rho_scratch_id",
                   "oflow_id", "wall_id", "vol_id", "offs_f", "offs_w", "lists",
-                  "lcount", "acount", "nww", "mask", "cell0", "disp", "queue",
+                  "lcount", "acount", "nww", "elist", "cell0", "disp", "queue",
                   "qcount", "ws", "stats"):
             setattr(E, k, T[k].data_ptr())
         E.ws_bytes = ws_bytes
