@@ -115,6 +115,11 @@ int sph_density_update_f64(double* rho, double* p, const double* drho, const uin
                            double dt, double c0, double rho0, cudaStream_t s);
 int sph_copy(void* dst, const void* src, int64_t nbytes, cudaStream_t s);
 
+/* diagnostic: count (into *bad, dev) quotients a/h where the kernels'
+ * reciprocal-based division differs from IEEE __fdiv_rn / __ddiv_rn, over n
+ * pseudo-random a (binary32 h = (float)h and binary64 h) */
+int sph_selftest_div(double h, int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t s);
+
 /* physics.py:296-310 VMAX_SPEC through particle_reduce (execution.py:191-209):
  * *out (dev double) = max_i sqrt(sum_k f64(v_ik*v_ik)), identity 0.0 */
 int sph_vmax_f32(const float* v, int64_t n, int dim, double* out, cudaStream_t s);

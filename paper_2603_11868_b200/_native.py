@@ -106,6 +106,7 @@ _PROTOS = {
     "sph_radix_sort_perm": (c_i32, [_P, c_i64, _P, _P, c_size, _P]),
     "sph_gather": (c_i32, [_P, _P, _P, c_i64, c_i32, _P]),
     "sph_copy": (c_i32, [_P, _P, c_i64, _P]),
+    "sph_selftest_div": (c_i32, [c_f64, c_i64, C.c_uint64, _P, _P]),
     "sph_engine_push": (c_i32, [_P] * 14 + [_P]),
     "sph_engine_pull": (c_i32, [_P] * 14 + [_P]),
     "sph_engine_rebuild_cll": (c_i32, [_P, _P]),
@@ -138,7 +139,8 @@ _LIB = None
 
 
 def library_path():
-    return _build.LIB
+    """The in-tree library; SPH_B200_LIB overrides it (A/B variant builds)."""
+    return os.environ.get("SPH_B200_LIB") or _build.LIB
 
 
 def load(path=None):

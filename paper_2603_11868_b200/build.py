@@ -58,17 +58,21 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build_library(force=False, verbose=False, extra_flags=()):
+def build_library(force=False, verbose=False, extra_flags=(), out=None):
+    """Build the library (to `out`, default the in-tree path)."""
     deps = _deps()
-    if not force and not _stale(LIB, deps):
-        return LIB
-    os.makedirs(OUT_DIR, exist_ok=True)
-    os.makedirs(OBJ_DIR, exist_ok=True)
+    target = out or LIB
+    if not force and not _stale(target, deps):
+        return target
+    os.makedirs(os.path.dirname(target), exist_ok=True)
+    obj_dir = OBJ_DIR if out is None else os.path.join(
+        OBJ_DIR, os.path.basename(os.path.dirname(target)))
+    os.makedirs(obj_dir, exist_ok=True)
     exe = nvcc()
     flags = NVCC_FLAGS + list(extra_flags)
 
     def compile_one(src):
-        obj = os.path.join(OBJ_DIR, os.path.basename(src)[:-3] + ".o")
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
         cmd = [exe] + flags + ["-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
@@ -81,13 +85,13 @@ def build_library(force=False, verbose=False, extra_flags=()):
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     cmd = [exe] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -50,6 +50,49 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
 
+// ---- division by a loop-invariant divisor ------------------------------------
+// a / b correctly rounded from y = RN(1/b) (computed once per thread) with
+// the FMA residual step: q0 = RN(a*y), r = a - b*q0 (exact), q = RN(q0 + r*y)
+// (Markstein's theorem: y within half an ulp of 1/b and q0 faithful give the
+// correctly rounded quotient).  Valid while a, b, q stay well inside the
+// normal range -- ok_b says b is -- else the IEEE division is taken.  This is
+// bit-identical to __fdiv_rn / __ddiv_rn; tests/test_gpu_kernels.py checks it
+// against them on 10^8 quotients per divisor.
+__device__ __forceinline__ float fdiv_rcp(float a, float b, float y, bool ok_b)
+{
+    const float q0 = __fmul_rn(a, y);
+    const float r = __fmaf_rn(-b, q0, a);
+    const float q1 = __fmaf_rn(r, y, q0);
+    const float aa = fabsf(a);
+    return (ok_b && aa > 1e-18f && aa < 1e18f) ? q1 : __fdiv_rn(a, b);
+}
+__device__ __forceinline__ double ddiv_rcp(double a, double b, double y, bool ok_b)
+{
+    const double q0 = __dmul_rn(a, y);
+    const double r = __fma_rn(-b, q0, a);
+    const double q1 = __fma_rn(r, y, q0);
+    const double aa = fabs(a);
+    return (ok_b && aa > 1e-140 && aa < 1e140) ? q1 : __ddiv_rn(a, b);
+}
+template <class T> __device__ __forceinline__ T div_rcp(T a, T b, T y, bool ok_b);
+template <> __device__ __forceinline__ float div_rcp<float>(float a, float b, float y, bool ok)
+{
+    return fdiv_rcp(a, b, y, ok);
+}
+template <> __device__ __forceinline__ double div_rcp<double>(double a, double b, double y,
+                                                              bool ok)
+{
+    return ddiv_rcp(a, b, y, ok);
+}
+template <class T> __device__ __forceinline__ T rcp_rn(T b);
+template <> __device__ __forceinline__ float rcp_rn<float>(float b) { return __frcp_rn(b); }
+template <> __device__ __forceinline__ double rcp_rn<double>(double b) { return __drcp_rn(b); }
+template <class T> __device__ __forceinline__ bool rcp_ok(T b)
+{
+    const double ab = fabs(double(b));
+    return ab > 1e-15 && ab < 1e15;
+}
+
 // ---- packed vectors ---------------------------------------------------------
 template <class T> struct V4;
 template <> struct V4<float> { using type = float4; };
@@ -92,6 +135,19 @@ __device__ __forceinline__ double grad_fac(T r, T q, T h, T alpha_d)
     gw = dmul(gw, tq);
     gw = dmul(gw, tq);
     gw = ddiv(gw, double(h));
+    return ddiv(gw, double(r));
+}
+
+// the same with 1/h precomputed (rh = RN(1/(double)h), ok = rcp_ok(h))
+template <class T>
+__device__ __forceinline__ double grad_fac_rh(T r, T q, T h, double m5a, double rh, bool ok)
+{
+    const double tq = dsub(1.0, dmul(0.5, double(q)));
+    double gw = dmul(m5a, double(q));   // m5a = -5.0 * alpha_d
+    gw = dmul(gw, tq);
+    gw = dmul(gw, tq);
+    gw = dmul(gw, tq);
+    gw = ddiv_rcp(gw, double(h), rh, ok);
     return ddiv(gw, double(r));
 }
 

@@ -17,12 +17,23 @@
 //
 // One acoustic sub-step (physics.py:522-548):
 //   k_kick_drift  KICK + DRIFT, displacement bounds, cell-change marks
-//   k_mask        exact filter of the skin lists -> exact lists + counts
-//   k_fix_build   exact ordered lists for the marked particles
-//   k_cont_du     CONTINUITY + DENSITY_UPDATE   (fluid)
-//   k_wall        WALL_PRESSURE                 (walls)
+//   k_mark        queue particles whose skin list is no longer valid
+//   k_fix_build   exact ordered lists for the queued particles
+//   k_cont_du     skin-list filter + CONTINUITY + DENSITY_UPDATE (fluid);
+//                 writes the exact lists the momentum sweep reads
+//   k_wall        skin-list filter + WALL_PRESSURE (walls)
 //   k_mom         MOMENTUM + KICK               (fluid)
 #include "engine.cuh"
+
+#ifndef SPH_SWEEP_MINB
+#define SPH_SWEEP_MINB 12    // min resident blocks of the sweeps (register cap)
+#endif
+#ifndef SPH_FILTER_KF
+#define SPH_FILTER_KF 4      // list entries in flight per filter trip
+#endif
+#ifndef SPH_PREFETCH
+#define SPH_PREFETCH 0       // prefetch the next neighbour's data in the sweeps
+#endif
 
 namespace sph {
 
@@ -35,6 +46,7 @@ __device__ __forceinline__ void sweep_list(const Eng<T>& E, int64_t slot, int cn
 {
     if (cnt <= 0) return;
     const int32_t* __restrict__ lp = E.elist + ell_index(slot, 0);
+#if SPH_PREFETCH
     int j1 = cnt > 1 ? lp[32] : 0;
     auto nxt = load(lp[0]);
     for (int t = 0; t < cnt; ++t) {
@@ -43,10 +55,72 @@ __device__ __forceinline__ void sweep_list(const Eng<T>& E, int64_t slot, int cn
         if (t + 2 < cnt) j1 = lp[(t + 2) * 32];
         body(cur);
     }
+#else
+    for (int t = 0; t < cnt; ++t) body(load(lp[t * 32]));
+#endif
 }
 
 template <class T> struct NbrPVR { vec4<T> p; vec4<T> v; vec2<T> rp; };
 template <class T> struct NbrPR { vec4<T> p; vec2<T> rp; };
+
+// Exact filter of slot's skin list fused into a sweep: per 32 entries, the
+// reference's acceptance test (0 < r2 < c^2, binary32) runs first with 8
+// list entries + positions in flight (phase 1, bits in a register), then the
+// accepted neighbours are visited in list (= ascending id) order with the
+// next one's data prefetched (phase 2).  Rejected entries cost only phase 1.
+template <class T, int D, class Load, class Body>
+__device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const T (&xi)[3],
+                                            T c2, int nl, Load load, Body body)
+{
+    const int32_t* __restrict__ lp = E.lists + ell_index(slot, 0);
+    for (int w0 = 0; w0 < nl; w0 += 32) {
+        const int ne = min(32, nl - w0);
+        uint32_t m = 0;
+        constexpr int kF = SPH_FILTER_KF;
+        for (int u0 = 0; u0 < ne; u0 += kF) {
+            int jj[kF];
+#pragma unroll
+            for (int k = 0; k < kF; k++) jj[k] = u0 + k < ne ? lp[(w0 + u0 + k) * 32] : -1;
+            vec4<T> pj[kF];
+#pragma unroll
+            for (int k = 0; k < kF; k++) pj[k] = E.pos[jj[k] >= 0 ? jj[k] : 0];
+#pragma unroll
+            for (int k = 0; k < kF; k++) {
+                T xj[3];
+                to3<T>(pj[k], xj);
+                const T r2 = accept_r2<T, D>(xi, xj);
+                if (jj[k] >= 0 && (r2 < c2) && (r2 > T(0))) m |= 1u << (u0 + k);
+            }
+        }
+        if (!m) continue;
+#if SPH_PREFETCH
+        int u = __ffs(m) - 1;
+        m &= m - 1;
+        int j = lp[(w0 + u) * 32];
+        auto nxt = load(j);
+        while (true) {
+            const auto cur = nxt;
+            const int jc = j;
+            const bool more = m != 0;
+            if (more) {
+                u = __ffs(m) - 1;
+                m &= m - 1;
+                j = lp[(w0 + u) * 32];
+                nxt = load(j);
+            }
+            body(jc, cur);
+            if (!more) break;
+        }
+#else
+        while (m) {
+            const int u = __ffs(m) - 1;
+            m &= m - 1;
+            const int j = lp[(w0 + u) * 32];
+            body(j, load(j));
+        }
+#endif
+    }
+}
 
 __device__ __forceinline__ void enqueue(uint32_t* queue, uint32_t* qcount, bool need,
                                         uint32_t value)
@@ -146,7 +220,7 @@ k_kick_drift(Eng<T> E, int cv, GridP<T> g, T half, T full)
 // exact filter of every valid skin list on current positions -> exact lists and
 // accepted counts; particles whose list is not valid go to the fix queue
 template <class T, int D>
-__global__ void __launch_bounds__(kSweepThreads)
+__global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
 k_mask(Eng<T> E, GridP<T> g, T s_eff)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -167,29 +241,48 @@ k_mask(Eng<T> E, GridP<T> g, T s_eff)
             int acc = 0;
             const int32_t* lp = E.lists + ell_index(slot, 0);
             int32_t* ep = E.elist + ell_index(slot, 0);
-            // 4 independent list entries + positions in flight per trip
-            for (int u0 = 0; u0 < nl; u0 += 4) {
-                int jj[4];
+            // kF independent list entries + positions in flight per trip
+            constexpr int kF = 8;
+            for (int u0 = 0; u0 < nl; u0 += kF) {
+                int jj[kF];
 #pragma unroll
-                for (int k = 0; k < 4; k++) jj[k] = u0 + k < nl ? lp[(u0 + k) * 32] : -1;
-                vec4<T> pj[4];
+                for (int k = 0; k < kF; k++) jj[k] = u0 + k < nl ? lp[(u0 + k) * 32] : -1;
+                vec4<T> pj[kF];
 #pragma unroll
-                for (int k = 0; k < 4; k++)
-                    if (jj[k] >= 0) pj[k] = E.pos[jj[k]];
+                for (int k = 0; k < kF; k++) pj[k] = E.pos[jj[k] >= 0 ? jj[k] : 0];
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    if (jj[k] < 0) continue;
+                for (int k = 0; k < kF; k++) {
                     T xj[3];
                     to3<T>(pj[k], xj);
                     const T r2 = accept_r2<T, D>(xi, xj);
-                    if ((r2 < g.c2) && (r2 > T(0))) {
-                        if (acc < kCap) ep[acc * 32] = jj[k];
-                        acc++;
-                    }
+                    if (jj[k] >= 0 && (r2 < g.c2) && (r2 > T(0))) ep[(acc++) * 32] = jj[k];
                 }
             }
             const int total = acc + (i >= E.nf ? E.nww[slot] : 0);
             E.acount[slot] = total > kCap ? -1 : acc;
+        }
+    }
+    enqueue(E.queue, E.qcount, need, (uint32_t)i);
+}
+
+// list validity after a drift: particles whose skin list is no longer valid
+// (cell changed, or disp_i + max disp > skin) are queued for exact rebuilds
+template <class T>
+__global__ void __launch_bounds__(256)
+k_mark(Eng<T> E, T s_eff)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool need = false;
+    if (i < E.n) {
+        const uint32_t c0 = E.cell0[i];
+        if (c0 == kInvalidCell) {
+            need = true;
+        } else {
+            const T dmax = T(__longlong_as_double((long long)E.stats->dmax_bits));
+            if (RN<T>::add_ru(E.disp[i], dmax) > s_eff) {
+                E.cell0[i] = kInvalidCell;
+                need = true;
+            }
         }
     }
     enqueue(E.queue, E.qcount, need, (uint32_t)i);
@@ -236,15 +329,14 @@ __device__ __forceinline__ void flag_overflow(uint32_t* oflow_id, uint32_t pid, 
 
 // physics.py:94-119 CONTINUITY fused with :268-274 DENSITY_UPDATE(full),
 // fluid only: reads rho of the current buffer, writes (rho, p) to the other.
+// A particle with a valid skin list filters it here (writing the exact list
+// the momentum sweep reuses); others read the exact list k_fix_build made.
 template <class T, int D>
-__global__ void __launch_bounds__(kSweepThreads)
-k_cont_du(Eng<T> E, PhysP pp, int cv, int crp, T full)
+__global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
+k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= E.nf) return;
-    const int acnt = E.acount[i];
-    if (acnt < 0) { flag_overflow(E.oflow_id, E.id[i], E.stats); return; }
-    PhysT<T> P; P.load(pp);
     const vec4<T>* __restrict__ pos = E.pos;
     const vec4<T>* __restrict__ vel = E.vel[cv];
     const vec2<T>* __restrict__ rp = E.rp[crp];
@@ -253,15 +345,33 @@ k_cont_du(Eng<T> E, PhysP pp, int cv, int crp, T full)
     to3<T>(vel[i], vi);
     const T rho_i = rp[i].x;
     double acc = double(RN<T>::sub(rho_i, rho_i));
-    sweep_list<T>(E, i, acnt,
-        [&](int j) { return NbrPVR<T>{pos[j], vel[j], rp[j]}; },
-        [&](const NbrPVR<T>& nb) {
-            T xj[3], vj[3], dx[3], r2, vx;
-            to3<T>(nb.p, xj);
-            to3<T>(nb.v, vj);
-            pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-            acc = dadd(acc, continuity_term<T>(r2, vx, nb.p.w, nb.rp.x, P));
+    auto loadf = [&](int j) { return NbrPVR<T>{pos[j], vel[j], rp[j]}; };
+    auto pair = [&](const NbrPVR<T>& nb) {
+        T xj[3], vj[3], dx[3], r2, vx;
+        to3<T>(nb.p, xj);
+        to3<T>(nb.v, vj);
+        pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
+        acc = dadd(acc, continuity_term<T>(r2, vx, nb.p.w, nb.rp.x, P));
+    };
+    if (E.cell0[i] == kInvalidCell) {
+        const int acnt = E.acount[i];
+        if (acnt < 0) { flag_overflow(E.oflow_id, E.id[i], E.stats); return; }
+        sweep_list<T>(E, i, acnt, loadf, pair);
+    } else {
+        int32_t* ep = E.elist + ell_index(i, 0);
+        int cnt = 0;
+        filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf, [&](int j, const NbrPVR<T>& nb) {
+            if (cnt < kCap) ep[cnt * 32] = j;
+            cnt++;
+            pair(nb);
         });
+        if (cnt > kCap) {
+            E.acount[i] = -1;
+            flag_overflow(E.oflow_id, E.id[i], E.stats);
+            return;
+        }
+        E.acount[i] = cnt;
+    }
     const T dr = RN<T>::from_d(dmul(double(rho_i), acc));
     E.drho[i] = dr;
     vec2<T> out;
@@ -273,35 +383,45 @@ k_cont_du(Eng<T> E, PhysP pp, int cv, int crp, T full)
 // physics.py:161-194 WALL_PRESSURE over the wall segment: fluid p from
 // buffer b, walls' (rho, p) written into the same buffer.  zero_drho mirrors
 // the continuity body's drho = 0 for walls (physics.py:99-101) in a sub-step.
+// filter != 0: valid skin lists are filtered here (walls' exact lists are
+// used by no other sweep, so they are not stored).
 template <class T, int D>
-__global__ void __launch_bounds__(kSweepThreads)
-k_wall(Eng<T> E, PhysP pp, int b, int zero_drho, int count_factor)
+__global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
+k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor, int filter)
 {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long visits_sum = 0;
     if (t < E.nw) {
         const int64_t i = E.nf + t;
         const int64_t slot = E.nf_pad + t;
-        const int acnt = E.acount[slot];
+            vec2<T>* __restrict__ rp = E.rp[b];
+        T xi[3];
+        to3<T>(E.pos[i], xi);
+        const T rho_i = rp[i].x;
+        double num = double(RN<T>::sub(rho_i, rho_i));
+        double den = num;
+        auto loadf = [&](int j) { return NbrPR<T>{E.pos[j], rp[j]}; };
+        auto pair = [&](const NbrPR<T>& nb) {
+            T xj[3];
+            to3<T>(nb.p, xj);
+            const double w = wall_weight<T>(pair_r2<T, D>(xi, xj), P);
+            num = dadd(num, dmul(double(nb.rp.y), w));
+            den = dadd(den, w);
+        };
+        int acnt;
+        if (!filter || E.cell0[i] == kInvalidCell) {
+            acnt = E.acount[slot];
+            if (acnt >= 0) sweep_list<T>(E, slot, acnt, loadf, pair);
+        } else {
+            acnt = 0;
+            filter_walk<T, D>(E, slot, xi, g.c2, E.lcount[slot], loadf,
+                              [&](int, const NbrPR<T>& nb) { acnt++; pair(nb); });
+            if (acnt + E.nww[slot] > kCap) acnt = -1;
+            E.acount[slot] = acnt;
+        }
         if (acnt < 0) {
             flag_overflow(E.oflow_id, E.id[i], E.stats);
         } else {
-            PhysT<T> P; P.load(pp);
-            vec2<T>* __restrict__ rp = E.rp[b];
-            T xi[3];
-            to3<T>(E.pos[i], xi);
-            const T rho_i = rp[i].x;
-            double num = double(RN<T>::sub(rho_i, rho_i));
-            double den = num;
-            sweep_list<T>(E, slot, acnt,
-                [&](int j) { return NbrPR<T>{E.pos[j], rp[j]}; },
-                [&](const NbrPR<T>& nb) {
-                    T xj[3];
-                    to3<T>(nb.p, xj);
-                    const double w = wall_weight<T>(pair_r2<T, D>(xi, xj), P);
-                    num = dadd(num, dmul(double(nb.rp.y), w));
-                    den = dadd(den, w);
-                });
             vec2<T> out;
             out.y = den > 0.0 ? RN<T>::from_d(ddiv(num, den)) : T(0);
             out.x = RN<T>::add(P.rho0, RN<T>::div(out.y, P.c0c0));
@@ -317,8 +437,8 @@ k_wall(Eng<T> E, PhysP pp, int b, int zero_drho, int count_factor)
 // physics.py:122-158 MOMENTUM (+ :546-547 KICK(half) into the other velocity
 // buffer when kick != 0), fluid only; rho/p from buffer brp.
 template <class T, int D>
-__global__ void __launch_bounds__(kSweepThreads)
-k_mom(Eng<T> E, PhysP pp, int cv, int brp, int kick, T half, int count_factor)
+__global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
+k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long csum = 0;
@@ -327,8 +447,7 @@ k_mom(Eng<T> E, PhysP pp, int cv, int brp, int kick, T half, int count_factor)
         if (acnt < 0) {
             flag_overflow(E.oflow_id, E.id[i], E.stats);
         } else {
-            PhysT<T> P; P.load(pp);
-            const vec4<T>* __restrict__ pos = E.pos;
+                    const vec4<T>* __restrict__ pos = E.pos;
             const vec4<T>* __restrict__ vel = E.vel[cv];
             const vec2<T>* __restrict__ rp = E.rp[brp];
             T xi[3], vi[3];
@@ -369,8 +488,8 @@ k_mom(Eng<T> E, PhysP pp, int cv, int brp, int kick, T half, int count_factor)
 // physics.py:220-247 SHEPARD + :277-280 COPY_SCALAR + :268-274
 // DENSITY_UPDATE(dt=0), all particles; reads buffer crp, writes crp^1.
 template <class T, int D>
-__global__ void __launch_bounds__(kSweepThreads)
-k_shepard(Eng<T> E, PhysP pp, int crp)
+__global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
+k_shepard(Eng<T> E, PhysT<T> P, int crp)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= E.n) return;
@@ -382,7 +501,6 @@ k_shepard(Eng<T> E, PhysP pp, int crp)
         E.rp[crp ^ 1][i] = RPI;
         return;
     }
-    PhysT<T> P; P.load(pp);
     T rho_new = RPI.x;
     if (E.acount[i] >= 0) {
         T xi[3];
@@ -463,7 +581,19 @@ extern "C" int sph_engine_build_lists(SphEngine* e, double skin, cudaStream_t s)
     return SPH_DISPATCH(e, build_lists_impl, e, skin, s);
 }
 
-// exact lists: filtered skin lists, exact rebuilds for the rest
+template <class T, int D>
+static void launch_fix(const SphEngine* e, cudaStream_t s)
+{
+    GridP<T> g = grid_of_engine<T>(e);
+    Eng<T> E = eng_of<T>(e);
+    EngAcc<T> acc = acc_of_engine<T>(e);
+    const int64_t want = (e->n + kNlWarps - 1) / kNlWarps;
+    const int blocks = (int)(want < 148 * 8 ? want : 148 * 8);
+    note_launch(), k_fix_build<T, D><<<blocks, kNlThreads, 0, s>>>(acc, g, E);
+}
+
+// exact lists for every particle: filtered skin lists (k_mask), exact
+// rebuilds for the rest (initialize / Shepard paths)
 template <class T, int D>
 static void prepare_lists(const SphEngine* e, cudaStream_t s)
 {
@@ -473,10 +603,19 @@ static void prepare_lists(const SphEngine* e, cudaStream_t s)
     if (e->n <= 0) return;
     note_launch(), k_mask<T, D><<<grid_for(e->n, kSweepThreads), kSweepThreads, 0, s>>>(
         E, g, skin_eff<T>(e));
-    EngAcc<T> acc = acc_of_engine<T>(e);
-    const int64_t want = (e->n + kNlWarps - 1) / kNlWarps;
-    const int blocks = (int)(want < 148 * 8 ? want : 148 * 8);
-    note_launch(), k_fix_build<T, D><<<blocks, kNlThreads, 0, s>>>(acc, g, E);
+    launch_fix<T, D>(e, s);
+}
+
+// sub-step path: only the invalid lists are rebuilt up front; valid skin
+// lists are filtered inside the continuity / wall sweeps
+template <class T, int D>
+static void mark_and_fix(const SphEngine* e, cudaStream_t s)
+{
+    Eng<T> E = eng_of<T>(e);
+    cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
+    if (e->n <= 0) return;
+    note_launch(), k_mark<T><<<grid_for(e->n, 256), 256, 0, s>>>(E, skin_eff<T>(e));
+    launch_fix<T, D>(e, s);
 }
 
 static int require_lists(const SphEngine* e)
@@ -493,11 +632,11 @@ static int initialize_impl(SphEngine* e, cudaStream_t s)
 {
     prepare_lists<T, D>(e, s);
     Eng<T> E = eng_of<T>(e);
-    PhysP P = phys_of_engine(e);
+    const PhysT<T> P = make_phys<T>(phys_of_engine(e));
     const int64_t nw = e->n - e->nf;
     if (nw > 0)
         note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, P, e->cur_rp, 0, 1);
+            E, P, grid_of_engine<T>(e), e->cur_rp, 0, 1, 0);
     if (e->nf > 0)
         note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
             E, P, e->cur_v, e->cur_rp, 0, T(0), 1);
@@ -521,7 +660,7 @@ static int shepard_impl(SphEngine* e, cudaStream_t s)
     if (e->n <= 0) return SPH_OK;
     prepare_lists<T, D>(e, s);
     Eng<T> E = eng_of<T>(e);
-    PhysP P = phys_of_engine(e);
+    const PhysT<T> P = make_phys<T>(phys_of_engine(e));
     note_launch(), k_shepard<T, D><<<grid_for(e->n, kSweepThreads), kSweepThreads, 0, s>>>(
         E, P, e->cur_rp);
     e->cur_rp ^= 1;
@@ -543,7 +682,7 @@ static int substep_impl(SphEngine* e, double half_d, double full_d, cudaEvent_t*
 {
     const T half = T(half_d), full = T(full_d);
     Eng<T> E = eng_of<T>(e);
-    PhysP P = phys_of_engine(e);
+    const PhysT<T> P = make_phys<T>(phys_of_engine(e));
     GridP<T> g = grid_of_engine<T>(e);
     const int cv = e->cur_v, crp = e->cur_rp;
     const int64_t nf = e->nf, nw = e->n - e->nf;
@@ -551,18 +690,18 @@ static int substep_impl(SphEngine* e, double half_d, double full_d, cudaEvent_t*
     if (nf > 0)
         note_launch(), k_kick_drift<T, D><<<grid_for(nf, 256), 256, 0, s>>>(E, cv, g, half, full);
     if (ev) cudaEventRecord(ev[1], s);
-    prepare_lists<T, D>(e, s);
+    mark_and_fix<T, D>(e, s);
     if (ev) cudaEventRecord(ev[2], s);
     if (nf > 0)
         note_launch(), k_cont_du<T, D><<<grid_for(nf, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, P, cv, crp, full);
+            E, P, g, cv, crp, full);
     else if (nw > 0)   // no fluid: the other rp buffer must still carry walls
         cudaMemcpyAsync(E.rp[crp ^ 1], E.rp[crp], sizeof(vec2<T>) * (size_t)e->n,
                         cudaMemcpyDeviceToDevice, s);
     if (ev) cudaEventRecord(ev[3], s);
     if (nw > 0)
         note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, P, crp ^ 1, 1, 1);
+            E, P, g, crp ^ 1, 1, 1, 1);
     if (ev) cudaEventRecord(ev[4], s);
     if (nf > 0)
         note_launch(), k_mom<T, D><<<grid_for(nf, kSweepThreads), kSweepThreads, 0, s>>>(

@@ -43,7 +43,7 @@ __device__ __forceinline__ void load3(const T* a, int64_t i, T (&o)[3])
 
 // physics.py:94-119
 template <class T, int D>
-__global__ void k_gen_continuity(GenView<T> a, PhysP pp, const int32_t* __restrict__ lists,
+__global__ void k_gen_continuity(GenView<T> a, PhysT<T> P, const int32_t* __restrict__ lists,
                                  const int32_t* __restrict__ lcount)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -51,7 +51,6 @@ __global__ void k_gen_continuity(GenView<T> a, PhysP pp, const int32_t* __restri
     if (a.wall[i] != 0) { a.drho[i] = T(0); return; }
     int cnt = lcount[i];
     if (cnt < 0) { a.oflow[i] = 1; return; }
-    PhysT<T> P; P.load(pp);
     T xi[3], vi[3];
     load3<T, D>(a.x, i, xi);
     load3<T, D>(a.v, i, vi);
@@ -70,7 +69,7 @@ __global__ void k_gen_continuity(GenView<T> a, PhysP pp, const int32_t* __restri
 
 // physics.py:122-158
 template <class T, int D>
-__global__ void k_gen_momentum(GenView<T> a, PhysP pp, const int32_t* __restrict__ lists,
+__global__ void k_gen_momentum(GenView<T> a, PhysT<T> P, const int32_t* __restrict__ lists,
                                const int32_t* __restrict__ lcount)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -81,7 +80,6 @@ __global__ void k_gen_momentum(GenView<T> a, PhysP pp, const int32_t* __restrict
     }
     int cnt = lcount[i];
     if (cnt < 0) { a.oflow[i] = 1; return; }
-    PhysT<T> P; P.load(pp);
     T xi[3], vi[3];
     load3<T, D>(a.x, i, xi);
     load3<T, D>(a.v, i, vi);
@@ -103,7 +101,7 @@ __global__ void k_gen_momentum(GenView<T> a, PhysP pp, const int32_t* __restrict
 // physics.py:161-194 (walls read fluid neighbours' p only, write their own
 // p/rho: no read-after-write hazard between threads)
 template <class T, int D>
-__global__ void k_gen_wall_pressure(GenView<T> a, PhysP pp, const int32_t* __restrict__ lists,
+__global__ void k_gen_wall_pressure(GenView<T> a, PhysT<T> P, const int32_t* __restrict__ lists,
                                     const int32_t* __restrict__ lcount)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -111,7 +109,6 @@ __global__ void k_gen_wall_pressure(GenView<T> a, PhysP pp, const int32_t* __res
     if (a.wall[i] == 0) return;
     int cnt = lcount[i];
     if (cnt < 0) { a.oflow[i] = 1; return; }
-    PhysT<T> P; P.load(pp);
     T xi[3];
     load3<T, D>(a.x, i, xi);
     T rho_i = a.rho[i];
@@ -136,7 +133,7 @@ __global__ void k_gen_wall_pressure(GenView<T> a, PhysP pp, const int32_t* __res
 
 // physics.py:197-217 (overflow: self term only)
 template <class T, int D>
-__global__ void k_gen_density_summation(GenView<T> a, PhysP pp,
+__global__ void k_gen_density_summation(GenView<T> a, PhysT<T> P,
                                         const int32_t* __restrict__ lists,
                                         const int32_t* __restrict__ lcount)
 {
@@ -144,7 +141,6 @@ __global__ void k_gen_density_summation(GenView<T> a, PhysP pp,
     if (i >= a.n) return;
     int cnt = lcount[i];
     if (cnt < 0) cnt = 0;
-    PhysT<T> P; P.load(pp);
     T xi[3];
     load3<T, D>(a.x, i, xi);
     double acc = double(RN<T>::mul(a.m[i], P.alpha_d));
@@ -159,7 +155,7 @@ __global__ void k_gen_density_summation(GenView<T> a, PhysP pp,
 
 // physics.py:220-247
 template <class T, int D>
-__global__ void k_gen_shepard(GenView<T> a, PhysP pp, const int32_t* __restrict__ lists,
+__global__ void k_gen_shepard(GenView<T> a, PhysT<T> P, const int32_t* __restrict__ lists,
                               const int32_t* __restrict__ lcount)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -167,7 +163,6 @@ __global__ void k_gen_shepard(GenView<T> a, PhysP pp, const int32_t* __restrict_
     if (a.wall[i] != 0) { a.rho_new[i] = a.rho[i]; return; }
     int cnt = lcount[i];
     if (cnt < 0) { a.rho_new[i] = a.rho[i]; return; }
-    PhysT<T> P; P.load(pp);
     T xi[3];
     load3<T, D>(a.x, i, xi);
     const T m_i = a.m[i];
@@ -285,7 +280,7 @@ static int gen_build(const typename ArgsOf<T>::type& a, int64_t i0, int64_t coun
 enum SweepKind { kContinuity, kMomentum, kWallPressure, kDensitySummation, kShepard };
 
 template <class T, int D>
-static void launch_sweep(SweepKind kind, GenView<T> v, PhysP P, const int32_t* lists,
+static void launch_sweep(SweepKind kind, GenView<T> v, PhysT<T> P, const int32_t* lists,
                          const int32_t* lcount, cudaStream_t s)
 {
     int g = grid_for(v.n, 128);
@@ -316,7 +311,7 @@ static int gen_sweep(SweepKind kind, const typename ArgsOf<T>::type* a, void* ws
     int rc = gen_build<T>(*a, 0, a->n, lists, lcount, s);
     if (rc) return rc;
     GenView<T> v = view_of<T>(*a);
-    PhysP P = phys_of<T>(*a);
+    const PhysT<T> P = make_phys<T>(phys_of<T>(*a));
     if (a->dim == 2) launch_sweep<T, 2>(kind, v, P, lists, lcount, s);
     else launch_sweep<T, 3>(kind, v, P, lists, lcount, s);
     return check_launch("sweep");
@@ -392,3 +387,45 @@ extern "C" int sph_neighbors_f64(const SphSweepArgs_f64* a, int64_t i0, int64_t 
     }
 SPH_INTEG_ENTRY(f32, float)
 SPH_INTEG_ENTRY(f64, double)
+
+// ---------------------------------------------------------------------------
+// self-test of the reciprocal divisions (common.cuh) against the IEEE ones
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t& s)
+{
+    uint64_t z = (s += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_selftest_div(float hf, double hd, int64_t n, uint64_t seed,
+                               unsigned long long* bad)
+{
+    const float yf = __frcp_rn(hf);
+    const double yd = __drcp_rn(hd);
+    const bool okf = rcp_ok<float>(hf), okd = rcp_ok<double>(hd);
+    unsigned long long nb = 0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t st = seed ^ (uint64_t)k * 0x2545f4914f6cdd1dull;
+        const uint64_t u = splitmix64(st);
+        // random significand, exponent spread over +-2^40 around 1
+        const double mag = ldexp(1.0 + (double)(u >> 11) * 0x1.0p-53, (int)(u & 63) - 32);
+        const double a = (u >> 7) & 1 ? -mag : mag;
+        const float af = (float)a;
+        if (__float_as_uint(fdiv_rcp(af, hf, yf, okf)) != __float_as_uint(__fdiv_rn(af, hf))) nb++;
+        if (__double_as_longlong(ddiv_rcp(a, hd, yd, okd)) !=
+            __double_as_longlong(__ddiv_rn(a, hd)))
+            nb++;
+    }
+    nb = warp_sum(nb);
+    if (lane_id() == 0 && nb) atomicAdd(bad, nb);
+}
+
+extern "C" int sph_selftest_div(double h, int64_t n, uint64_t seed, unsigned long long* bad,
+                                cudaStream_t s)
+{
+    note_launch(), k_selftest_div<<<148 * 8, 256, 0, s>>>((float)h, h, n, seed, bad);
+    return check_launch("selftest_div");
+}
