@@ -45,19 +45,18 @@ __device__ __forceinline__ void sweep_list(const Eng<T>& E, int64_t slot, int cn
                                            Body body)
 {
     if (cnt <= 0) return;
-    const int32_t* __restrict__ lp = E.elist + ell_index(slot, 0);
-#if SPH_PREFETCH
-    int j1 = cnt > 1 ? lp[32] : 0;
-    auto nxt = load(lp[0]);
-    for (int t = 0; t < cnt; ++t) {
-        const auto cur = nxt;
-        if (t + 1 < cnt) nxt = load(j1);
-        if (t + 2 < cnt) j1 = lp[(t + 2) * 32];
-        body(cur);
+    // quad-ELL: 4 entries per int4; the next quad is requested before the
+    // current one is processed, so the list stream never stalls a pair
+    const int4* __restrict__ q4 = reinterpret_cast<const int4*>(E.elist + ell_base(slot));
+    int4 qn = q4[0];
+    for (int t0 = 0; t0 < cnt; t0 += 4) {
+        const int4 q = qn;
+        if (t0 + 4 < cnt) qn = q4[((t0 >> 2) + 1) * 32];
+        body(load(q.x));
+        if (t0 + 1 < cnt) body(load(q.y));
+        if (t0 + 2 < cnt) body(load(q.z));
+        if (t0 + 3 < cnt) body(load(q.w));
     }
-#else
-    for (int t = 0; t < cnt; ++t) body(load(lp[t * 32]));
-#endif
 }
 
 template <class T> struct NbrPVR { vec4<T> p; vec4<T> v; vec2<T> rp; };
@@ -72,15 +71,16 @@ template <class T, int D, class Load, class Body>
 __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const T (&xi)[3],
                                             T c2, int nl, Load load, Body body)
 {
-    const int32_t* __restrict__ lp = E.lists + ell_index(slot, 0);
+    const int32_t* __restrict__ lp = E.lists + ell_base(slot);
+    const int4* __restrict__ q4 = reinterpret_cast<const int4*>(lp);
     for (int w0 = 0; w0 < nl; w0 += 32) {
         const int ne = min(32, nl - w0);
         uint32_t m = 0;
-        constexpr int kF = SPH_FILTER_KF;
-        for (int u0 = 0; u0 < ne; u0 += kF) {
-            int jj[kF];
-#pragma unroll
-            for (int k = 0; k < kF; k++) jj[k] = u0 + k < ne ? lp[(w0 + u0 + k) * 32] : -1;
+        for (int u0 = 0; u0 < ne; u0 += 4) {
+            const int4 q = q4[((w0 + u0) >> 2) * 32];
+            int jj[4] = {q.x, u0 + 1 < ne ? q.y : -1, u0 + 2 < ne ? q.z : -1,
+                         u0 + 3 < ne ? q.w : -1};
+            constexpr int kF = 4;
             vec4<T> pj[kF];
 #pragma unroll
             for (int k = 0; k < kF; k++) pj[k] = E.pos[jj[k] >= 0 ? jj[k] : 0];
@@ -96,7 +96,7 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
 #if SPH_PREFETCH
         int u = __ffs(m) - 1;
         m &= m - 1;
-        int j = lp[(w0 + u) * 32];
+        int j = lp[ell_off(w0 + u)];
         auto nxt = load(j);
         while (true) {
             const auto cur = nxt;
@@ -105,7 +105,7 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
             if (more) {
                 u = __ffs(m) - 1;
                 m &= m - 1;
-                j = lp[(w0 + u) * 32];
+                j = lp[ell_off(w0 + u)];
                 nxt = load(j);
             }
             body(jc, cur);
@@ -115,7 +115,7 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
         while (m) {
             const int u = __ffs(m) - 1;
             m &= m - 1;
-            const int j = lp[(w0 + u) * 32];
+            const int j = lp[ell_off(w0 + u)];
             body(j, load(j));
         }
 #endif
@@ -239,23 +239,22 @@ k_mask(Eng<T> E, GridP<T> g, T s_eff)
             to3<T>(E.pos[i], xi);
             const int nl = E.lcount[slot];
             int acc = 0;
-            const int32_t* lp = E.lists + ell_index(slot, 0);
-            int32_t* ep = E.elist + ell_index(slot, 0);
-            // kF independent list entries + positions in flight per trip
-            constexpr int kF = 8;
-            for (int u0 = 0; u0 < nl; u0 += kF) {
-                int jj[kF];
+            const int4* q4 = reinterpret_cast<const int4*>(E.lists + ell_base(slot));
+            int32_t* ep = E.elist + ell_base(slot);
+            // one quad of list entries + 4 positions in flight per trip
+            for (int u0 = 0; u0 < nl; u0 += 4) {
+                const int4 q = q4[(u0 >> 2) * 32];
+                const int jj[4] = {q.x, u0 + 1 < nl ? q.y : -1, u0 + 2 < nl ? q.z : -1,
+                                   u0 + 3 < nl ? q.w : -1};
+                vec4<T> pj[4];
 #pragma unroll
-                for (int k = 0; k < kF; k++) jj[k] = u0 + k < nl ? lp[(u0 + k) * 32] : -1;
-                vec4<T> pj[kF];
+                for (int k = 0; k < 4; k++) pj[k] = E.pos[jj[k] >= 0 ? jj[k] : 0];
 #pragma unroll
-                for (int k = 0; k < kF; k++) pj[k] = E.pos[jj[k] >= 0 ? jj[k] : 0];
-#pragma unroll
-                for (int k = 0; k < kF; k++) {
+                for (int k = 0; k < 4; k++) {
                     T xj[3];
                     to3<T>(pj[k], xj);
                     const T r2 = accept_r2<T, D>(xi, xj);
-                    if (jj[k] >= 0 && (r2 < g.c2) && (r2 > T(0))) ep[(acc++) * 32] = jj[k];
+                    if (jj[k] >= 0 && (r2 < g.c2) && (r2 > T(0))) ep[ell_off(acc++)] = jj[k];
                 }
             }
             const int total = acc + (i >= E.nf ? E.nww[slot] : 0);
@@ -358,10 +357,10 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
         if (acnt < 0) { flag_overflow(E.oflow_id, E.id[i], E.stats); return; }
         sweep_list<T>(E, i, acnt, loadf, pair);
     } else {
-        int32_t* ep = E.elist + ell_index(i, 0);
+        int32_t* ep = E.elist + ell_base(i);
         int cnt = 0;
         filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf, [&](int j, const NbrPVR<T>& nb) {
-            if (cnt < kCap) ep[cnt * 32] = j;
+            if (cnt < kCap) ep[ell_off(cnt)] = j;
             cnt++;
             pair(nb);
         });

@@ -42,10 +42,17 @@ struct GridP {
     T o[3]; T cs; T c2; int s[3];
 };
 
-// tile-ELL: entry t of slot s at [s/32][t][s%32]
+// Quad tile-ELL: a 32-particle tile stores entry t of particle (lane) s at
+// [s/32][t/4][s%32][t%4], so one int4 load per lane fetches 4 consecutive
+// entries and a warp's int4 loads cover one contiguous 512-byte block.
+__device__ __forceinline__ size_t ell_base(int64_t slot)
+{
+    return (size_t)(slot >> 5) * (kCap * 32) + (size_t)(slot & 31) * 4;
+}
+__device__ __forceinline__ int ell_off(int t) { return (t >> 2) * 128 + (t & 3); }
 __device__ __forceinline__ size_t ell_index(int64_t slot, int t)
 {
-    return (size_t)(slot >> 5) * (kCap * 32) + (size_t)t * 32 + (size_t)(slot & 31);
+    return ell_base(slot) + (size_t)ell_off(t);
 }
 // filter-mask word w of slot s at [s/32][w][s%32]
 __device__ __forceinline__ size_t mask_index(int64_t slot, int w)
@@ -433,8 +440,10 @@ k_build_lists(const Acc acc, const GridP<T> g, int64_t first, int64_t count,
 #pragma unroll 4
     for (int q = 0; q < 32; q++) mc = max(mc, scnt[q]);
     int32_t* dst = lists + (size_t)((slot_first + t0) >> 5) * (kCap * 32);
-    for (int idx = threadIdx.x; idx < mc * 32; idx += kNlThreads)
-        dst[idx] = stage[(idx >> 5) * kStagePitch + (idx & 31)];
+    for (int idx = threadIdx.x; idx < mc * 32; idx += kNlThreads) {
+        const int t = idx >> 5, q = idx & 31;
+        dst[ell_off(t) + q * 4] = stage[t * kStagePitch + q];
+    }
     if (threadIdx.x < 32 && t0 + threadIdx.x < count)
         lcount[slot_first + t0 + threadIdx.x] = scnt[threadIdx.x];
 }

@@ -196,7 +196,10 @@ def neighbor_lists(policy, positions, ids, cll, cutoff, first=0, count=None):
         _native.check(rc, "neighbor_lists")
         c = cnts.cpu().numpy()[:count]
         ell = lists.cpu().numpy()
-    rows = ell.transpose(0, 2, 1).reshape(-1, NEIGHBOR_CAPACITY)[:count]
+    # quad tile-ELL [tile][t/4][lane][t%4] -> rows [particle][t]
+    tiles_ = ell.shape[0]
+    rows = (ell.reshape(tiles_, NEIGHBOR_CAPACITY // 4, 32, 4).transpose(0, 2, 1, 3)
+            .reshape(-1, NEIGHBOR_CAPACITY)[:count])
     return c, rows
 
 
