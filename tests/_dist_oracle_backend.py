@@ -1,0 +1,117 @@
+"""CPU oracle composition implementing the DistributedSimulation backend
+protocol (test infrastructure).  Every phase runs the oracle's restated
+reference bodies (oracle/sph_oracle.c) over the rank's owned + ghost
+particles; the decomposition logic under test is the product's
+(paper_2603_11868_b200/distributed.py)."""
+
+import numpy as np
+
+from oracle import oracle as O
+from paper_2603_11868_b200.distributed import FIELDS
+
+
+class OracleBackend:
+    def __init__(self, scalars, sing):
+        # scalars = force_args tail (cell_size, cutoff, h, alpha_d, c0, rho0,
+        # alpha_visc, eps_h2) in the run dtype; sing: rho0, c0, h, g
+        self.sc = scalars
+        self.sing = sing
+        self.f = None
+        self.n_own = 0
+        self._inter = 0
+        self._ovf = 0
+
+    def load(self, local, n_owned, grid):
+        self.f = {k: np.array(local[k], copy=True, order="C") for k in FIELDS}
+        self.n_own = n_owned
+        self.grid = grid
+        x = self.f["x"]
+        dt = x.dtype.type
+        self.origin = grid.origin.astype(x.dtype)
+        self.shape = grid.shape_array()
+        keys, _ = O.compute_keys(x, self.origin, dt(grid.cell_size), self.shape)
+        _, oob_own = O.compute_keys(x[:n_owned], self.origin, dt(grid.cell_size), self.shape)
+        self.offsets, self.pids = O.build_cll(keys, grid.cell_count)
+        return oob_own
+
+    def _force(self):
+        f = self.f
+        return (f["x"], f["v"], f["rho"], f["p"], f["m"], f["wall"], f["id"],
+                np.asarray(self.sing["g"], f["x"].dtype), self.offsets, self.pids,
+                self.origin, self.shape, f["drho"], f["dvdt"], f["nnb"], f["oflow"],
+                *self.sc)
+
+    def _ovf_check(self):
+        if self.f["oflow"][: self.n_own].any():
+            self._ovf = 1
+
+    def norms(self):
+        n = self.n_own
+        return [O.vmax(self.f["v"][:n]) if n else 0.0,
+                O.vmax(self.f["dvdt"][:n]) if n else 0.0]
+
+    def shepard(self):
+        f = self.f
+        dt = f["x"].dtype.type
+        sc = self.sc
+        O.sweep("shepard", (f["x"], f["rho"], f["m"], f["wall"], f["id"], self.offsets,
+                            self.pids, self.origin, self.shape, f["rho_scratch"],
+                            sc[0], sc[1], sc[2], sc[3]))
+        f["rho"][:] = f["rho_scratch"]
+        O.integrate("density_update", (f["rho"], f["p"], f["drho"], f["wall"], dt(0),
+                                       dt(self.sing["c0"]), dt(self.sing["rho0"])))
+
+    def kick_drift(self, half, full):
+        f = self.f
+        O.integrate("kick", (f["v"], f["dvdt"], f["wall"], half))
+        O.integrate("drift", (f["x"], f["v"], f["wall"], full))
+        self._half = half
+
+    def continuity_du(self, full):
+        f = self.f
+        dt = f["x"].dtype.type
+        O.sweep("continuity", self._force())
+        self._ovf_check()
+        O.integrate("density_update", (f["rho"], f["p"], f["drho"], f["wall"], full,
+                                       dt(self.sing["c0"]), dt(self.sing["rho0"])))
+
+    def wall_pressure(self, initial=False):
+        f = self.f
+        O.sweep("wall_pressure", self._force())
+        self._ovf_check()
+        n = self.n_own
+        w = f["wall"][:n] != 0
+        self._inter += int(f["nnb"][:n][w].sum())
+
+    def momentum_kick(self, half):
+        f = self.f
+        O.sweep("momentum", self._force())
+        self._ovf_check()
+        n = self.n_own
+        fl = f["wall"][:n] == 0
+        s = int(f["nnb"][:n][fl].sum())
+        self._inter += s if half is None else 2 * s
+        if half is not None:
+            O.integrate("kick", (f["v"], f["dvdt"], f["wall"], half))
+
+    def get(self, name, idx):
+        a = self.f[name]
+        return a if idx is None else a[idx]
+
+    def set(self, name, idx, vals):
+        self.f[name][idx] = vals
+
+    def counters(self):
+        out = (self._inter, self._ovf)
+        self._inter, self._ovf = 0, 0
+        return out
+
+    def stability(self):
+        n = self.n_own
+        if n == 0:
+            return np.inf, 0.0
+        v = self.f["v"][:n]
+        return float(self.f["rho"][:n].min()), float((v * v).sum(axis=1).max())
+
+    def export_owned(self):
+        return {k: self.f[k][: self.n_own].copy() for k in FIELDS}
