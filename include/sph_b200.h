@@ -184,8 +184,10 @@ typedef struct {
     /* sizes */
     int64_t n, nf, ncells; int32_t dim; int32_t key_bits;
     /* per-particle SoA, physical order (dev).  f32 run: float4/float2,
-     * f64 run: double4/double2 (reinterpret). pos.w == m. */
-    void* pos; void* vel[2]; void* rp[2]; void* dvdt; void* drho;
+     * f64 run: double4/double2 (reinterpret). pos.w == m; vel.w is scratch
+     * (m/rho of the sub-step's continuity sweep); rq = (rho, p/rho^2) of the
+     * sub-step's momentum sweep (library-maintained, no host meaning). */
+    void* pos; void* vel[2]; void* rp[2]; void* rq; void* dvdt; void* drho;
     uint32_t* id; uint32_t* nnb; uint32_t* refpos;
     /* by-id cold fields (dev) */
     void* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; void* vol_id;

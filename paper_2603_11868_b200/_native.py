@@ -74,7 +74,7 @@ class SphEngine(C.Structure):
     _fields_ = [
         ("n", c_i64), ("nf", c_i64), ("ncells", c_i64),
         ("dim", c_i32), ("key_bits", c_i32),
-        ("pos", P), ("vel", P * 2), ("rp", P * 2), ("dvdt", P), ("drho", P),
+        ("pos", P), ("vel", P * 2), ("rp", P * 2), ("rq", P), ("dvdt", P), ("drho", P),
         ("id", P), ("nnb", P), ("refpos", P),
         ("rho_scratch_id", P), ("oflow_id", P), ("wall_id", P), ("vol_id", P),
         ("offs_f", P), ("offs_w", P),

@@ -58,13 +58,18 @@ __device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a,
 // normal range -- ok_b says b is -- else the IEEE division is taken.  This is
 // bit-identical to __fdiv_rn / __ddiv_rn; tests/test_gpu_kernels.py checks it
 // against them on 10^8 quotients per divisor.
+// The IEEE fallbacks are out-of-line calls: inlined, the compiler
+// if-converts them and evaluates the full division on every pair.
+static __device__ __noinline__ float fdiv_slow(float a, float b) { return __fdiv_rn(a, b); }
+static __device__ __noinline__ double ddiv_slow(double a, double b) { return __ddiv_rn(a, b); }
 __device__ __forceinline__ float fdiv_rcp(float a, float b, float y, bool ok_b)
 {
     const float q0 = __fmul_rn(a, y);
     const float r = __fmaf_rn(-b, q0, a);
     const float q1 = __fmaf_rn(r, y, q0);
     const float aa = fabsf(a);
-    return (ok_b && aa > 1e-18f && aa < 1e18f) ? q1 : __fdiv_rn(a, b);
+    if (ok_b && aa > 1e-18f && aa < 1e18f) return q1;
+    return fdiv_slow(a, b);
 }
 __device__ __forceinline__ double ddiv_rcp(double a, double b, double y, bool ok_b)
 {
@@ -72,7 +77,8 @@ __device__ __forceinline__ double ddiv_rcp(double a, double b, double y, bool ok
     const double r = __fma_rn(-b, q0, a);
     const double q1 = __fma_rn(r, y, q0);
     const double aa = fabs(a);
-    return (ok_b && aa > 1e-140 && aa < 1e140) ? q1 : __ddiv_rn(a, b);
+    if (ok_b && aa > 1e-140 && aa < 1e140) return q1;
+    return ddiv_slow(a, b);
 }
 template <class T> __device__ __forceinline__ T div_rcp(T a, T b, T y, bool ok_b);
 template <> __device__ __forceinline__ float div_rcp<float>(float a, float b, float y, bool ok)

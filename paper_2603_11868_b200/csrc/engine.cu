@@ -28,6 +28,12 @@
 #ifndef SPH_SWEEP_MINB
 #define SPH_SWEEP_MINB 12    // min resident blocks of the sweeps (register cap)
 #endif
+#ifndef SPH_CONT_MINB
+#define SPH_CONT_MINB 12
+#endif
+#ifndef SPH_MOM_MINB
+#define SPH_MOM_MINB 8       // the momentum sweep holds more live state
+#endif
 #ifndef SPH_FILTER_KF
 #define SPH_FILTER_KF 4      // list entries in flight per filter trip
 #endif
@@ -52,14 +58,32 @@ __device__ __forceinline__ void sweep_list(const Eng<T>& E, int64_t slot, int cn
     for (int t0 = 0; t0 < cnt; t0 += 4) {
         const int4 q = qn;
         if (t0 + 4 < cnt) qn = q4[((t0 >> 2) + 1) * 32];
-        body(load(q.x));
-        if (t0 + 1 < cnt) body(load(q.y));
-        if (t0 + 2 < cnt) body(load(q.z));
-        if (t0 + 3 < cnt) body(load(q.w));
+        body(t0, load(q.x));
+        if (t0 + 1 < cnt) body(t0 + 1, load(q.y));
+        if (t0 + 2 < cnt) body(t0 + 2, load(q.z));
+        if (t0 + 3 < cnt) body(t0 + 3, load(q.w));
     }
 }
 
 template <class T> struct NbrPVR { vec4<T> p; vec4<T> v; vec2<T> rp; };
+template <class T> struct NbrPV { vec4<T> p; vec4<T> v; };
+
+// momentum operands of a particle: (rho, p / rho^2) (physics.py:147-148)
+template <class T>
+__device__ __forceinline__ vec2<T> rq_of(const vec2<T>& rp)
+{
+    vec2<T> q;
+    q.x = rp.x;
+    q.y = RN<T>::div(rp.y, RN<T>::mul(rp.x, rp.x));
+    return q;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_rq_fill(Eng<T> E, int crp, int64_t count)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) E.rq[i] = rq_of<T>(E.rp[crp][i]);
+}
 template <class T> struct NbrPR { vec4<T> p; vec2<T> rp; };
 
 // Exact filter of slot's skin list fused into a sweep: per 32 entries, the
@@ -183,13 +207,19 @@ k_skin_build(const EngAcc<T> acc, const GridP<T> g, T cs2, int64_t first, int64_
 // upward-rounded displacement bound and the list-cell check
 template <class T, int D>
 __global__ void __launch_bounds__(256)
-k_kick_drift(Eng<T> E, int cv, GridP<T> g, T half, T full)
+k_kick_drift(Eng<T> E, int cv, int crp, GridP<T> g, T half, T full)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     T dnew = T(0);
-    if (i < E.nf) {
+    if (i >= E.nf && i < E.n) {
+        // walls: only the continuity operand m/rho (physics.py:113)
+        reinterpret_cast<T*>(&E.vel[cv][i])[3] = RN<T>::div(E.pos[i].w, E.rp[crp][i].x);
+    } else if (i < E.nf) {
         vec4<T> P4 = E.pos[i], V4 = E.vel[cv][i];
         const vec4<T> A4 = E.dvdt[i];
+        // the continuity operand m_j/rho_j of this sub-step (physics.py:113):
+        // a per-particle quotient, evaluated once here instead of per pair
+        V4.w = RN<T>::div(P4.w, E.rp[crp][i].x);
         V4.x = RN<T>::add(V4.x, RN<T>::mul(half, A4.x));
         V4.y = RN<T>::add(V4.y, RN<T>::mul(half, A4.y));
         if (D == 3) V4.z = RN<T>::add(V4.z, RN<T>::mul(half, A4.z));
@@ -331,7 +361,7 @@ __device__ __forceinline__ void flag_overflow(uint32_t* oflow_id, uint32_t pid, 
 // A particle with a valid skin list filters it here (writing the exact list
 // the momentum sweep reuses); others read the exact list k_fix_build made.
 template <class T, int D>
-__global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
+__global__ void __launch_bounds__(kSweepThreads, SPH_CONT_MINB)
 k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -344,26 +374,34 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
     to3<T>(vel[i], vi);
     const T rho_i = rp[i].x;
     double acc = double(RN<T>::sub(rho_i, rho_i));
-    auto loadf = [&](int j) { return NbrPVR<T>{pos[j], vel[j], rp[j]}; };
-    auto pair = [&](const NbrPVR<T>& nb) {
+    auto loadf = [&](int j) { return NbrPV<T>{pos[j], vel[j]}; };
+    auto pair = [&](int, const NbrPV<T>& nb) {
         T xj[3], vj[3], dx[3], r2, vx;
         to3<T>(nb.p, xj);
         to3<T>(nb.v, vj);
         pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-        acc = dadd(acc, continuity_term<T>(r2, vx, nb.p.w, nb.rp.x, P));
+        acc = dadd(acc, continuity_term<T>(r2, vx, nb.v.w, P));   // v.w = m_j/rho_j
     };
+    int cnt;
     if (E.cell0[i] == kInvalidCell) {
-        const int acnt = E.acount[i];
-        if (acnt < 0) { flag_overflow(E.oflow_id, E.id[i], E.stats); return; }
-        sweep_list<T>(E, i, acnt, loadf, pair);
+        cnt = E.acount[i];
+        if (cnt < 0) { flag_overflow(E.oflow_id, E.id[i], E.stats); return; }
+        sweep_list<T>(E, i, cnt, loadf, pair);
     } else {
-        int32_t* ep = E.elist + ell_base(i);
-        int cnt = 0;
-        filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf, [&](int j, const NbrPVR<T>& nb) {
-            if (cnt < kCap) ep[ell_off(cnt)] = j;
+        // the exact list, also stored a full int4 quad at a time
+        int4* __restrict__ eq = reinterpret_cast<int4*>(E.elist + ell_base(i));
+        int e0 = 0, e1 = 0, e2 = 0;
+        cnt = 0;
+        filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf, [&](int j, const NbrPV<T>& nb) {
+            const int r = cnt & 3;
+            if (r == 0) e0 = j;
+            else if (r == 1) e1 = j;
+            else if (r == 2) e2 = j;
+            else if (cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, j);
+            pair(cnt, nb);
             cnt++;
-            pair(nb);
         });
+        if ((cnt & 3) && cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, 0);
         if (cnt > kCap) {
             E.acount[i] = -1;
             flag_overflow(E.oflow_id, E.id[i], E.stats);
@@ -377,6 +415,7 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
     out.x = RN<T>::add(rho_i, RN<T>::mul(full, dr));
     out.y = RN<T>::mul(P.c0c0, RN<T>::sub(out.x, P.rho0));
     E.rp[crp ^ 1][i] = out;
+    E.rq[i] = rq_of<T>(out);
 }
 
 // physics.py:161-194 WALL_PRESSURE over the wall segment: fluid p from
@@ -400,7 +439,7 @@ k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor,
         double num = double(RN<T>::sub(rho_i, rho_i));
         double den = num;
         auto loadf = [&](int j) { return NbrPR<T>{E.pos[j], rp[j]}; };
-        auto pair = [&](const NbrPR<T>& nb) {
+        auto pair = [&](int, const NbrPR<T>& nb) {
             T xj[3];
             to3<T>(nb.p, xj);
             const double w = wall_weight<T>(pair_r2<T, D>(xi, xj), P);
@@ -414,7 +453,7 @@ k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor,
         } else {
             acnt = 0;
             filter_walk<T, D>(E, slot, xi, g.c2, E.lcount[slot], loadf,
-                              [&](int, const NbrPR<T>& nb) { acnt++; pair(nb); });
+                              [&](int, const NbrPR<T>& nb) { pair(acnt++, nb); });
             if (acnt + E.nww[slot] > kCap) acnt = -1;
             E.acount[slot] = acnt;
         }
@@ -425,6 +464,7 @@ k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor,
             out.y = den > 0.0 ? RN<T>::from_d(ddiv(num, den)) : T(0);
             out.x = RN<T>::add(P.rho0, RN<T>::div(out.y, P.c0c0));
             rp[i] = out;
+            E.rq[i] = rq_of<T>(out);
             E.nnb[i] = (uint32_t)acnt;
             if (zero_drho) E.drho[i] = T(0);
             visits_sum = (unsigned long long)acnt * (unsigned long long)count_factor;
@@ -436,7 +476,7 @@ k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor,
 // physics.py:122-158 MOMENTUM (+ :546-547 KICK(half) into the other velocity
 // buffer when kick != 0), fluid only; rho/p from buffer brp.
 template <class T, int D>
-__global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
+__global__ void __launch_bounds__(kSweepThreads, SPH_MOM_MINB)
 k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -448,25 +488,23 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor)
         } else {
                     const vec4<T>* __restrict__ pos = E.pos;
             const vec4<T>* __restrict__ vel = E.vel[cv];
-            const vec2<T>* __restrict__ rp = E.rp[brp];
+            const vec2<T>* __restrict__ rq = E.rq;   // (rho, p/rho^2) of buffer brp
             T xi[3], vi[3];
             to3<T>(pos[i], xi);
             const vec4<T> VI = vel[i];
             to3<T>(VI, vi);
-            const vec2<T> RPI = rp[i];
-            const T rho_i = RPI.x;
-            const T pi_rr = RN<T>::div(RPI.y, RN<T>::mul(rho_i, rho_i));
+            const vec2<T> RQI = rq[i];
+            const T rho_i = RQI.x;
+            const T pi_rr = RQI.y;
             T a[3] = {P.g[0], P.g[1], P.g[2]};
-            sweep_list<T>(E, i, acnt,
-                [&](int j) { return NbrPVR<T>{pos[j], vel[j], rp[j]}; },
-                [&](const NbrPVR<T>& nb) {
-                    T xj[3], vj[3], dx[3], r2, vx;
-                    to3<T>(nb.p, xj);
-                    to3<T>(nb.v, vj);
-                    pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-                    momentum_pair<T, D>(r2, vx, dx, rho_i, pi_rr, nb.rp.x, nb.rp.y, nb.p.w, P,
-                                        a);
-                });
+            auto loadf = [&](int j) { return NbrPVR<T>{pos[j], vel[j], rq[j]}; };
+            sweep_list<T>(E, i, acnt, loadf, [&](int, const NbrPVR<T>& nb) {
+                T xj[3], vj[3], dx[3], r2, vx;
+                to3<T>(nb.p, xj);
+                to3<T>(nb.v, vj);
+                pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
+                momentum_pair<T, D>(r2, vx, dx, rho_i, pi_rr, nb.rp.x, nb.rp.y, nb.p.w, P, a);
+            });
             vec4<T> A4;
             A4.x = a[0]; A4.y = a[1]; A4.z = D == 3 ? a[2] : T(0); A4.w = T(0);
             E.dvdt[i] = A4;
@@ -510,7 +548,7 @@ k_shepard(Eng<T> E, PhysT<T> P, int crp)
         double den = double(RN<T>::mul(RN<T>::div(m_i, RPI.x), P.alpha_d));
         sweep_list<T>(E, i, E.acount[i],
             [&](int j) { return NbrPR<T>{E.pos[j], rp[j]}; },
-            [&](const NbrPR<T>& nb) {
+            [&](int, const NbrPR<T>& nb) {
                 T xj[3];
                 to3<T>(nb.p, xj);
                 const double w = wall_weight<T>(pair_r2<T, D>(xi, xj), P);
@@ -636,9 +674,11 @@ static int initialize_impl(SphEngine* e, cudaStream_t s)
     if (nw > 0)
         note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
             E, P, grid_of_engine<T>(e), e->cur_rp, 0, 1, 0);
-    if (e->nf > 0)
+    if (e->nf > 0) {
+        note_launch(), k_rq_fill<T><<<grid_for(e->nf, 256), 256, 0, s>>>(E, e->cur_rp, e->nf);
         note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
             E, P, e->cur_v, e->cur_rp, 0, T(0), 1);
+    }
     // momentum writes dvdt = 0 for walls (physics.py:128-131)
     if (nw > 0)
         cudaMemsetAsync((char*)e->dvdt + sizeof(vec4<T>) * (size_t)e->nf, 0,
@@ -686,8 +726,9 @@ static int substep_impl(SphEngine* e, double half_d, double full_d, cudaEvent_t*
     const int cv = e->cur_v, crp = e->cur_rp;
     const int64_t nf = e->nf, nw = e->n - e->nf;
     if (ev) cudaEventRecord(ev[0], s);
-    if (nf > 0)
-        note_launch(), k_kick_drift<T, D><<<grid_for(nf, 256), 256, 0, s>>>(E, cv, g, half, full);
+    if (e->n > 0)
+        note_launch(), k_kick_drift<T, D><<<grid_for(e->n, 256), 256, 0, s>>>(E, cv, crp, g, half,
+                                                                            full);
     if (ev) cudaEventRecord(ev[1], s);
     mark_and_fix<T, D>(e, s);
     if (ev) cudaEventRecord(ev[2], s);

@@ -7,6 +7,10 @@
 //   vel  vec4 x2 (double buffer)    -- kick2 writes the other buffer
 //   rp   vec2 (rho, p) x2           -- continuity+density update writes the
 //                                      other buffer, walls follow
+//   rq   vec2 (rho, p/rho^2)        -- per-neighbour momentum operands, written
+//                                      with rp by the density update / walls
+//   vel.w = m/rho                   -- per-neighbour continuity operand, set by
+//                                      kick+drift before every continuity sweep
 //   dvdt vec4, drho, id, nnb, refpos (registry position of each particle)
 // Cold per-particle fields no kernel reads per pair (rho_scratch, oflow,
 // wall, Vol) are stored BY ORIGINAL ID, so re-sorting never moves them.
@@ -25,7 +29,7 @@ constexpr uint32_t kInvalidCell = 0xffffffffu;   // list is not a valid skin lis
 template <class T>
 struct Eng {
     int64_t n, nf, nw, nf_pad;
-    vec4<T>* pos; vec4<T>* vel[2]; vec2<T>* rp[2]; vec4<T>* dvdt; T* drho;
+    vec4<T>* pos; vec4<T>* vel[2]; vec2<T>* rp[2]; vec2<T>* rq; vec4<T>* dvdt; T* drho;
     uint32_t* id; uint32_t* nnb; uint32_t* refpos;
     T* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; T* vol_id;
     uint32_t* offs_f; uint32_t* offs_w;
@@ -42,6 +46,7 @@ inline Eng<T> eng_of(const SphEngine* e)
     g.pos = (vec4<T>*)e->pos;
     g.vel[0] = (vec4<T>*)e->vel[0]; g.vel[1] = (vec4<T>*)e->vel[1];
     g.rp[0] = (vec2<T>*)e->rp[0]; g.rp[1] = (vec2<T>*)e->rp[1];
+    g.rq = (vec2<T>*)e->rq;
     g.dvdt = (vec4<T>*)e->dvdt; g.drho = (T*)e->drho;
     g.id = e->id; g.nnb = e->nnb; g.refpos = e->refpos;
     g.rho_scratch_id = (T*)e->rho_scratch_id; g.oflow_id = e->oflow_id;

@@ -62,7 +62,7 @@ __global__ void k_gen_continuity(GenView<T> a, PhysT<T> P, const int32_t* __rest
         load3<T, D>(a.x, j, xj);
         load3<T, D>(a.v, j, vj);
         pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-        acc = dadd(acc, continuity_term<T>(r2, vx, a.m[j], a.rho[j], P));
+        acc = dadd(acc, continuity_term<T>(r2, vx, RN<T>::div(a.m[j], a.rho[j]), P));
     }
     a.drho[i] = RN<T>::from_d(dmul(double(rho_i), acc));
 }
@@ -92,7 +92,8 @@ __global__ void k_gen_momentum(GenView<T> a, PhysT<T> P, const int32_t* __restri
         load3<T, D>(a.x, j, xj);
         load3<T, D>(a.v, j, vj);
         pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-        momentum_pair<T, D>(r2, vx, dx, rho_i, pi_rr, a.rho[j], a.p[j], a.m[j], P, acc);
+        momentum_pair<T, D>(r2, vx, dx, rho_i, pi_rr, a.rho[j],
+                            RN<T>::div(a.p[j], RN<T>::mul(a.rho[j], a.rho[j])), a.m[j], P, acc);
     }
     for (int k = 0; k < D; k++) a.dvdt[i * D + k] = acc[k];
     a.nnb[i] = (uint32_t)cnt;

@@ -509,6 +509,7 @@ class Simulation:
         T["vel1"] = torch.empty((n, 4), dtype=tdt, device=dev)
         T["rp0"] = torch.empty((n, 2), dtype=tdt, device=dev)
         T["rp1"] = torch.empty((n, 2), dtype=tdt, device=dev)
+        T["rq"] = torch.empty((n, 2), dtype=tdt, device=dev)
         T["dvdt"] = torch.empty((n, 4), dtype=tdt, device=dev)
         T["drho"] = torch.empty((n,), dtype=tdt, device=dev)
         for k in ("id", "nnb", "refpos", "oflow_id", "wall_id"):
@@ -538,6 +539,7 @@ class Simulation:
         E.pos = T["pos"].data_ptr()
         E.vel[0], E.vel[1] = T["vel0"].data_ptr(), T["vel1"].data_ptr()
         E.rp[0], E.rp[1] = T["rp0"].data_ptr(), T["rp1"].data_ptr()
+        E.rq = T["rq"].data_ptr()
         for k in ("dvdt", "drho", "id", "nnb", "refpos", "rho_scratch_id",
                   "oflow_id", "wall_id", "vol_id", "offs_f", "offs_w", "lists",
                   "lcount", "acount", "nww", "elist", "cell0", "disp", "queue",
