@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 1
+#define SPH_ABI_VERSION 2
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -191,6 +191,10 @@ typedef struct {
     uint32_t* id; uint32_t* nnb; uint32_t* refpos;
     /* by-id cold fields (dev) */
     void* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; void* vol_id;
+    /* multi-rank slabs: 1 for particles this rank owns, 0 for halo ghosts,
+     * by id; NULL = every particle is owned.  Ghosts are not integrated and
+     * count in no counter or reduction (their state arrives by unpack). */
+    uint8_t* owned_id;
     /* cell offsets into each segment (dev, ncells+1 each) */
     uint32_t* offs_f; uint32_t* offs_w;
     /* ascending-id Verlet (skin) lists and this sub-step's exact lists, both
@@ -251,6 +255,36 @@ int sph_engine_substep_timed(SphEngine* e, double half_dt, double full_dt, float
  * flags & 2: recompute the exact vmax/amax (physics.py:390-391) and the
  * stability inputs (physics.py:554-564) into e->stats */
 int sph_engine_stats(SphEngine* e, int flags, cudaStream_t s);
+
+/* ---- multi-rank slab decomposition ------------------------
+ * The sub-step and initialize split at the points where halo data must be
+ * exchanged between ranks; sph_engine_substep == phases 0..3. */
+#define SPH_PHASE_KICK_DRIFT 0      /* KICK + DRIFT of owned fluid, m/rho operands  */
+#define SPH_PHASE_CONTINUITY 1      /* list upkeep, CONTINUITY + DENSITY_UPDATE      */
+#define SPH_PHASE_WALL 2            /* WALL_PRESSURE into the sub-step's rp buffer   */
+#define SPH_PHASE_MOMENTUM 3        /* MOMENTUM + KICK; the sub-step's buffers become
+                                       current                                      */
+#define SPH_PHASE_INIT_WALL 4       /* initialize: exact lists + WALL_PRESSURE       */
+#define SPH_PHASE_INIT_MOMENTUM 5   /* initialize: MOMENTUM (no kick)                */
+int sph_engine_phase(SphEngine* e, int32_t phase, double half_dt, double full_dt,
+                     cudaStream_t s);
+/* Halo records of the particles at physical indices phys[0..count), packed
+ * as count x width run-precision values (owner side) and written back into
+ * the ghosts (receiver side):
+ *   XV      pos (x, y, z, m), current vel (x, y, z, m/rho), displacement
+ *           bound since the list build; unpack re-checks the ghost's list
+ *           cell and folds the bound into the step's maximum displacement
+ *   RP_NEXT (rho, p) of the in-flight sub-step buffer (after CONTINUITY or
+ *           WALL phases)
+ *   RP_CUR  (rho, p) of the current buffer (after Shepard / INIT_WALL) */
+#define SPH_HALO_XV 0
+#define SPH_HALO_RP_NEXT 1
+#define SPH_HALO_RP_CUR 2
+int32_t sph_engine_halo_width(int32_t kind);
+int sph_engine_pack(const SphEngine* e, int32_t kind, const int32_t* phys, int64_t count,
+                    void* out, cudaStream_t s);
+int sph_engine_unpack(SphEngine* e, int32_t kind, const int32_t* phys, int64_t count,
+                      const void* in, cudaStream_t s);
 
 #ifdef __cplusplus
 }

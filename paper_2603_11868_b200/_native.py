@@ -77,6 +77,7 @@ class SphEngine(C.Structure):
         ("pos", P), ("vel", P * 2), ("rp", P * 2), ("rq", P), ("dvdt", P), ("drho", P),
         ("id", P), ("nnb", P), ("refpos", P),
         ("rho_scratch_id", P), ("oflow_id", P), ("wall_id", P), ("vol_id", P),
+        ("owned_id", P),
         ("offs_f", P), ("offs_w", P),
         ("lists", P), ("lcount", P), ("acount", P), ("nww", P), ("elist", P),
         ("cell0", P), ("disp", P), ("queue", P), ("qcount", P),
@@ -90,8 +91,13 @@ class SphEngine(C.Structure):
     ]
 
 
+ABI_VERSION = 2   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
+# sph_engine_phase / halo records (include/sph_b200.h)
+PHASE_KICK_DRIFT, PHASE_CONTINUITY, PHASE_WALL, PHASE_MOMENTUM = 0, 1, 2, 3
+PHASE_INIT_WALL, PHASE_INIT_MOMENTUM = 4, 5
+HALO_XV, HALO_RP_NEXT, HALO_RP_CUR = 0, 1, 2
 
 # name -> (restype, argtypes)
 _P = c_void_p
@@ -117,6 +123,10 @@ _PROTOS = {
     "sph_engine_substep": (c_i32, [_P, c_f64, c_f64, _P]),
     "sph_engine_substep_timed": (c_i32, [_P, c_f64, c_f64, _P, _P]),
     "sph_engine_stats": (c_i32, [_P, c_i32, _P]),
+    "sph_engine_phase": (c_i32, [_P, c_i32, c_f64, c_f64, _P]),
+    "sph_engine_halo_width": (c_i32, [c_i32]),
+    "sph_engine_pack": (c_i32, [_P, c_i32, _P, c_i64, _P, _P]),
+    "sph_engine_unpack": (c_i32, [_P, c_i32, _P, c_i64, _P, _P]),
 }
 for _sfx, _real in (("f32", c_f32), ("f64", c_f64)):
     for _k in ("continuity", "momentum", "wall_pressure", "density_summation",
@@ -158,7 +168,7 @@ def load(path=None):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.sph_abi_version() != 1:
+    if lib.sph_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libsphb200.so ABI version mismatch")
     if path is None:
         _LIB = lib

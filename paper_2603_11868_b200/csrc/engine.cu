@@ -211,10 +211,11 @@ k_kick_drift(Eng<T> E, int cv, int crp, GridP<T> g, T half, T full)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     T dnew = T(0);
-    if (i >= E.nf && i < E.n) {
-        // walls: only the continuity operand m/rho (physics.py:113)
+    if (i >= E.n) {
+    } else if (i >= E.nf || !is_owned(E, i)) {
+        // walls and halo ghosts: only the continuity operand m/rho (physics.py:113)
         reinterpret_cast<T*>(&E.vel[cv][i])[3] = RN<T>::div(E.pos[i].w, E.rp[crp][i].x);
-    } else if (i < E.nf) {
+    } else {
         vec4<T> P4 = E.pos[i], V4 = E.vel[cv][i];
         const vec4<T> A4 = E.dvdt[i];
         // the continuity operand m_j/rho_j of this sub-step (physics.py:113):
@@ -350,10 +351,13 @@ k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E)
 // ---------------------------------------------------------------------------
 // sweeps (thread per particle, ascending-id accumulation)
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void flag_overflow(uint32_t* oflow_id, uint32_t pid, SphStepStats* st)
+// neighborhood.py:200-202 / physics.py:357-360 (owned particles only)
+template <class T>
+__device__ __forceinline__ void flag_overflow(const Eng<T>& E, int64_t i)
 {
-    oflow_id[pid] = 1;
-    atomicAdd(&st->overflow, 1u);
+    if (!is_owned(E, i)) return;
+    E.oflow_id[E.id[i]] = 1;
+    atomicAdd(&E.stats->overflow, 1u);
 }
 
 // physics.py:94-119 CONTINUITY fused with :268-274 DENSITY_UPDATE(full),
@@ -385,7 +389,7 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
     int cnt;
     if (E.cell0[i] == kInvalidCell) {
         cnt = E.acount[i];
-        if (cnt < 0) { flag_overflow(E.oflow_id, E.id[i], E.stats); return; }
+        if (cnt < 0) { flag_overflow(E, i); return; }
         sweep_list<T>(E, i, cnt, loadf, pair);
     } else {
         // the exact list, also stored a full int4 quad at a time
@@ -404,7 +408,7 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
         if ((cnt & 3) && cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, 0);
         if (cnt > kCap) {
             E.acount[i] = -1;
-            flag_overflow(E.oflow_id, E.id[i], E.stats);
+            flag_overflow(E, i);
             return;
         }
         E.acount[i] = cnt;
@@ -458,7 +462,7 @@ k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor,
             E.acount[slot] = acnt;
         }
         if (acnt < 0) {
-            flag_overflow(E.oflow_id, E.id[i], E.stats);
+            flag_overflow(E, i);
         } else {
             vec2<T> out;
             out.y = den > 0.0 ? RN<T>::from_d(ddiv(num, den)) : T(0);
@@ -467,7 +471,8 @@ k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor,
             E.rq[i] = rq_of<T>(out);
             E.nnb[i] = (uint32_t)acnt;
             if (zero_drho) E.drho[i] = T(0);
-            visits_sum = (unsigned long long)acnt * (unsigned long long)count_factor;
+            if (is_owned(E, i))
+                visits_sum = (unsigned long long)acnt * (unsigned long long)count_factor;
         }
     }
     add_interactions(E.stats, visits_sum);
@@ -484,7 +489,7 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor)
     if (i < E.nf) {
         const int acnt = E.acount[i];
         if (acnt < 0) {
-            flag_overflow(E.oflow_id, E.id[i], E.stats);
+            flag_overflow(E, i);
         } else {
                     const vec4<T>* __restrict__ pos = E.pos;
             const vec4<T>* __restrict__ vel = E.vel[cv];
@@ -516,7 +521,7 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor)
                 if (D == 3) V4.z = RN<T>::add(V4.z, RN<T>::mul(half, A4.z));
                 E.vel[cv ^ 1][i] = V4;
             }
-            csum = (unsigned long long)acnt * (unsigned long long)count_factor;
+            if (is_owned(E, i)) csum = (unsigned long long)acnt * (unsigned long long)count_factor;
         }
     }
     add_interactions(E.stats, csum);
@@ -664,25 +669,40 @@ static int require_lists(const SphEngine* e)
     return SPH_OK;
 }
 
+// physics.py:460-467 initialize, in its two halo-exchange phases: exact
+// lists + WALL_PRESSURE into the current buffer, then MOMENTUM (no kick)
 template <class T, int D>
-static int initialize_impl(SphEngine* e, cudaStream_t s)
+static void init_wall(SphEngine* e, cudaStream_t s)
 {
     prepare_lists<T, D>(e, s);
-    Eng<T> E = eng_of<T>(e);
-    const PhysT<T> P = make_phys<T>(phys_of_engine(e));
     const int64_t nw = e->n - e->nf;
     if (nw > 0)
         note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, P, grid_of_engine<T>(e), e->cur_rp, 0, 1, 0);
+            eng_of<T>(e), make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_rp, 0,
+            1, 0);
+}
+
+template <class T, int D>
+static void init_momentum(SphEngine* e, cudaStream_t s)
+{
+    Eng<T> E = eng_of<T>(e);
+    const int64_t nw = e->n - e->nf;
     if (e->nf > 0) {
         note_launch(), k_rq_fill<T><<<grid_for(e->nf, 256), 256, 0, s>>>(E, e->cur_rp, e->nf);
         note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, P, e->cur_v, e->cur_rp, 0, T(0), 1);
+            E, make_phys<T>(phys_of_engine(e)), e->cur_v, e->cur_rp, 0, T(0), 1);
     }
     // momentum writes dvdt = 0 for walls (physics.py:128-131)
     if (nw > 0)
         cudaMemsetAsync((char*)e->dvdt + sizeof(vec4<T>) * (size_t)e->nf, 0,
                         sizeof(vec4<T>) * (size_t)nw, s);
+}
+
+template <class T, int D>
+static int initialize_impl(SphEngine* e, cudaStream_t s)
+{
+    init_wall<T, D>(e, s);
+    init_momentum<T, D>(e, s);
     return check_launch("engine_initialize");
 }
 
@@ -713,6 +733,54 @@ extern "C" int sph_engine_shepard(SphEngine* e, cudaStream_t s)
     return SPH_DISPATCH(e, shepard_impl, e, s);
 }
 
+// physics.py:522-548, one acoustic sub-step in the phases between which a
+// multi-rank run exchanges halo data
+template <class T, int D>
+static void sub_kick_drift(SphEngine* e, T half, T full, cudaStream_t s)
+{
+    if (e->n > 0)
+        note_launch(), k_kick_drift<T, D><<<grid_for(e->n, 256), 256, 0, s>>>(
+            eng_of<T>(e), e->cur_v, e->cur_rp, grid_of_engine<T>(e), half, full);
+}
+
+template <class T, int D>
+static void sub_continuity(SphEngine* e, T full, cudaStream_t s)
+{
+    Eng<T> E = eng_of<T>(e);
+    const int crp = e->cur_rp;
+    if (e->nf > 0)
+        note_launch(), k_cont_du<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
+            E, make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full);
+    else if (e->n > 0)   // no fluid: the other rp buffer must still carry walls
+        cudaMemcpyAsync(E.rp[crp ^ 1], E.rp[crp], sizeof(vec2<T>) * (size_t)e->n,
+                        cudaMemcpyDeviceToDevice, s);
+}
+
+template <class T, int D>
+static void sub_wall(SphEngine* e, cudaStream_t s)
+{
+    const int64_t nw = e->n - e->nf;
+    if (nw > 0)
+        note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
+            eng_of<T>(e), make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_rp ^ 1,
+            1, 1, 1);
+}
+
+template <class T, int D>
+static void sub_momentum(SphEngine* e, T half, cudaStream_t s)
+{
+    Eng<T> E = eng_of<T>(e);
+    const int cv = e->cur_v;
+    if (e->nf > 0)
+        note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
+            E, make_phys<T>(phys_of_engine(e)), cv, e->cur_rp ^ 1, 1, half, 2);
+    else if (e->n > 0)
+        cudaMemcpyAsync(E.vel[cv ^ 1], E.vel[cv], sizeof(vec4<T>) * (size_t)e->n,
+                        cudaMemcpyDeviceToDevice, s);
+    e->cur_v = cv ^ 1;
+    e->cur_rp ^= 1;
+}
+
 // ev (optional, 6 events) brackets: kick+drift | list filter + fix-ups |
 // continuity+DU | wall pressure | momentum+kick (bench.py per-kernel timing)
 template <class T, int D>
@@ -720,38 +788,17 @@ static int substep_impl(SphEngine* e, double half_d, double full_d, cudaEvent_t*
                         cudaStream_t s)
 {
     const T half = T(half_d), full = T(full_d);
-    Eng<T> E = eng_of<T>(e);
-    const PhysT<T> P = make_phys<T>(phys_of_engine(e));
-    GridP<T> g = grid_of_engine<T>(e);
-    const int cv = e->cur_v, crp = e->cur_rp;
-    const int64_t nf = e->nf, nw = e->n - e->nf;
     if (ev) cudaEventRecord(ev[0], s);
-    if (e->n > 0)
-        note_launch(), k_kick_drift<T, D><<<grid_for(e->n, 256), 256, 0, s>>>(E, cv, crp, g, half,
-                                                                            full);
+    sub_kick_drift<T, D>(e, half, full, s);
     if (ev) cudaEventRecord(ev[1], s);
     mark_and_fix<T, D>(e, s);
     if (ev) cudaEventRecord(ev[2], s);
-    if (nf > 0)
-        note_launch(), k_cont_du<T, D><<<grid_for(nf, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, P, g, cv, crp, full);
-    else if (nw > 0)   // no fluid: the other rp buffer must still carry walls
-        cudaMemcpyAsync(E.rp[crp ^ 1], E.rp[crp], sizeof(vec2<T>) * (size_t)e->n,
-                        cudaMemcpyDeviceToDevice, s);
+    sub_continuity<T, D>(e, full, s);
     if (ev) cudaEventRecord(ev[3], s);
-    if (nw > 0)
-        note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, P, g, crp ^ 1, 1, 1, 1);
+    sub_wall<T, D>(e, s);
     if (ev) cudaEventRecord(ev[4], s);
-    if (nf > 0)
-        note_launch(), k_mom<T, D><<<grid_for(nf, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, P, cv, crp ^ 1, 1, half, 2);
-    else
-        cudaMemcpyAsync(E.vel[cv ^ 1], E.vel[cv], sizeof(vec4<T>) * (size_t)e->n,
-                        cudaMemcpyDeviceToDevice, s);
+    sub_momentum<T, D>(e, half, s);
     if (ev) cudaEventRecord(ev[5], s);
-    e->cur_v = cv ^ 1;
-    e->cur_rp = crp ^ 1;
     return check_launch("engine_substep");
 }
 
@@ -776,4 +823,137 @@ extern "C" int sph_engine_substep_timed(SphEngine* e, double half_dt, double ful
     }
     for (int k = 0; k < 6; k++) cudaEventDestroy(ev[k]);
     return rc ? rc : check_launch("engine_substep_timed");
+}
+
+template <class T, int D>
+static int phase_impl(SphEngine* e, int phase, double half_d, double full_d, cudaStream_t s)
+{
+    const T half = T(half_d), full = T(full_d);
+    switch (phase) {
+    case SPH_PHASE_KICK_DRIFT: sub_kick_drift<T, D>(e, half, full, s); break;
+    case SPH_PHASE_CONTINUITY:
+        mark_and_fix<T, D>(e, s);
+        sub_continuity<T, D>(e, full, s);
+        break;
+    case SPH_PHASE_WALL: sub_wall<T, D>(e, s); break;
+    case SPH_PHASE_MOMENTUM: sub_momentum<T, D>(e, half, s); break;
+    case SPH_PHASE_INIT_WALL: init_wall<T, D>(e, s); break;
+    case SPH_PHASE_INIT_MOMENTUM: init_momentum<T, D>(e, s); break;
+    default: set_error("engine_phase: unknown phase"); return SPH_ERR_INVALID;
+    }
+    return check_launch("engine_phase");
+}
+
+extern "C" int sph_engine_phase(SphEngine* e, int32_t phase, double half_dt, double full_dt,
+                                cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc || (rc = require_lists(e))) return rc;
+    return SPH_DISPATCH(e, phase_impl, e, phase, half_dt, full_dt, s);
+}
+
+// ---------------------------------------------------------------------------
+// halo records (multi-rank slabs)
+// ---------------------------------------------------------------------------
+template <class T>
+__global__ void __launch_bounds__(256)
+k_pack(Eng<T> E, int kind, int cv, int b, const int32_t* __restrict__ phys, int64_t count,
+       T* __restrict__ out)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= count) return;
+    const int64_t i = phys[k];
+    if (kind == SPH_HALO_XV) {
+        const vec4<T> P4 = E.pos[i], V4 = E.vel[cv][i];
+        T* o = out + 9 * k;
+        o[0] = P4.x; o[1] = P4.y; o[2] = P4.z; o[3] = P4.w;
+        o[4] = V4.x; o[5] = V4.y; o[6] = V4.z; o[7] = V4.w;
+        o[8] = E.disp[i];
+    } else {
+        const vec2<T> RP = E.rp[b][i];
+        out[2 * k] = RP.x;
+        out[2 * k + 1] = RP.y;
+    }
+}
+
+template <class T, int D>
+__global__ void __launch_bounds__(256)
+k_unpack(Eng<T> E, GridP<T> g, int kind, int cv, int b, const int32_t* __restrict__ phys,
+         int64_t count, const T* __restrict__ in)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    T dsp = T(0);
+    if (k < count) {
+        const int64_t i = phys[k];
+        if (kind == SPH_HALO_XV) {
+            const T* r = in + 9 * k;
+            vec4<T> P4, V4;
+            P4.x = r[0]; P4.y = r[1]; P4.z = r[2]; P4.w = r[3];
+            V4.x = r[4]; V4.y = r[5]; V4.z = r[6]; V4.w = r[7];
+            dsp = r[8];
+            E.pos[i] = P4;
+            E.vel[cv][i] = V4;
+            E.disp[i] = dsp;
+            // the ghost's list stays valid only in the cell it was built for
+            const T xn[3] = {P4.x, P4.y, P4.z};
+            int c[3];
+            if (cell_key_of<T, D>(xn, g, c) != E.cell0[i]) E.cell0[i] = kInvalidCell;
+        } else {
+            vec2<T> RP;
+            RP.x = in[2 * k];
+            RP.y = in[2 * k + 1];
+            E.rp[b][i] = RP;
+            E.rq[i] = rq_of<T>(RP);
+        }
+    }
+    if (kind == SPH_HALO_XV) {
+        const unsigned long long m = warp_max_u64(dbits(double(dsp)));
+        if (lane_id() == 0 && m) atomicMax(&E.stats->dmax_bits, m);
+    }
+}
+
+extern "C" int32_t sph_engine_halo_width(int32_t kind)
+{
+    return kind == SPH_HALO_XV ? 9 : (kind == SPH_HALO_RP_NEXT || kind == SPH_HALO_RP_CUR) ? 2
+                                                                                         : -1;
+}
+
+template <class T, int D>
+static int pack_impl(const SphEngine* e, int kind, const int32_t* phys, int64_t count, void* out,
+                     cudaStream_t s)
+{
+    if (count > 0)
+        note_launch(), k_pack<T><<<grid_for(count, 256), 256, 0, s>>>(
+            eng_of<T>(e), kind, e->cur_v, kind == SPH_HALO_RP_NEXT ? e->cur_rp ^ 1 : e->cur_rp,
+            phys, count, (T*)out);
+    return check_launch("engine_pack");
+}
+
+template <class T, int D>
+static int unpack_impl(SphEngine* e, int kind, const int32_t* phys, int64_t count,
+                       const void* in, cudaStream_t s)
+{
+    if (count > 0)
+        note_launch(), k_unpack<T, D><<<grid_for(count, 256), 256, 0, s>>>(
+            eng_of<T>(e), grid_of_engine<T>(e), kind, e->cur_v,
+            kind == SPH_HALO_RP_NEXT ? e->cur_rp ^ 1 : e->cur_rp, phys, count, (const T*)in);
+    return check_launch("engine_unpack");
+}
+
+extern "C" int sph_engine_pack(const SphEngine* e, int32_t kind, const int32_t* phys,
+                               int64_t count, void* out, cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc) return rc;
+    if (sph_engine_halo_width(kind) < 0 || count < 0) return SPH_ERR_INVALID;
+    return SPH_DISPATCH(e, pack_impl, e, kind, phys, count, out, s);
+}
+
+extern "C" int sph_engine_unpack(SphEngine* e, int32_t kind, const int32_t* phys, int64_t count,
+                                 const void* in, cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc) return rc;
+    if (sph_engine_halo_width(kind) < 0 || count < 0) return SPH_ERR_INVALID;
+    return SPH_DISPATCH(e, unpack_impl, e, kind, phys, count, in, s);
 }

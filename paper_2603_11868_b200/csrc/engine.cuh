@@ -32,6 +32,7 @@ struct Eng {
     vec4<T>* pos; vec4<T>* vel[2]; vec2<T>* rp[2]; vec2<T>* rq; vec4<T>* dvdt; T* drho;
     uint32_t* id; uint32_t* nnb; uint32_t* refpos;
     T* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; T* vol_id;
+    const uint8_t* owned_id;
     uint32_t* offs_f; uint32_t* offs_w;
     int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; int32_t* elist;
     uint32_t* cell0; T* disp; uint32_t* queue; uint32_t* qcount;
@@ -51,6 +52,7 @@ inline Eng<T> eng_of(const SphEngine* e)
     g.id = e->id; g.nnb = e->nnb; g.refpos = e->refpos;
     g.rho_scratch_id = (T*)e->rho_scratch_id; g.oflow_id = e->oflow_id;
     g.wall_id = e->wall_id; g.vol_id = (T*)e->vol_id;
+    g.owned_id = e->owned_id;
     g.offs_f = e->offs_f; g.offs_w = e->offs_w;
     g.lists = e->lists; g.lcount = e->lcount; g.acount = e->acount; g.nww = e->nww;
     g.elist = e->elist; g.cell0 = e->cell0; g.disp = (T*)e->disp; g.queue = e->queue;
@@ -104,6 +106,13 @@ template <class T>
 __device__ __forceinline__ void to3(const vec4<T>& v, T (&o)[3])
 {
     o[0] = v.x; o[1] = v.y; o[2] = v.z;
+}
+
+// multi-rank slabs: halo ghosts are neither integrated nor counted
+template <class T>
+__device__ __forceinline__ bool is_owned(const Eng<T>& E, int64_t i)
+{
+    return !E.owned_id || E.owned_id[E.id[i]];
 }
 
 __device__ __forceinline__ void add_interactions(SphStepStats* st, unsigned long long c)

@@ -197,6 +197,7 @@ __global__ void k_stats(Eng<T> E, int cv, int crp)
     unsigned nanf = 0u;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E.n;
          i += (int64_t)gridDim.x * blockDim.x) {
+        if (!is_owned(E, i)) continue;
         vec4<T> V4 = E.vel[cv][i], A4 = E.dvdt[i];
         T vv[3], aa[3];
         to3<T>(V4, vv);

@@ -27,12 +27,18 @@ with current values:
 
 Hence an N-rank run is bit-identical to the 1-rank run and to the reference.
 
-The per-rank compute is a backend: :class:`EngineBackend` (the CUDA engine,
-below) in production, the CPU oracle composition in tests/.
+Data plane.  Per-particle state lives in torch tensors on the rank's device
+(uint32 fields as int32); migration and ghost exchange are
+``batch_isend_irecv`` between neighbouring ranks -- NCCL moves device memory
+directly, gloo (CPU tests) stages through the host.  The per-rank compute is
+a backend: :class:`EngineBackend` (the CUDA engine, device-resident) in
+production, the CPU oracle composition in tests/.  Backends own the halo
+record format (``pack`` / ``unpack``).
 """
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -43,6 +49,10 @@ HALO_PLANES = 2
 # per-particle state carried across ranks (registry field order)
 FIELDS = ("x", "v", "rho", "p", "m", "Vol", "drho", "dvdt", "rho_scratch",
           "id", "wall", "nnb", "oflow")
+INDEX_FIELDS = ("id", "wall", "nnb", "oflow")
+
+# halo record kinds (include/sph_b200.h SPH_HALO_*)
+XV, RP_NEXT, RP_CUR = 0, 1, 2
 
 
 def cell_plane(x0, origin0, cell_size, nplanes):
@@ -56,6 +66,27 @@ def cell_plane(x0, origin0, cell_size, nplanes):
         c = np.where(~(f >= 0) | (f >= 9.2233720368547758e18), 0,
                      np.where(f < nplanes, f, nplanes - 1))
     return c.astype(np.int64)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def as_tensor(arr, device):
+    """numpy field -> torch tensor on device (uint32 as int32)."""
+    torch = _torch()
+    if isinstance(arr, torch.Tensor):
+        return arr.to(device)
+    a = np.ascontiguousarray(arr)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    return torch.from_numpy(a).to(device)
+
+
+def to_numpy(t, name):
+    a = t.detach().cpu().numpy()
+    return a.view(np.uint32) if name in INDEX_FIELDS else a
 
 
 @dataclass
@@ -95,103 +126,92 @@ class SlabLayout:
         return SlabLayout(np.asarray(cuts, np.int64), nplanes)
 
     def owner(self, planes):
+        """Owning rank of each plane (numpy or torch input, same kind out)."""
+        torch = _torch()
+        if isinstance(planes, torch.Tensor):
+            cuts = torch.as_tensor(self.cuts, device=planes.device)
+            return torch.searchsorted(cuts, planes, right=True) - 1
         return np.searchsorted(self.cuts, np.asarray(planes), side="right") - 1
 
     def halo_mask(self, rank, planes):
         """Planes within HALO_PLANES outside rank's slab."""
         a, b = int(self.cuts[rank]), int(self.cuts[rank + 1])
-        planes = np.asarray(planes)
         return ((planes >= a - HALO_PLANES) & (planes < a)) | \
                ((planes >= b) & (planes < b + HALO_PLANES))
 
 
 class Comm:
-    """Point-to-point and collective plumbing over torch.distributed."""
+    """Point-to-point and collective plumbing over torch.distributed.
+
+    ``device``: where the data plane lives.  NCCL moves device tensors
+    directly; gloo only moves host tensors, so device tensors are staged."""
 
     def __init__(self, device=None):
-        import torch
+        torch = _torch()
         import torch.distributed as dist
         self.torch = torch
         self.dist = dist
         self.rank = dist.get_rank()
         self.size = dist.get_world_size()
-        self.device = device if device is not None else torch.device("cpu")
-
-    def _t(self, arr):
-        torch = self.torch
-        a = np.ascontiguousarray(arr)
-        if a.dtype == np.uint32:
-            a = a.view(np.int32)
-        return torch.from_numpy(a).to(self.device)
+        self.device = torch.device(device) if device is not None else torch.device("cpu")
+        self.gloo = dist.get_backend() == "gloo"
+        self.wire = torch.device("cpu") if self.gloo else self.device
 
     def allreduce(self, values, op):
-        torch = self.torch
-        t = torch.tensor(np.asarray(values, np.float64), device=self.device)
+        t = self.torch.tensor(np.asarray(values, np.float64), device=self.wire)
         self.dist.all_reduce(t, op={"max": self.dist.ReduceOp.MAX,
                                     "min": self.dist.ReduceOp.MIN,
                                     "sum": self.dist.ReduceOp.SUM}[op])
         return t.cpu().numpy()
 
     def allreduce_i64(self, values):
-        torch = self.torch
-        t = torch.tensor(np.asarray(values, np.int64), device=self.device)
+        t = self.torch.tensor(np.asarray(values, np.int64), device=self.wire)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
         return t.cpu().numpy()
 
-    def exchange(self, sends, recv_counts, template):
-        """sends: {rank: array}; recv_counts: {rank: n}; template gives the
-        per-row shape / dtype.  Returns {rank: array} received."""
+    def exchange(self, sends, recv_counts, row_shape, dtype):
+        """sends: {rank: tensor (k, *row_shape)}; recv_counts: {rank: n}.
+        Returns {rank: tensor} received, on self.device."""
         torch = self.torch
-        ops, recvs = [], {}
-        row = template.shape[1:]
-        dt = template.dtype
-        tdt = np.int32 if dt == np.uint32 else dt
+        ops, recvs, keep = [], {}, []
         for q, n in recv_counts.items():
             if n:
-                buf = torch.empty((n,) + row, dtype=getattr(torch, np.dtype(tdt).name),
-                                  device=self.device)
+                buf = torch.empty((n,) + tuple(row_shape), dtype=dtype, device=self.wire)
                 recvs[q] = buf
                 ops.append(self.dist.P2POp(self.dist.irecv, buf, q))
-        sent = []
-        for q, arr in sends.items():
-            if len(arr):
-                t = self._t(arr)
-                sent.append(t)
+        for q, t in sends.items():
+            if t.shape[0]:
+                t = t.contiguous().to(self.wire)
+                keep.append(t)
                 ops.append(self.dist.P2POp(self.dist.isend, t, q))
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
-        out = {}
-        for q, buf in recvs.items():
-            a = buf.cpu().numpy()
-            out[q] = a.view(np.uint32) if dt == np.uint32 else a
-        return out
+        return {q: b.to(self.device) for q, b in recvs.items()}
 
     def exchange_counts(self, counts):
         """All ranks' send counts: counts[q] = rows this rank sends to q;
         returns rows this rank receives from each q."""
         torch = self.torch
         send = torch.tensor([counts.get(q, 0) for q in range(self.size)],
-                            dtype=torch.int64, device=self.device)
-        recv = torch.empty_like(send)
-        self.dist.all_to_all_single(recv, send) if self.device.type != "cpu" \
-            else self._alltoall_gloo(send, recv)
-        return {q: int(recv[q].item()) for q in range(self.size) if q != self.rank}
-
-    def _alltoall_gloo(self, send, recv):
-        # gloo has no all_to_all_single; gather the matrix instead
-        mats = [self.torch.empty_like(send) for _ in range(self.size)]
-        self.dist.all_gather(mats, send)
-        for q in range(self.size):
-            recv[q] = mats[q][self.rank]
+                            dtype=torch.int64, device=self.wire)
+        if self.gloo:   # gloo has no all_to_all_single: gather the matrix
+            mats = [torch.empty_like(send) for _ in range(self.size)]
+            self.dist.all_gather(mats, send)
+            recv = torch.stack([m[self.rank] for m in mats])
+        else:
+            recv = torch.empty_like(send)
+            self.dist.all_to_all_single(recv, send)
+        recv = recv.cpu().tolist()
+        return {q: int(recv[q]) for q in range(self.size) if q != self.rank}
 
 
 class DistributedSimulation:
     """Simulation.initialize/advance (physics.py:416-564) over slabs.
 
-    ``owned``: dict of registry fields of the particles this rank owns at
-    start (any partition is fine; the first step migrates).  ``backend``
-    implements the per-rank phases on owned + ghost particles.
+    ``owned``: dict of registry fields (numpy or torch) of the particles this
+    rank owns at start (any partition is fine; the first step migrates).
+    ``backend`` runs the per-rank phases on owned + ghost particles.
     """
 
     def __init__(self, comm, backend, grid, owned, sing, dt_max=1e-3, sort_every=100,
@@ -200,11 +220,11 @@ class DistributedSimulation:
         self.comm = comm
         self.backend = backend
         self.grid = grid
-        self.owned = {f: np.array(owned[f], copy=True) for f in FIELDS}
+        self.owned = {f: as_tensor(owned[f], comm.device).clone() for f in FIELDS}
         self.sing = sing
-        self.dtype = self.owned["x"].dtype
+        self.dtype = np.dtype(str(self.owned["x"].dtype).replace("torch.", ""))
         self.dt_max = dt_max
-        self.sort_every = sort_every
+        self.sort_every = sort_every      # physical order is per rank; not mirrored
         self.shepard_every = shepard_every
         self.fixed_dt = fixed_dt
         self.cfl_acoustic = cfl_acoustic
@@ -217,8 +237,7 @@ class DistributedSimulation:
         self.interaction_count = 0
         self.out_of_bounds = 0
         self.last_nsub = 0
-        self._send = {}        # rank -> local owned indices sent as ghosts
-        self._ghost_from = {}  # rank -> (start, count) of its ghosts locally
+        self._sel = {}         # "fluid"/"wall" -> (send rows {q}, ghost rows {q})
         self._n_owned = 0
         self.migrated = 0      # particles sent to another rank (this rank)
         self.ghost_fluid = 0   # fluid ghosts received at the last step
@@ -226,98 +245,84 @@ class DistributedSimulation:
     # -- decomposition ----------------------------------------------------------
 
     def _planes(self, x):
-        return cell_plane(x[:, 0], self.grid.origin.astype(self.dtype)[0],
-                          self.dtype.type(self.grid.cell_size), int(self.grid.shape[0]))
+        return self.backend.planes(x)
 
     def _rebalance(self):
-        hist = np.bincount(self._planes(self.owned["x"]),
-                           minlength=int(self.grid.shape[0]))
+        torch = self.comm.torch
+        planes = self._planes(self.owned["x"])
+        hist = torch.bincount(planes, minlength=int(self.grid.shape[0])).cpu().numpy()
         tot = self.comm.allreduce_i64(hist)
         self.layout = SlabLayout.balanced(tot, self.comm.size)
 
+    def _exchange_fields(self, fields, send_rows, recv_counts):
+        out = {}
+        for f in FIELDS:
+            arr = fields[f]
+            got = self.comm.exchange({q: arr[r] for q, r in send_rows.items()}, recv_counts,
+                                     arr.shape[1:], arr.dtype)
+            out[f] = got
+        return out
+
     def _migrate(self):
         """Owned particles go to the owner of their current plane."""
-        planes = self._planes(self.owned["x"])
-        dest = self.layout.owner(planes)
+        torch = self.comm.torch
         me = self.comm.rank
+        dest = self.layout.owner(self._planes(self.owned["x"]))
         keep = dest == me
-        counts = {q: int((dest == q).sum()) for q in range(self.comm.size) if q != me}
-        self.migrated += sum(counts.values())
-        recv_counts = self.comm.exchange_counts(counts)
-        new = {}
-        for f in FIELDS:
-            arr = self.owned[f]
-            sends = {q: arr[dest == q] for q in counts}
-            got = self.comm.exchange(sends, recv_counts, arr[:1] if len(arr) else
-                                     np.zeros((1,) + arr.shape[1:], arr.dtype))
-            parts = [arr[keep]] + [got[q] for q in sorted(got)]
-            new[f] = np.concatenate(parts) if parts else arr[:0]
+        cnt = torch.bincount(dest, minlength=self.comm.size).cpu().tolist()
+        send_rows = {q: torch.nonzero(dest == q).flatten()
+                     for q in range(self.comm.size) if q != me and cnt[q]}
+        self.migrated += sum(cnt[q] for q in send_rows)
+        recv_counts = self.comm.exchange_counts({q: cnt[q] for q in send_rows})
+        got = self._exchange_fields(self.owned, send_rows, recv_counts)
+        new = {f: torch.cat([self.owned[f][keep]] + [got[f][q] for q in sorted(got[f])])
+               for f in FIELDS}
         # deterministic local order (by id) -- any order gives the same bits
-        order = np.argsort(new["id"], kind="stable")
+        order = torch.argsort(new["id"], stable=True)
         self.owned = {f: new[f][order] for f in FIELDS}
 
     def _build_local(self):
-        """Owned + ghosts; returns the local field dict and remembers the
-        ghost send lists for the per-sub-step refreshes."""
-        planes = self._planes(self.owned["x"])
+        """Owned + ghosts (rows [0, n_own) owned, then ghosts grouped by
+        source rank); remembers the send/receive rows of the refreshes."""
+        torch = self.comm.torch
         me = self.comm.rank
-        self._send = {}
+        planes = self._planes(self.owned["x"])
+        send_rows = {}
         for q in range(self.comm.size):
             if q == me:
                 continue
-            idx = np.nonzero(self.layout.halo_mask(q, planes))[0]
-            if idx.size:
-                self._send[q] = idx
-        counts = {q: len(v) for q, v in self._send.items()}
-        recv_counts = self.comm.exchange_counts(counts)
-        n_own = len(self.owned["id"])
-        local = {}
-        self._ghost_from = {}
-        off = n_own
+            idx = torch.nonzero(self.layout.halo_mask(q, planes)).flatten()
+            if idx.numel():
+                send_rows[q] = idx
+        recv_counts = self.comm.exchange_counts({q: len(v) for q, v in send_rows.items()})
+        got = self._exchange_fields(self.owned, send_rows, recv_counts)
+        n_own = int(self.owned["id"].shape[0])
+        local = {f: torch.cat([self.owned[f]] + [got[f][q] for q in sorted(got[f])])
+                 for f in FIELDS}
+        ghost_rows, off = {}, n_own
         for q in sorted(recv_counts):
-            self._ghost_from[q] = (off, recv_counts[q])
+            ghost_rows[q] = torch.arange(off, off + recv_counts[q], device=self.comm.device)
             off += recv_counts[q]
-        for f in FIELDS:
-            arr = self.owned[f]
-            sends = {q: arr[idx] for q, idx in self._send.items()}
-            got = self.comm.exchange(sends, recv_counts, arr[:1] if len(arr) else
-                                     np.zeros((1,) + arr.shape[1:], arr.dtype))
-            local[f] = np.concatenate([arr] + [got[q] for q in sorted(got)])
+        wall = local["wall"]
+        self._sel = {}
+        for name, want_wall in (("fluid", False), ("wall", True)):
+            s = {q: r[(wall[r] != 0) == want_wall] for q, r in send_rows.items()}
+            g = {q: r[(wall[r] != 0) == want_wall] for q, r in ghost_rows.items()}
+            self._sel[name] = (s, g)
         self._n_owned = n_own
-        self.ghost_fluid = int((local["wall"][n_own:] == 0).sum())
+        self.ghost_fluid = int((wall[n_own:] == 0).sum())
         return local
 
-    def _refresh(self, names, walls):
-        """Ghosts <- owners for fields ``names``; walls: None = all ghosts,
-        False = fluid ghosts only, True = wall ghosts only."""
-        wall_own = self.backend.get("wall", None)[: self._n_owned]
-        sends = {}
-        for q, idx in self._send.items():
-            if walls is None:
-                sel = idx
-            elif walls:
-                sel = idx[wall_own[idx] != 0]
-            else:
-                sel = idx[wall_own[idx] == 0]
-            sends[q] = sel
-        # receivers derive the same selection from the ghosts' own wall flags
-        wall_loc = self.backend.get("wall", None)
-        recv_sel = {}
-        for q, (start, cnt) in self._ghost_from.items():
-            g = np.arange(start, start + cnt)
-            if walls is None:
-                recv_sel[q] = g
-            elif walls:
-                recv_sel[q] = g[wall_loc[g] != 0]
-            else:
-                recv_sel[q] = g[wall_loc[g] == 0]
-        for name in names:
-            cur = self.backend.get(name, None)
-            payload = {q: cur[sel] for q, sel in sends.items()}
-            got = self.comm.exchange(payload, {q: len(s) for q, s in recv_sel.items()},
-                                     cur[:1])
-            for q, vals in got.items():
-                self.backend.set(name, recv_sel[q], vals)
+    def _refresh(self, kind, which):
+        """Ghosts <- owners: halo records of `kind` for the fluid or wall
+        ghosts (`which`)."""
+        send_rows, ghost_rows = self._sel[which]
+        be = self.backend
+        payload = {q: be.pack(kind, r) for q, r in send_rows.items()}
+        got = self.comm.exchange(payload, {q: int(r.numel()) for q, r in ghost_rows.items()},
+                                 (be.halo_width(kind),), be.halo_dtype)
+        for q, buf in got.items():
+            be.unpack(kind, ghost_rows[q], buf)
 
     # -- reference API ------------------------------------------------------------
 
@@ -331,8 +336,9 @@ class DistributedSimulation:
 
     def initialize(self):
         self._load_step()
+        self.backend.prepare(None)
         self.backend.wall_pressure(initial=True)
-        self._refresh(("rho", "p"), walls=True)
+        self._refresh(RP_CUR, "wall")
         self.backend.momentum_kick(None)
         self._finish_counts()
 
@@ -349,10 +355,7 @@ class DistributedSimulation:
     def advance(self, end_time=None):
         from .physics import SimulationUnstableError, timestep_formula
         self._load_step()
-        if self.shepard_every and self.step_count > 0 \
-                and self.step_count % self.shepard_every == 0:
-            self.backend.shepard()
-            self._refresh(("rho", "p"), walls=False)
+        # compute_timestep reads only v and dvdt, which Shepard leaves alone
         vmax, amax = self.comm.allreduce(self.backend.norms(), "max")
         if self.fixed_dt is not None:
             dt_ac = dt_adv = self.fixed_dt
@@ -363,17 +366,22 @@ class DistributedSimulation:
         dt = dt_adv
         if end_time is not None:
             dt = min(dt, end_time - self.time)
+        self.backend.prepare((float(vmax), float(amax), dt))
+        if self.shepard_every and self.step_count > 0 \
+                and self.step_count % self.shepard_every == 0:
+            self.backend.shepard()
+            self._refresh(RP_CUR, "fluid")
         nsub = max(1, int(math.ceil(dt / dt_ac)))
         dts = dt / nsub
         T = self.dtype.type
         half, full = T(0.5 * dts), T(dts)
         for _ in range(nsub):
             self.backend.kick_drift(half, full)
-            self._refresh(("x", "v"), walls=False)
+            self._refresh(XV, "fluid")
             self.backend.continuity_du(full)
-            self._refresh(("rho", "p"), walls=False)
+            self._refresh(RP_NEXT, "fluid")
             self.backend.wall_pressure()
-            self._refresh(("rho", "p"), walls=True)
+            self._refresh(RP_NEXT, "wall")
             self.backend.momentum_kick(half)
         self.last_nsub = nsub
         self._finish_counts()
@@ -390,11 +398,233 @@ class DistributedSimulation:
         return dt
 
     def gather(self):
-        """All owned particles of all ranks, ordered by id (every rank)."""
+        """All owned particles of all ranks as numpy, ordered by id (every rank)."""
         out = {}
         for f in FIELDS:
             lst = [None] * self.comm.size
-            self.comm.dist.all_gather_object(lst, self.owned[f])
+            self.comm.dist.all_gather_object(lst, to_numpy(self.owned[f], f))
             out[f] = np.concatenate(lst)
         order = np.argsort(out["id"], kind="stable")
         return {f: out[f][order] for f in FIELDS}
+
+
+class EngineBackend:
+    """The CUDA engine (csrc/engine.cu) as the per-rank compute of a slab.
+
+    Each step the rank's owned + ghost particles are pushed (device to
+    device) into one engine with local ids = rank of the global id (the
+    accumulation order is therefore the reference's), ghosts flagged in
+    ``owned_id`` so they are neither integrated nor counted; the phases run
+    through ``sph_engine_phase`` and halo records through
+    ``sph_engine_pack/unpack`` at physical indices.
+    """
+
+    def __init__(self, scalars, sing, grid, device):
+        torch = _torch()
+        from . import _native
+        self.L = _native.lib()
+        self._native = _native
+        self.scalars = scalars
+        self.sing = sing
+        self.grid = grid
+        self.device = torch.device(device)
+        self.f64 = np.dtype(type(scalars[0])) == np.float64
+        self.np_dtype = np.float64 if self.f64 else np.float32
+        self.halo_dtype = torch.float64 if self.f64 else torch.float32
+        self.dim = grid.dim
+        self.E = None
+        self.T = None
+        self._caps = (0, 0, 0)
+        self._skin_factor = 3.0
+        from ._device import stream_ptr
+        self.stream = stream_ptr(self.device)
+
+    # -- helpers ------------------------------------------------------------------
+
+    def _call(self, name, *args):
+        rc = getattr(self.L, name)(ctypes.byref(self.E), *args, self.stream)
+        self._native.check(rc, name)
+
+    def _stats(self):
+        torch = _torch()
+        host = self.T["stats"].cpu()
+        torch.cuda.current_stream(self.device).synchronize()
+        return self._native.SphStepStats.from_buffer_copy(host.numpy().tobytes())
+
+    def _ensure(self, n, nf, nw):
+        from .physics import engine_alloc, engine_set_counts
+        cn, cf, cw = self._caps
+        if self.E is None or n > cn or nf > cf or nw > cw:
+            grow = lambda a, c: max(a, int(c * 1.15) + 64)   # noqa: E731
+            caps = (grow(n, cn), grow(nf, cf), grow(nw, cw))
+            self.E, self.T = engine_alloc(self.device, caps[0], caps[1], caps[2], self.dim,
+                                          self.f64, self.grid, self.scalars, self.sing["g"])
+            self._caps = caps
+        engine_set_counts(self.E, n, nf)
+        self.E.owned_id = self.T["owned_id"].data_ptr()
+
+    def planes(self, x):
+        """Axis-0 cell planes of positions x (n, d) on the device, by the
+        library's binning kernel (neighborhood.py:76-84)."""
+        torch = _torch()
+        n = int(x.shape[0])
+        if n == 0:
+            return torch.zeros(0, dtype=torch.int64, device=self.device)
+        keys, _ = self._keys(x)
+        per_plane = int(np.prod(self.grid.shape[1:]))
+        return keys // per_plane
+
+    def _keys(self, x):
+        torch = _torch()
+        n = int(x.shape[0])
+        keys = torch.empty(n, dtype=torch.int64, device=self.device)
+        oob = torch.zeros(1, dtype=torch.int32, device=self.device)
+        origin = np.zeros(3, self.np_dtype)
+        origin[:self.dim] = self.grid.origin.astype(self.np_dtype)
+        shape = np.ones(3, np.int64)
+        shape[:self.dim] = self.grid.shape
+        fn = getattr(self.L, f"sph_cell_keys_{self._native.sfx(np.dtype(self.np_dtype))}")
+        xc = x.contiguous()
+        rc = fn(ctypes.c_void_p(xc.data_ptr()), n, self.dim,
+                origin.ctypes.data_as(ctypes.c_void_p), self.np_dtype(self.grid.cell_size),
+                shape.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(keys.data_ptr()),
+                ctypes.c_void_p(oob.data_ptr()), self.stream)
+        self._native.check(rc, "cell_keys")
+        return keys, oob
+
+    # -- backend protocol ---------------------------------------------------------
+
+    def load(self, local, n_owned, grid):
+        torch = _torch()
+        n = int(local["id"].shape[0])
+        wall = local["wall"]
+        nf = int((wall == 0).sum())
+        self._ensure(n, nf, n - nf)
+        gid = local["id"].to(torch.int64)
+        order = torch.argsort(gid)
+        lid = torch.empty(n, dtype=torch.int32, device=self.device)
+        lid[order] = torch.arange(n, dtype=torch.int32, device=self.device)
+        self.gid_of_lid = local["id"][order]
+        self.n, self.n_own = n, n_owned
+        owned = self.T["owned_id"]
+        owned[:n].zero_()
+        owned[lid[:n_owned].to(torch.int64)] = 1
+        if n:
+            args = [local[f].contiguous() for f in ("x", "v", "rho", "p", "m", "Vol",
+                                                    "drho", "dvdt", "rho_scratch")]
+            args += [lid, wall.contiguous(), local["nnb"].contiguous(),
+                     local["oflow"].contiguous()]
+            self._call("sph_engine_push", *[ctypes.c_void_p(a.data_ptr()) for a in args])
+            # physical index of every local row (push records refpos = row)
+            ref = self.T["refpos"][:n].to(torch.int64)
+            self.phys_of_row = torch.empty(n, dtype=torch.int32, device=self.device)
+            self.phys_of_row[ref] = torch.arange(n, dtype=torch.int32, device=self.device)
+            del args
+        self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_RESET))
+        oob = 0
+        if n_owned:
+            _, o = self._keys(local["x"][:n_owned])
+            oob = int(o.item())
+        return oob
+
+    def prepare(self, step):
+        """Lists for the step: exact (skin 0) for initialize, else a skin
+        sized from (vmax, amax, dt) as in Simulation._choose_skin."""
+        skin = 0.0
+        if step is not None:
+            vmax, amax, dt = step
+            cutoff = float(self.E.cutoff)
+            est = vmax * dt + amax * dt * dt
+            cap = (0.45 if self.dim == 3 else 1.0) * cutoff
+            skin = min(self._skin_factor * est + 0.02 * cutoff, cap)
+        self._call("sph_engine_build_lists", ctypes.c_double(skin))
+
+    def norms(self):
+        self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_NORMS))
+        s = self._stats()
+        from .physics import _bits_to_double
+        return [_bits_to_double(s.vmax_bits), _bits_to_double(s.amax_bits)]
+
+    def _phase(self, phase, half=0.0, full=0.0):
+        self._call("sph_engine_phase", ctypes.c_int32(phase), ctypes.c_double(float(half)),
+                   ctypes.c_double(float(full)))
+
+    def shepard(self):
+        self._call("sph_engine_shepard")
+
+    def kick_drift(self, half, full):
+        self._phase(self._native.PHASE_KICK_DRIFT, half, full)
+
+    def continuity_du(self, full):
+        self._phase(self._native.PHASE_CONTINUITY, 0.0, full)
+
+    def wall_pressure(self, initial=False):
+        self._phase(self._native.PHASE_INIT_WALL if initial else self._native.PHASE_WALL)
+
+    def momentum_kick(self, half):
+        if half is None:
+            self._phase(self._native.PHASE_INIT_MOMENTUM)
+        else:
+            self._phase(self._native.PHASE_MOMENTUM, half, 0.0)
+
+    def halo_width(self, kind):
+        return int(self.L.sph_engine_halo_width(kind))
+
+    def pack(self, kind, rows):
+        torch = _torch()
+        k = int(rows.numel())
+        out = torch.empty((k, self.halo_width(kind)), dtype=self.halo_dtype, device=self.device)
+        if k:
+            phys = self.phys_of_row[rows]
+            self._call("sph_engine_pack", ctypes.c_int32(kind), ctypes.c_void_p(phys.data_ptr()),
+                       k, ctypes.c_void_p(out.data_ptr()))
+        return out
+
+    def unpack(self, kind, rows, buf):
+        k = int(rows.numel())
+        if k:
+            phys = self.phys_of_row[rows]
+            buf = buf.contiguous()
+            self._call("sph_engine_unpack", ctypes.c_int32(kind),
+                       ctypes.c_void_p(phys.data_ptr()), k, ctypes.c_void_p(buf.data_ptr()))
+
+    def counters(self):
+        s = self._stats()
+        self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_RESET))
+        nfix = int(s.nfix)
+        frac = nfix / max(1, self.n)
+        if frac > 2e-2:
+            self._skin_factor = min(self._skin_factor * 1.5, 16.0)
+        return int(s.interactions), int(s.overflow)
+
+    def stability(self):
+        if self.n_own == 0:
+            return np.inf, 0.0
+        self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_NORMS))
+        s = self._stats()
+        from .physics import _key_to_double
+        rho_min = math.nan if s.nan_flags & 1 else _key_to_double(s.rho_min_key)
+        v2 = math.nan if s.nan_flags & 2 else _key_to_double(s.v2max_key)
+        return rho_min, v2
+
+    def export_owned(self):
+        """Owned particles (rows [0, n_own) of the last load) in registry
+        layout with global ids."""
+        torch = _torch()
+        n, d = self.n, self.dim
+        tdt = self.halo_dtype
+        out = {}
+        for f in FIELDS:
+            if f in ("x", "v", "dvdt"):
+                out[f] = torch.empty((n, d), dtype=tdt, device=self.device)
+            elif f in INDEX_FIELDS:
+                out[f] = torch.empty((n,), dtype=torch.int32, device=self.device)
+            else:
+                out[f] = torch.empty((n,), dtype=tdt, device=self.device)
+        if n:
+            order = ("x", "v", "rho", "p", "m", "Vol", "drho", "dvdt", "rho_scratch",
+                     "id", "wall", "nnb", "oflow")
+            self._call("sph_engine_pull", *[ctypes.c_void_p(out[f].data_ptr()) for f in order])
+        own = {f: out[f][: self.n_own] for f in FIELDS}
+        own["id"] = self.gid_of_lid[own["id"].to(torch.int64)]
+        return own

@@ -407,6 +407,70 @@ def _bits_to_double(b):
     return struct.unpack("<d", struct.pack("<Q", b))[0]
 
 
+def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
+    """Device storage of one engine (include/sph_b200.h SphEngine) for up to
+    n_cap particles of which at most nf_cap fluid and nw_cap wall (the list
+    tiles of the two segments are sized separately).  Returns the struct and
+    the torch tensors backing it; engine_set_counts sets the live sizes."""
+    torch = torch_mod()
+    tdt = torch.float64 if f64 else torch.float32
+    i32 = torch.int32
+    ncells = grid.cell_count
+    lib = _native.lib()
+    n = max(int(n_cap), 1)
+    tiles = max((nf_cap + 31) // 32 + (nw_cap + 31) // 32, 1)
+    T = {}
+    for k in ("pos", "vel0", "vel1", "dvdt"):
+        T[k] = torch.empty((n, 4), dtype=tdt, device=dev)
+    for k in ("rp0", "rp1", "rq"):
+        T[k] = torch.empty((n, 2), dtype=tdt, device=dev)
+    for k in ("drho", "rho_scratch_id", "vol_id", "disp"):
+        T[k] = torch.empty((n,), dtype=tdt, device=dev)
+    for k in ("id", "nnb", "refpos", "oflow_id", "wall_id", "cell0", "queue"):
+        T[k] = torch.empty((n,), dtype=i32, device=dev)
+    T["owned_id"] = torch.ones((n,), dtype=torch.uint8, device=dev)
+    T["offs_f"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
+    T["offs_w"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
+    T["lists"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
+    T["elist"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
+    for k in ("lcount", "acount", "nww"):
+        T[k] = torch.empty((tiles * 32,), dtype=i32, device=dev)
+    T["qcount"] = torch.zeros((4,), dtype=i32, device=dev)
+    ws_bytes = lib.sph_engine_workspace_bytes(n, ncells, int(f64))
+    T["ws"] = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
+    T["stats"] = torch.zeros((ctypes.sizeof(_native.SphStepStats),), dtype=torch.uint8,
+                             device=dev)
+    E = _native.SphEngine()
+    E.ncells, E.dim = ncells, d
+    E.key_bits = max(1, int(ncells - 1).bit_length())
+    E.pos = T["pos"].data_ptr()
+    E.vel[0], E.vel[1] = T["vel0"].data_ptr(), T["vel1"].data_ptr()
+    E.rp[0], E.rp[1] = T["rp0"].data_ptr(), T["rp1"].data_ptr()
+    E.rq = T["rq"].data_ptr()
+    for k in ("dvdt", "drho", "id", "nnb", "refpos", "rho_scratch_id",
+              "oflow_id", "wall_id", "vol_id", "offs_f", "offs_w", "lists",
+              "lcount", "acount", "nww", "elist", "cell0", "disp", "queue",
+              "qcount", "ws", "stats"):
+        setattr(E, k, T[k].data_ptr())
+    E.owned_id = None      # every particle owned (multi-rank runs set it)
+    E.ws_bytes = ws_bytes
+    (cs, cutoff, h, alpha_d, c0, rho0, avisc, eps_h2) = scalars
+    g = np.asarray(g)
+    origin = grid.origin.astype(np.float64 if f64 else np.float32)
+    for k in range(3):
+        E.g[k] = float(g[k]) if k < d else 0.0
+        E.origin[k] = float(origin[k]) if k < d else 0.0
+        E.shape[k] = int(grid.shape[k]) if k < d else 1
+    E.cell_size, E.cutoff, E.h, E.alpha_d = float(cs), float(cutoff), float(h), float(alpha_d)
+    E.c0, E.rho0, E.alpha_visc, E.eps_h2 = float(c0), float(rho0), float(avisc), float(eps_h2)
+    E.f64 = int(f64)
+    return E, T
+
+
+def engine_set_counts(E, n, nf):
+    E.n, E.nf = int(n), int(nf)
+
+
 class Simulation:
     """Advective-step driver (physics.py:416-564) with the state in HBM.
 
@@ -487,79 +551,18 @@ class Simulation:
     # -- device state ---------------------------------------------------------
 
     def _alloc(self):
-        torch = torch_mod()
         reg = self.registry
-        dev = device_of(self.policy)
-        n, d = reg.particle_count, reg.dim
-        f64 = reg.dtype == np.float64
-        tdt = torch.float64 if f64 else torch.float32
-        ncells = self.grid.cell_count
-        if self.grid.dim != d:
+        if self.grid.dim != reg.dim:
             raise ValueError("grid and registry dimensions differ")
-        key_bits = max(1, int(ncells - 1).bit_length())
-        lib = _native.lib()
-        wall = reg.raw_view("wall")
-        nf = int((wall == 0).sum())
-        nw = n - nf
-        tiles = (nf + 31) // 32 + (nw + 31) // 32
-        i32 = torch.int32
-        T = {}
-        T["pos"] = torch.empty((n, 4), dtype=tdt, device=dev)
-        T["vel0"] = torch.empty((n, 4), dtype=tdt, device=dev)
-        T["vel1"] = torch.empty((n, 4), dtype=tdt, device=dev)
-        T["rp0"] = torch.empty((n, 2), dtype=tdt, device=dev)
-        T["rp1"] = torch.empty((n, 2), dtype=tdt, device=dev)
-        T["rq"] = torch.empty((n, 2), dtype=tdt, device=dev)
-        T["dvdt"] = torch.empty((n, 4), dtype=tdt, device=dev)
-        T["drho"] = torch.empty((n,), dtype=tdt, device=dev)
-        for k in ("id", "nnb", "refpos", "oflow_id", "wall_id"):
-            T[k] = torch.empty((n,), dtype=i32, device=dev)
-        T["rho_scratch_id"] = torch.empty((n,), dtype=tdt, device=dev)
-        T["vol_id"] = torch.empty((n,), dtype=tdt, device=dev)
-        T["offs_f"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
-        T["offs_w"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
-        T["lists"] = torch.empty((max(tiles, 1), NEIGHBOR_CAPACITY, 32), dtype=i32,
-                                 device=dev)
-        slots = max(tiles, 1) * 32
-        T["lcount"] = torch.empty((slots,), dtype=i32, device=dev)
-        T["acount"] = torch.empty((slots,), dtype=i32, device=dev)
-        T["nww"] = torch.empty((slots,), dtype=i32, device=dev)
-        T["elist"] = torch.empty((max(tiles, 1), NEIGHBOR_CAPACITY, 32), dtype=i32,
-                                 device=dev)
-        T["cell0"] = torch.empty((max(n, 1),), dtype=i32, device=dev)
-        T["disp"] = torch.empty((max(n, 1),), dtype=tdt, device=dev)
-        T["queue"] = torch.empty((max(n, 1),), dtype=i32, device=dev)
-        T["qcount"] = torch.zeros((4,), dtype=i32, device=dev)
-        ws_bytes = lib.sph_engine_workspace_bytes(n, ncells, int(f64))
-        T["ws"] = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
-        T["stats"] = torch.zeros((ctypes.sizeof(_native.SphStepStats),),
-                                 dtype=torch.uint8, device=dev)
-        E = _native.SphEngine()
-        E.n, E.nf, E.ncells, E.dim, E.key_bits = n, nf, ncells, d, key_bits
-        E.pos = T["pos"].data_ptr()
-        E.vel[0], E.vel[1] = T["vel0"].data_ptr(), T["vel1"].data_ptr()
-        E.rp[0], E.rp[1] = T["rp0"].data_ptr(), T["rp1"].data_ptr()
-        E.rq = T["rq"].data_ptr()
-        for k in ("dvdt", "drho", "id", "nnb", "refpos", "rho_scratch_id",
-                  "oflow_id", "wall_id", "vol_id", "offs_f", "offs_w", "lists",
-                  "lcount", "acount", "nww", "elist", "cell0", "disp", "queue",
-                  "qcount", "ws", "stats"):
-            setattr(E, k, T[k].data_ptr())
-        E.ws_bytes = ws_bytes
-        (cs, cutoff, h, alpha_d, c0, rho0, avisc, eps_h2) = force_scalars(reg, self.grid)
-        g = np.asarray(reg.singular("g"))
-        origin = self.grid.origin.astype(reg.dtype)
-        for k in range(3):
-            E.g[k] = float(g[k]) if k < d else 0.0
-            E.origin[k] = float(origin[k]) if k < d else 0.0
-            E.shape[k] = int(self.grid.shape[k]) if k < d else 1
-        E.cell_size, E.cutoff, E.h, E.alpha_d = (float(cs), float(cutoff),
-                                                 float(h), float(alpha_d))
-        E.c0, E.rho0, E.alpha_visc, E.eps_h2 = (float(c0), float(rho0),
-                                                float(avisc), float(eps_h2))
-        E.f64 = int(f64)
-        self._dev = {"device": dev, "E": E, "T": T, "tdtype": tdt,
-                     "stream": stream_ptr(dev),
+        nf = int((reg.raw_view("wall") == 0).sum())
+        n = reg.particle_count
+        E, T = engine_alloc(device_of(self.policy), n, nf, n - nf, reg.dim,
+                            reg.dtype == np.float64, self.grid,
+                            force_scalars(reg, self.grid), reg.singular("g"))
+        engine_set_counts(E, n, nf)
+        torch = torch_mod()
+        self._dev = {"device": T["pos"].device, "E": E, "T": T, "tdtype": T["pos"].dtype,
+                     "stream": stream_ptr(T["pos"].device),
                      "stats_host": torch.empty(T["stats"].shape, dtype=torch.uint8,
                                                pin_memory=True)}
 

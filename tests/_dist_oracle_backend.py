@@ -2,29 +2,43 @@
 protocol (test infrastructure).  Every phase runs the oracle's restated
 reference bodies (oracle/sph_oracle.c) over the rank's owned + ghost
 particles; the decomposition logic under test is the product's
-(paper_2603_11868_b200/distributed.py)."""
+(paper_2603_11868_b200/distributed.py).  Halo records: XV = (x, v) rows,
+RP_* = (rho, p) rows."""
 
 import numpy as np
+import torch
 
 from oracle import oracle as O
-from paper_2603_11868_b200.distributed import FIELDS
+from paper_2603_11868_b200.distributed import (FIELDS, INDEX_FIELDS, XV, as_tensor,
+                                               cell_plane)
 
 
 class OracleBackend:
-    def __init__(self, scalars, sing):
+    def __init__(self, scalars, sing, grid):
         # scalars = force_args tail (cell_size, cutoff, h, alpha_d, c0, rho0,
         # alpha_visc, eps_h2) in the run dtype; sing: rho0, c0, h, g
         self.sc = scalars
         self.sing = sing
+        self.grid = grid
         self.f = None
         self.n_own = 0
         self._inter = 0
         self._ovf = 0
+        self.halo_dtype = torch.from_numpy(np.zeros(1, type(scalars[0]))).dtype
+
+    def planes(self, x):
+        xn = x.numpy()
+        return torch.from_numpy(cell_plane(xn[:, 0], self.grid.origin.astype(xn.dtype)[0],
+                                           xn.dtype.type(self.grid.cell_size),
+                                           int(self.grid.shape[0])))
 
     def load(self, local, n_owned, grid):
-        self.f = {k: np.array(local[k], copy=True, order="C") for k in FIELDS}
+        self.f = {}
+        for k in FIELDS:
+            a = local[k].numpy()
+            self.f[k] = np.array(a.view(np.uint32) if k in INDEX_FIELDS else a,
+                                 copy=True, order="C")
         self.n_own = n_owned
-        self.grid = grid
         x = self.f["x"]
         dt = x.dtype.type
         self.origin = grid.origin.astype(x.dtype)
@@ -33,6 +47,9 @@ class OracleBackend:
         _, oob_own = O.compute_keys(x[:n_owned], self.origin, dt(grid.cell_size), self.shape)
         self.offsets, self.pids = O.build_cll(keys, grid.cell_count)
         return oob_own
+
+    def prepare(self, step):
+        pass
 
     def _force(self):
         f = self.f
@@ -65,7 +82,6 @@ class OracleBackend:
         f = self.f
         O.integrate("kick", (f["v"], f["dvdt"], f["wall"], half))
         O.integrate("drift", (f["x"], f["v"], f["wall"], full))
-        self._half = half
 
     def continuity_du(self, full):
         f = self.f
@@ -94,12 +110,29 @@ class OracleBackend:
         if half is not None:
             O.integrate("kick", (f["v"], f["dvdt"], f["wall"], half))
 
-    def get(self, name, idx):
-        a = self.f[name]
-        return a if idx is None else a[idx]
+    def halo_width(self, kind):
+        return 2 * self.f["x"].shape[1] if kind == XV else 2
 
-    def set(self, name, idx, vals):
-        self.f[name][idx] = vals
+    def pack(self, kind, rows):
+        r = rows.numpy()
+        f = self.f
+        if kind == XV:
+            a = np.concatenate([f["x"][r], f["v"][r]], axis=1)
+        else:
+            a = np.stack([f["rho"][r], f["p"][r]], axis=1)
+        return torch.from_numpy(np.ascontiguousarray(a))
+
+    def unpack(self, kind, rows, buf):
+        r = rows.numpy()
+        b = buf.numpy()
+        f = self.f
+        if kind == XV:
+            d = f["x"].shape[1]
+            f["x"][r] = b[:, :d]
+            f["v"][r] = b[:, d:]
+        else:
+            f["rho"][r] = b[:, 0]
+            f["p"][r] = b[:, 1]
 
     def counters(self):
         out = (self._inter, self._ovf)
@@ -114,4 +147,4 @@ class OracleBackend:
         return float(self.f["rho"][:n].min()), float((v * v).sum(axis=1).max())
 
     def export_owned(self):
-        return {k: self.f[k][: self.n_own].copy() for k in FIELDS}
+        return {k: as_tensor(self.f[k][: self.n_own].copy(), "cpu") for k in FIELDS}

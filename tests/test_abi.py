@@ -13,7 +13,7 @@ HEADER = os.path.join(ROOT, "include", "sph_b200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|long long|const char\*)\s+(sph_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|size_t|long long|const char\*)\s+(sph_\w+)\s*\(",
                                  text, flags=re.M)))
 
 
@@ -26,7 +26,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_native.EXPORTED)
-    assert lib.sph_abi_version() == 1
+    assert lib.sph_abi_version() == 2
 
 
 def test_struct_layouts_match_header():

@@ -46,7 +46,7 @@ def _worker(rank, world, port, kind, steps, shepard_every, rebalance, out_q):
         sel = np.arange(n) % world == rank
         owned = {f: reg.raw_view(f)[sel] for f in FIELDS}
         sing = {k: reg.singular(k) for k in ("rho0", "c0", "h", "g")}
-        be = OracleBackend(force_scalars(reg, grid), sing)
+        be = OracleBackend(force_scalars(reg, grid), sing, grid)
         sim = DistributedSimulation(Comm(), be, grid, owned, sing,
                                     shepard_every=shepard_every,
                                     rebalance_every=rebalance)
