@@ -6,9 +6,10 @@
 One "step" = one Simulation.advance (physics.py:489-552): CLL rebuild, the
 time-step reductions and nsub acoustic sub-steps, exactly the reference's
 work.  value = particles x steps / device time (CUDA events, summed over
-steps; L2 flushed between steps), whole job = sum over ranks.  At N > 1 each
-rank runs its own replica of the configuration (weak scaling; slab
-decomposition is not in this round -- see DESIGN.md).
+steps; L2 flushed between steps; max over ranks).  At N > 1 the same
+configuration is slab-partitioned over the N GPUs (distributed.py: balanced
+axis-0 slabs, 2-plane halos, NCCL halo exchange and migration; strong
+scaling, results bit-identical to one GPU).
 
 Prints ONE JSON line (rank 0).
 """
@@ -297,9 +298,8 @@ def gpu_arm(args, rank, world, local_rank):
         "config": {"workload": CONFIGS[args.config][0], "case": args.config,
                    "particles": n, "fluid": nf, "wall": nw, "grid_cells": ncells,
                    "nsub_per_step": nsubs, "l2": "flushed between steps (256 MB write)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "sub_step_updates_per_s": world * n * sum(nsubs) / total,
-                   "gpips": world * 0 if False else None},
+                   "parallelism": "single GPU",
+                   "sub_step_updates_per_s": world * n * sum(nsubs) / total},
         "gpu_launches": int(launches),
         "clocks": clocks,
         "roofline": {
@@ -316,6 +316,121 @@ def gpu_arm(args, rank, world, local_rank):
             "note": "sweeps are FP64/issue bound in bit-exact mode (SURVEY 8d); "
                     "see profiles/ for ncu pipe utilisation"},
         "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def slab_arm(args, rank, world, local_rank):
+    """N > 1: the configuration slab-partitioned over the ranks (SURVEY.md
+    8e) through distributed.DistributedSimulation with the CUDA engine."""
+    import numpy as np
+    import torch
+    from paper_2603_11868_b200 import _native
+    from paper_2603_11868_b200.distributed import (FIELDS, Comm, DistributedSimulation,
+                                                   EngineBackend, SlabLayout, cell_plane)
+    from paper_2603_11868_b200.physics import force_scalars
+
+    dev = torch.device("cuda", local_rank)
+    lib = _native.lib()
+    reg, grid = build_case(args.config)
+    n = reg.particle_count
+    d = reg.dim
+    nw = int((reg.raw_view("wall") != 0).sum())
+    nf = n - nw
+    x = reg.raw_view("x")
+    planes = cell_plane(x[:, 0], grid.origin.astype(x.dtype)[0], x.dtype.type(grid.cell_size),
+                        int(grid.shape[0]))
+    layout = SlabLayout.balanced(np.bincount(planes, minlength=int(grid.shape[0])), world)
+    mine = layout.owner(planes) == rank
+    owned = {f: reg.raw_view(f)[mine] for f in FIELDS}
+    sing = {k: reg.singular(k) for k in ("rho0", "c0", "h", "g")}
+    comm = Comm(dev)
+    be = EngineBackend(force_scalars(reg, grid), sing, grid, dev)
+    sim = DistributedSimulation(comm, be, grid, owned, sing, layout=layout, rebalance_every=10)
+    del reg, owned
+    sim.initialize()
+    for _ in range(args.warmup):
+        sim.advance()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    sampler = ClockSampler(local_rank)
+    torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.sph_kernel_launches()
+    sampler.start()
+    times, nsubs = [], []
+    for _ in range(args.steps):
+        flush.zero_()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        sim.advance()
+        ev1.record()
+        ev1.synchronize()
+        times.append(ev0.elapsed_time(ev1) / 1e3)
+        nsubs.append(sim.last_nsub)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = lib.sph_kernel_launches() - launches0
+    total = float(comm.allreduce([sum(times)], "max")[0])
+    value = n * args.steps / total
+
+    e2e = None
+    if not args.no_e2e:   # public API with the owned state in pinned host memory
+        cap = {f: int(sim.owned[f].shape[0] * 1.5) + 1024 for f in FIELDS}
+        host = {f: torch.empty((cap[f],) + tuple(sim.owned[f].shape[1:]),
+                               dtype=sim.owned[f].dtype, pin_memory=True) for f in FIELDS}
+        cnt = int(sim.owned["id"].shape[0])
+        for f in FIELDS:
+            host[f][:cnt].copy_(sim.owned[f])
+        ksteps = max(1, min(args.steps, 3))
+        torch.distributed.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nb_in = nb_out = 0
+        for _ in range(ksteps):
+            sim.owned = {f: host[f][:cnt].to(dev, non_blocking=True) for f in FIELDS}
+            nb_in = sum(host[f][:cnt].numel() * host[f].element_size() for f in FIELDS)
+            sim.advance()
+            cnt = int(sim.owned["id"].shape[0])
+            for f in FIELDS:
+                host[f][:cnt].copy_(sim.owned[f])
+            nb_out = sum(host[f][:cnt].numel() * host[f].element_size() for f in FIELDS)
+        torch.cuda.synchronize()
+        secs = float(comm.allreduce([time.perf_counter() - t0], "max")[0])
+        e2e = {"value": n * ksteps / secs, "unit": UNIT,
+               "h2d_bytes_per_step": nb_in, "d2h_bytes_per_step": nb_out, "steps": ksteps,
+               "timer": "host wall clock, max over ranks, around H2D of the owned "
+                        "state + advance + D2H (rank 0's bytes)"}
+    peaks, peak_src = measured_peaks()
+    ncells = grid.cell_count
+    passes = max(1, math.ceil(max(1, (ncells - 1).bit_length()) / 8))
+    b_full = step_bytes_model(d, n, nf, nw, statistics.mean(nsubs), ncells, passes)
+    per_gpu = value / world * b_full / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 (mixed f64)",
+        "data": "synthetic (reference lattice dam break, deterministic)",
+        "config": {"workload": CONFIGS[args.config][0], "case": args.config,
+                   "particles": n, "fluid": nf, "wall": nw, "grid_cells": ncells,
+                   "nsub_per_step": nsubs, "l2": "flushed between steps (256 MB write)",
+                   "parallelism": f"slabs x{world} (axis-0, 2-plane halos, NCCL P2P)",
+                   "slab_cuts": [int(c) for c in sim.layout.cuts],
+                   "sub_step_updates_per_s": n * sum(nsubs) / total},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "roofline": {
+            "bound": "hbm", "kernel": "whole step (byte model)", "achieved": per_gpu,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": per_gpu / peaks["hbm_gbs"],
+            "traffic": None, "peak_source": peak_src,
+            "step_model_bytes_per_update": b_full,
+            "note": "per-GPU step-level byte model (SURVEY 8d); the per-kernel split "
+                    "is measured by the 1-GPU run"},
+        "cpu_baseline": None,
         "e2e": e2e,
     }
     if rank == 0:
@@ -377,11 +492,18 @@ def main():
         return
     if world > 1:
         import torch
+        local_rank %= max(1, torch.cuda.device_count())   # ranks sharing a GPU (gloo check)
         torch.cuda.set_device(local_rank)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.distributed.init_process_group("nccl")
+        # NCCL between GPUs; SPH_BENCH_BACKEND=gloo runs the same slab path
+        # host-staged (e.g. ranks sharing one GPU to validate it -- not a
+        # performance configuration)
+        torch.distributed.init_process_group(os.environ.get("SPH_BENCH_BACKEND", "nccl"))
     try:
-        gpu_arm(args, rank, world, local_rank)
+        if world > 1:
+            slab_arm(args, rank, world, local_rank)
+        else:
+            gpu_arm(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch

@@ -255,12 +255,27 @@ class DistributedSimulation:
         self.layout = SlabLayout.balanced(tot, self.comm.size)
 
     def _exchange_fields(self, fields, send_rows, recv_counts):
-        out = {}
-        for f in FIELDS:
-            arr = fields[f]
-            got = self.comm.exchange({q: arr[r] for q, r in send_rows.items()}, recv_counts,
-                                     arr.shape[1:], arr.dtype)
-            out[f] = got
+        """Rows of every field to each neighbour in ONE message: the fields
+        are viewed as int32 columns of one (n, width) matrix."""
+        torch = self.comm.torch
+        n = int(fields["id"].shape[0])
+        widths = [int(np.prod(fields[f].shape[1:], dtype=np.int64)) *
+                  fields[f].element_size() // 4 for f in FIELDS]
+        if n:
+            packed = torch.cat([fields[f].reshape(n, -1).contiguous().view(torch.int32)
+                                for f in FIELDS], dim=1)
+        else:
+            packed = torch.empty((0, sum(widths)), dtype=torch.int32, device=self.comm.device)
+        got = self.comm.exchange({q: packed[r] for q, r in send_rows.items()}, recv_counts,
+                                 (sum(widths),), torch.int32)
+        out = {f: {} for f in FIELDS}
+        for q, m in got.items():
+            c0 = 0
+            for f, w in zip(FIELDS, widths):
+                ref = fields[f]
+                out[f][q] = m[:, c0:c0 + w].contiguous().view(ref.dtype).reshape(
+                    (m.shape[0],) + tuple(ref.shape[1:]))
+                c0 += w
         return out
 
     def _migrate(self):
@@ -520,6 +535,7 @@ class EngineBackend:
             self.phys_of_row = torch.empty(n, dtype=torch.int32, device=self.device)
             self.phys_of_row[ref] = torch.arange(n, dtype=torch.int32, device=self.device)
             del args
+        self._phys = {}
         self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_RESET))
         oob = 0
         if n_owned:
@@ -570,12 +586,21 @@ class EngineBackend:
     def halo_width(self, kind):
         return int(self.L.sph_engine_halo_width(kind))
 
+    def _phys_of(self, rows):
+        # the orchestrator's row selections live for the whole step
+        key = id(rows)
+        hit = self._phys.get(key)
+        if hit is None or hit[0] is not rows:
+            hit = (rows, self.phys_of_row[rows])
+            self._phys[key] = hit
+        return hit[1]
+
     def pack(self, kind, rows):
         torch = _torch()
         k = int(rows.numel())
         out = torch.empty((k, self.halo_width(kind)), dtype=self.halo_dtype, device=self.device)
         if k:
-            phys = self.phys_of_row[rows]
+            phys = self._phys_of(rows)
             self._call("sph_engine_pack", ctypes.c_int32(kind), ctypes.c_void_p(phys.data_ptr()),
                        k, ctypes.c_void_p(out.data_ptr()))
         return out
@@ -583,7 +608,7 @@ class EngineBackend:
     def unpack(self, kind, rows, buf):
         k = int(rows.numel())
         if k:
-            phys = self.phys_of_row[rows]
+            phys = self._phys_of(rows)
             buf = buf.contiguous()
             self._call("sph_engine_unpack", ctypes.c_int32(kind),
                        ctypes.c_void_p(phys.data_ptr()), k, ctypes.c_void_p(buf.data_ptr()))
