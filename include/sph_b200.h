@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 2
+#define SPH_ABI_VERSION 3
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -184,10 +184,11 @@ typedef struct {
     /* sizes */
     int64_t n, nf, ncells; int32_t dim; int32_t key_bits;
     /* per-particle SoA, physical order (dev).  f32 run: float4/float2,
-     * f64 run: double4/double2 (reinterpret). pos.w == m; vel.w is scratch
+     * f64 run: double4/double2 (reinterpret). pos.w == m; pos, vel and rp
+     * are double buffers (cur_pos / cur_v / cur_rp select); vel.w is scratch
      * (m/rho of the sub-step's continuity sweep); rq = (rho, p/rho^2) of the
      * sub-step's momentum sweep (library-maintained, no host meaning). */
-    void* pos; void* vel[2]; void* rp[2]; void* rq; void* dvdt; void* drho;
+    void* pos[2]; void* vel[2]; void* rp[2]; void* rq; void* dvdt; void* drho;
     uint32_t* id; uint32_t* nnb; uint32_t* refpos;
     /* by-id cold fields (dev) */
     void* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; void* vol_id;
@@ -212,7 +213,8 @@ typedef struct {
     double cell_size, cutoff, h, alpha_d, c0, rho0, alpha_visc, eps_h2;
     double skin;                      /* Verlet skin of the current lists    */
     /* double-buffer selectors and list state, maintained by the library */
-    int32_t cur_v, cur_rp;
+    int32_t cur_v, cur_rp, cur_pos;
+    int32_t drifted;                  /* next sub-step's kick+drift already applied */
     int32_t f64;                      /* 0: f32 run, 1: f64 run */
     int32_t lists_ready;
 } SphEngine;
@@ -246,6 +248,16 @@ int sph_engine_shepard(SphEngine* e, cudaStream_t s);
 /* physics.py:522-548 one acoustic sub-step: KICK, DRIFT, CONTINUITY,
  * DENSITY_UPDATE, WALL_PRESSURE, MOMENTUM, KICK (fused) */
 int sph_engine_substep(SphEngine* e, double half_dt, double full_dt, cudaStream_t s);
+/* nsub consecutive sub-steps of one advective step (physics.py:522-548): the
+ * momentum sweep of every sub-step but the last also applies the next
+ * sub-step's KICK + DRIFT (same dt), writing positions to the other buffer,
+ * so one pass over the particles disappears per sub-step */
+int sph_engine_substeps(SphEngine* e, double half_dt, double full_dt, int32_t nsub,
+                        cudaStream_t s);
+/* the same, synchronised, with the CUDA-event time of each of the five
+ * parts summed over the sub-steps (ms_out[5]; see sph_engine_substep_timed) */
+int sph_engine_substeps_timed(SphEngine* e, double half_dt, double full_dt, int32_t nsub,
+                              float* ms_out, cudaStream_t s);
 /* the same sub-step, synchronised, with CUDA-event times (ms) of its five
  * kernels: kick+drift, neighbour lists, continuity+density update, wall
  * pressure, momentum+kick (bench.py per-kernel roofline) */

@@ -74,7 +74,7 @@ class SphEngine(C.Structure):
     _fields_ = [
         ("n", c_i64), ("nf", c_i64), ("ncells", c_i64),
         ("dim", c_i32), ("key_bits", c_i32),
-        ("pos", P), ("vel", P * 2), ("rp", P * 2), ("rq", P), ("dvdt", P), ("drho", P),
+        ("pos", P * 2), ("vel", P * 2), ("rp", P * 2), ("rq", P), ("dvdt", P), ("drho", P),
         ("id", P), ("nnb", P), ("refpos", P),
         ("rho_scratch_id", P), ("oflow_id", P), ("wall_id", P), ("vol_id", P),
         ("owned_id", P),
@@ -87,11 +87,11 @@ class SphEngine(C.Structure):
         ("cell_size", c_f64), ("cutoff", c_f64), ("h", c_f64), ("alpha_d", c_f64),
         ("c0", c_f64), ("rho0", c_f64), ("alpha_visc", c_f64), ("eps_h2", c_f64),
         ("skin", c_f64),
-        ("cur_v", c_i32), ("cur_rp", c_i32), ("f64", c_i32), ("lists_ready", c_i32),
+        ("cur_v", c_i32), ("cur_rp", c_i32), ("cur_pos", c_i32), ("drifted", c_i32), ("f64", c_i32), ("lists_ready", c_i32),
     ]
 
 
-ABI_VERSION = 2   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 3   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)
@@ -123,6 +123,8 @@ _PROTOS = {
     "sph_engine_substep": (c_i32, [_P, c_f64, c_f64, _P]),
     "sph_engine_substep_timed": (c_i32, [_P, c_f64, c_f64, _P, _P]),
     "sph_engine_stats": (c_i32, [_P, c_i32, _P]),
+    "sph_engine_substeps": (c_i32, [_P, c_f64, c_f64, c_i32, _P]),
+    "sph_engine_substeps_timed": (c_i32, [_P, c_f64, c_f64, c_i32, _P, _P]),
     "sph_engine_phase": (c_i32, [_P, c_i32, c_f64, c_f64, _P]),
     "sph_engine_halo_width": (c_i32, [c_i32]),
     "sph_engine_pack": (c_i32, [_P, c_i32, _P, c_i64, _P, _P]),

@@ -162,47 +162,234 @@ __device__ __forceinline__ void enqueue(uint32_t* queue, uint32_t* qcount, bool 
 // ---------------------------------------------------------------------------
 // skin lists (one per advective step)
 // ---------------------------------------------------------------------------
+// Every particle of a cell shares the cell's 3^d candidate block, so the
+// lists are built per CELL: one block loads the block's candidates once,
+// sorts them by original id in shared memory, and then each warp streams
+// the sorted candidates past one particle of the cell -- the ballot-compacted
+// survivors are already in ascending id, so no per-particle sort is needed.
+// Blocks larger than the tile fall back to the per-particle collector.
+template <class T, int D> struct SkinTile;
+template <> struct SkinTile<float, 2> { static constexpr int kThreads = 128, kCands = 256; };
+template <> struct SkinTile<float, 3> { static constexpr int kThreads = 256, kCands = 1024; };
+template <> struct SkinTile<double, 2> { static constexpr int kThreads = 128, kCands = 256; };
+template <> struct SkinTile<double, 3> { static constexpr int kThreads = 256, kCands = 512; };
+
+template <class T, int D>
+__global__ void __launch_bounds__(SkinTile<T, D>::kThreads, 2048 / SkinTile<T, D>::kThreads)
+k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E, int64_t ncells)
+{
+    constexpr int NT = SkinTile<T, D>::kThreads, NW = NT / 32, kC = SkinTile<T, D>::kCands;
+    __shared__ unsigned long long skey[kC];
+    __shared__ vec4<T> spos[kC];
+    __shared__ uint32_t run_start[2 * 9], run_pre[2 * 9 + 1];
+    const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+    const unsigned lt = lanemask_lt();
+    const int64_t nf = E.nf;
+    for (int64_t c = blockIdx.x; c < ncells; c += gridDim.x) {
+        const uint32_t f0 = E.offs_f[c], f1 = E.offs_f[c + 1];
+        const uint32_t w0 = E.offs_w[c], w1 = E.offs_w[c + 1];
+        const int ntf = (int)(f1 - f0), nt = ntf + (int)(w1 - w0);
+        if (nt == 0) continue;   // uniform over the block
+        int cc[3];
+        if (D == 3) {
+            cc[2] = (int)(c % g.s[2]);
+            cc[1] = (int)((c / g.s[2]) % g.s[1]);
+            cc[0] = (int)(c / ((int64_t)g.s[1] * g.s[2]));
+        } else {
+            cc[1] = (int)(c % g.s[1]);
+            cc[0] = (int)(c / g.s[1]);
+            cc[2] = 0;
+        }
+        const int xlo = max(cc[0] - 1, 0), xhi = min(cc[0] + 1, g.s[0] - 1);
+        const int ylo = max(cc[1] - 1, 0), yhi = min(cc[1] + 1, g.s[1] - 1);
+        const int zlo = D == 3 ? max(cc[2] - 1, 0) : 0;
+        const int zhi = D == 3 ? min(cc[2] + 1, g.s[2] - 1) : 0;
+        const int nyr = D == 3 ? (yhi - ylo + 1) : 1;
+        const int rps = (xhi - xlo + 1) * nyr;
+        const int nruns = 2 * rps;
+        if (warp == 0) {   // run bounds of both segments + exclusive prefix
+            int64_t s0 = 0, s1 = 0;
+            if ((int)lane < nruns) {
+                const int seg = (int)lane / rps, rr = (int)lane - seg * rps;
+                const int ax = xlo + rr / nyr, ay = ylo + rr % nyr;
+                uint32_t klo, khi;
+                if (D == 3) {
+                    const uint32_t rowk = ((uint32_t)ax * g.s[1] + ay) * g.s[2];
+                    klo = rowk + zlo;
+                    khi = rowk + zhi;
+                } else {
+                    klo = (uint32_t)ax * g.s[1] + ylo;
+                    khi = (uint32_t)ax * g.s[1] + yhi;
+                }
+                acc.run(seg, klo, khi, s0, s1);
+            }
+            const uint32_t len = (uint32_t)(s1 - s0);
+            uint32_t incl = len;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (unsigned)o) incl += t;
+            }
+            if ((int)lane < nruns) {
+                run_start[lane] = (uint32_t)s0;
+                run_pre[lane] = incl - len;
+            }
+            if ((int)lane == nruns - 1) run_pre[nruns] = incl;
+        }
+        __syncthreads();
+        const int M = (int)run_pre[nruns];
+        if (M <= kC) {
+            int P = 32;
+            while (P < M) P <<= 1;
+            for (int k = tid; k < P; k += NT) {
+                unsigned long long key = ~0ull;
+                if (k < M) {
+                    int r = 0;
+                    while (r + 1 < nruns && run_pre[r + 1] <= (uint32_t)k) r++;
+                    const uint32_t j = run_start[r] + ((uint32_t)k - run_pre[r]);
+                    key = ((unsigned long long)E.id[j] << 32) | j;
+                }
+                skey[k] = key;
+            }
+            __syncthreads();
+            for (int k = 2; k <= P; k <<= 1) {          // ascending bitonic by id
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    for (int q = tid; q < (P >> 1); q += NT) {
+                        const int lo = ((q & ~(j - 1)) << 1) | (q & (j - 1)), hi = lo + j;
+                        const unsigned long long x0 = skey[lo], x1 = skey[hi];
+                        if ((x0 > x1) == ((lo & k) == 0)) { skey[lo] = x1; skey[hi] = x0; }
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int k = tid; k < M; k += NT) spos[k] = E.pos[(uint32_t)skey[k]];
+            __syncthreads();
+            for (int t = warp; t < nt; t += NW) {
+                const bool fluid = t < ntf;
+                const int64_t i = fluid ? (int64_t)f0 + t : nf + w0 + (t - ntf);
+                const int64_t slot = fluid ? i : E.nf_pad + (i - nf);
+                T xi[3];
+                to3<T>(E.pos[i], xi);
+                int cxyz[3];
+                const bool in_cell = cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c;
+                int cnt = 0, nacc = 0;
+                for (int base = 0; base < M; base += 32) {
+                    const int k = base + (int)lane;
+                    bool st = false, ct = false;
+                    uint32_t j = 0;
+                    if (k < M) {
+                        j = (uint32_t)skey[k];
+                        T xj[3];
+                        to3<T>(spos[k], xj);
+                        const T r2 = accept_r2<T, D>(xi, xj);
+                        const bool stores = fluid || (int64_t)j < nf;
+                        if ((int64_t)j != i) {
+                            st = stores && (r2 < cs2);
+                            ct = !stores && (r2 < g.c2) && (r2 > T(0));
+                        }
+                    }
+                    const unsigned bs = __ballot_sync(0xffffffffu, st);
+                    if (st) {
+                        const int p = cnt + __popc(bs & lt);
+                        if (p < kCap) E.lists[ell_index(slot, p)] = (int32_t)j;
+                    }
+                    cnt += __popc(bs);
+                    nacc += __popc(__ballot_sync(0xffffffffu, ct));
+                }
+                if (lane == 0) {
+                    const bool ok = in_cell && cnt <= kCap;
+                    E.cell0[i] = ok ? (uint32_t)c : kInvalidCell;
+                    E.lcount[slot] = ok ? cnt : 0;
+                    E.nww[slot] = nacc;   // walls: static wall-wall count
+                    E.disp[i] = T(0);
+                }
+            }
+        } else if (tid == 0) {   // oversized block: per-particle path (k_skin_big)
+            E.queue[atomicAdd(E.qcount, 1u)] = (uint32_t)c;
+        }
+        __syncthreads();   // shared tile reused by the next cell
+    }
+}
+
+// skin lists of the cells k_skin_tile queued (candidate block above the
+// tile): one warp per particle of the cell, per-particle collect + sort
 template <class T, int D>
 __global__ void __launch_bounds__(kNlThreads, 4)
-k_skin_build(const EngAcc<T> acc, const GridP<T> g, T cs2, int64_t first, int64_t count,
-             int64_t slot_first, unsigned store_mask, Eng<T> E)
+k_skin_big(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E)
 {
-    // one warp per particle, grid-stride; lists written straight into the
-    // tile-ELL slot (L2 merges the 4-byte column writes of a tile's warps),
-    // which keeps shared memory at 16 KB per block and occupancy at 64 warps
     __shared__ WarpBuf bufs[kNlWarps];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     WarpBuf& sb = bufs[warp];
-    for (int64_t t = (int64_t)blockIdx.x * kNlWarps + warp; t < count;
-         t += (int64_t)gridDim.x * kNlWarps) {
-        const int64_t i = first + t;
-        const int64_t slot = slot_first + t;
-        T xi[3];
-        acc.position(i, xi);
-        CollectCounts cc = warp_collect<T, D, true>(acc, g, i, xi, cs2, store_mask, sb);
-        int c[3];
-        const uint32_t key0 = cell_key_of<T, D>(xi, g, c);
-        int stored = cc.stored;
-        if (stored > kCap) {   // list storage exhausted: exact rebuilds instead
-            stored = 0;
-        } else {
-            warp_emit_sorted(sb, stored, lane, [&](int pos, uint32_t j) {
-                E.lists[ell_index(slot, pos)] = (int32_t)j;
-            });
+    const uint32_t nq = *(volatile uint32_t*)E.qcount;
+    const int64_t nf = E.nf;
+    for (uint32_t q = blockIdx.x; q < nq; q += gridDim.x) {
+        const uint32_t c = E.queue[q];
+        const uint32_t f0 = E.offs_f[c], ntf = E.offs_f[c + 1] - f0;
+        const uint32_t w0 = E.offs_w[c], nt = ntf + (E.offs_w[c + 1] - w0);
+        for (uint32_t t = warp; t < nt; t += kNlWarps) {
+            const bool fluid = t < ntf;
+            const int64_t i = fluid ? (int64_t)f0 + t : nf + w0 + (t - ntf);
+            const int64_t slot = fluid ? i : E.nf_pad + (i - nf);
+            T xi[3];
+            acc.position(i, xi);
+            CollectCounts cnts = warp_collect<T, D, true>(acc, g, i, xi, cs2, fluid ? 3u : 1u, sb);
+            int cxyz[3];
+            const uint32_t key0 = cell_key_of<T, D>(xi, g, cxyz);
+            int stored = cnts.stored;
+            if (stored > kCap) {
+                stored = 0;
+            } else {
+                warp_emit_sorted(sb, stored, lane, [&](int pos, uint32_t j) {
+                    E.lists[ell_index(slot, pos)] = (int32_t)j;
+                });
+            }
+            if (lane == 0) {
+                E.cell0[i] = cnts.stored > kCap ? kInvalidCell : key0;
+                E.lcount[slot] = stored;
+                E.nww[slot] = cnts.accepted;
+                E.disp[i] = T(0);
+            }
+            __syncwarp();
         }
-        if (lane == 0) {
-            E.cell0[i] = cc.stored > kCap ? kInvalidCell : key0;
-            E.lcount[slot] = stored;
-            E.nww[slot] = cc.accepted;   // walls: static wall-wall count
-            E.disp[i] = T(0);
-        }
-        __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------------------
 // per-sub-step list maintenance
 // ---------------------------------------------------------------------------
+// physics.py:526-529 KICK(half) then DRIFT(full) of one fluid particle
+// (in registers); returns the new position
+template <class T, int D>
+__device__ __forceinline__ void kick_drift_one(vec4<T>& P4, vec4<T>& V4, const vec4<T>& A4,
+                                               T half, T full)
+{
+    V4.x = RN<T>::add(V4.x, RN<T>::mul(half, A4.x));
+    V4.y = RN<T>::add(V4.y, RN<T>::mul(half, A4.y));
+    if (D == 3) V4.z = RN<T>::add(V4.z, RN<T>::mul(half, A4.z));
+    P4.x = RN<T>::add(P4.x, RN<T>::mul(full, V4.x));
+    P4.y = RN<T>::add(P4.y, RN<T>::mul(full, V4.y));
+    if (D == 3) P4.z = RN<T>::add(P4.z, RN<T>::mul(full, V4.z));
+}
+
+// skin-list bookkeeping of a drift xo -> xn: the path length bound (upward
+// rounded |xn - xo| added to disp) and the list-cell check; returns the bound
+template <class T, int D>
+__device__ __forceinline__ T drift_bookkeeping(const Eng<T>& E, const GridP<T>& g, int64_t i,
+                                               const T (&xo)[3], const T (&xn)[3])
+{
+    T s2 = T(0);
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+        const T dk = RN<T>::mul_ru(fabs(RN<T>::sub(xn[k], xo[k])), RN<T>::kOnePlus2Eps);
+        s2 = RN<T>::add_ru(s2, RN<T>::mul_ru(dk, dk));
+    }
+    const T dnew = RN<T>::add_ru(E.disp[i], RN<T>::sqrt_ru(s2));
+    E.disp[i] = dnew;
+    int c[3];
+    if (cell_key_of<T, D>(xn, g, c) != E.cell0[i]) E.cell0[i] = kInvalidCell;
+    return dnew;
+}
+
 // physics.py:526-529 KICK(half) then DRIFT(full), fluid only, plus the
 // upward-rounded displacement bound and the list-cell check
 template <class T, int D>
@@ -221,28 +408,12 @@ k_kick_drift(Eng<T> E, int cv, int crp, GridP<T> g, T half, T full)
         // the continuity operand m_j/rho_j of this sub-step (physics.py:113):
         // a per-particle quotient, evaluated once here instead of per pair
         V4.w = RN<T>::div(P4.w, E.rp[crp][i].x);
-        V4.x = RN<T>::add(V4.x, RN<T>::mul(half, A4.x));
-        V4.y = RN<T>::add(V4.y, RN<T>::mul(half, A4.y));
-        if (D == 3) V4.z = RN<T>::add(V4.z, RN<T>::mul(half, A4.z));
         const T xo[3] = {P4.x, P4.y, P4.z};
-        P4.x = RN<T>::add(P4.x, RN<T>::mul(full, V4.x));
-        P4.y = RN<T>::add(P4.y, RN<T>::mul(full, V4.y));
-        if (D == 3) P4.z = RN<T>::add(P4.z, RN<T>::mul(full, V4.z));
+        kick_drift_one<T, D>(P4, V4, A4, half, full);
         E.vel[cv][i] = V4;
         E.pos[i] = P4;
-        // |x_new - x_old| bounded from above
         const T xn[3] = {P4.x, P4.y, P4.z};
-        T s2 = T(0);
-#pragma unroll
-        for (int k = 0; k < D; k++) {
-            const T dk = RN<T>::mul_ru(fabs(RN<T>::sub(xn[k], xo[k])), RN<T>::kOnePlus2Eps);
-            s2 = RN<T>::add_ru(s2, RN<T>::mul_ru(dk, dk));
-        }
-        dnew = RN<T>::add_ru(E.disp[i], RN<T>::sqrt_ru(s2));
-        E.disp[i] = dnew;
-        int c[3];
-        const uint32_t key = cell_key_of<T, D>(xn, g, c);
-        if (key != E.cell0[i]) E.cell0[i] = kInvalidCell;
+        dnew = drift_bookkeeping<T, D>(E, g, i, xo, xn);
     }
     const unsigned long long b = warp_max_u64(dbits(double(dnew)));
     if (lane_id() == 0 && b) atomicMax(&E.stats->dmax_bits, b);
@@ -429,7 +600,8 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
 // used by no other sweep, so they are not stored).
 template <class T, int D>
 __global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
-k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor, int filter)
+k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor, int filter,
+       int cvn)
 {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long visits_sum = 0;
@@ -469,6 +641,9 @@ k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor,
             out.x = RN<T>::add(P.rho0, RN<T>::div(out.y, P.c0c0));
             rp[i] = out;
             E.rq[i] = rq_of<T>(out);
+            // the next sub-step's continuity operand m/rho, in the velocity
+            // buffer current then (walls never move: both buffers agree)
+            if (cvn >= 0) reinterpret_cast<T*>(&E.vel[cvn][i])[3] = RN<T>::div(E.pos[i].w, out.x);
             E.nnb[i] = (uint32_t)acnt;
             if (zero_drho) E.drho[i] = T(0);
             if (is_owned(E, i))
@@ -480,12 +655,19 @@ k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor,
 
 // physics.py:122-158 MOMENTUM (+ :546-547 KICK(half) into the other velocity
 // buffer when kick != 0), fluid only; rho/p from buffer brp.
+//
+// fuse != 0 (every sub-step of a step but the last): the next sub-step's
+// KICK(half) + DRIFT(full) with the same dvdt follow here -- positions into
+// the other buffer, m/rho for its continuity sweep, the skin-list
+// bookkeeping -- so that sub-step starts at its list maintenance.
 template <class T, int D>
 __global__ void __launch_bounds__(kSweepThreads, SPH_MOM_MINB)
-k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor)
+k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor, GridP<T> g,
+      int fuse, T full)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long csum = 0;
+    T dnew = T(0);
     if (i < E.nf) {
         const int acnt = E.acount[i];
         if (acnt < 0) {
@@ -519,12 +701,25 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor)
                 V4.x = RN<T>::add(V4.x, RN<T>::mul(half, A4.x));
                 V4.y = RN<T>::add(V4.y, RN<T>::mul(half, A4.y));
                 if (D == 3) V4.z = RN<T>::add(V4.z, RN<T>::mul(half, A4.z));
+                if (fuse) {
+                    vec4<T> P4 = pos[i];
+                    const T xo[3] = {P4.x, P4.y, P4.z};
+                    kick_drift_one<T, D>(P4, V4, A4, half, full);
+                    V4.w = RN<T>::div(P4.w, rho_i);   // rho after this sub-step's DU
+                    E.pos_next[i] = P4;
+                    const T xn[3] = {P4.x, P4.y, P4.z};
+                    dnew = drift_bookkeeping<T, D>(E, g, i, xo, xn);
+                }
                 E.vel[cv ^ 1][i] = V4;
             }
             if (is_owned(E, i)) csum = (unsigned long long)acnt * (unsigned long long)count_factor;
         }
     }
     add_interactions(E.stats, csum);
+    if (fuse) {
+        const unsigned long long b = warp_max_u64(dbits(double(dnew)));
+        if (lane_id() == 0 && b) atomicMax(&E.stats->dmax_bits, b);
+    }
 }
 
 // physics.py:220-247 SHEPARD + :277-280 COPY_SCALAR + :268-274
@@ -601,17 +796,14 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
     EngAcc<T> acc = acc_of_engine<T>(e);
     Eng<T> E = eng_of<T>(e);
     const T cs2 = skin_cs2<T>(e);
-    auto blocks = [](int64_t cnt) {
-        const int64_t want = (cnt + kNlWarps - 1) / kNlWarps;
-        return (unsigned)(want < 148 * 32 ? want : 148 * 32);
-    };
-    if (e->nf > 0)
-        note_launch(), k_skin_build<T, D><<<blocks(e->nf), kNlThreads, 0, s>>>(
-            acc, g, cs2, 0, e->nf, 0, 3u, E);
-    const int64_t nw = e->n - e->nf;
-    if (nw > 0)
-        note_launch(), k_skin_build<T, D><<<blocks(nw), kNlThreads, 0, s>>>(
-            acc, g, cs2, e->nf, nw, E.nf_pad, 1u, E);
+    if (e->n > 0) {
+        constexpr int NT = SkinTile<T, D>::kThreads;
+        const int64_t want = e->ncells;
+        const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
+        cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
+        note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, e->ncells);
+        note_launch(), k_skin_big<T, D><<<148 * 2, kNlThreads, 0, s>>>(acc, g, cs2, E);
+    }
     e->lists_ready = 1;
     return check_launch("engine_build_lists");
 }
@@ -679,7 +871,7 @@ static void init_wall(SphEngine* e, cudaStream_t s)
     if (nw > 0)
         note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
             eng_of<T>(e), make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_rp, 0,
-            1, 0);
+            1, 0, -1);
 }
 
 template <class T, int D>
@@ -690,7 +882,8 @@ static void init_momentum(SphEngine* e, cudaStream_t s)
     if (e->nf > 0) {
         note_launch(), k_rq_fill<T><<<grid_for(e->nf, 256), 256, 0, s>>>(E, e->cur_rp, e->nf);
         note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, make_phys<T>(phys_of_engine(e)), e->cur_v, e->cur_rp, 0, T(0), 1);
+            E, make_phys<T>(phys_of_engine(e)), e->cur_v, e->cur_rp, 0, T(0), 1,
+            grid_of_engine<T>(e), 0, T(0));
     }
     // momentum writes dvdt = 0 for walls (physics.py:128-131)
     if (nw > 0)
@@ -763,33 +956,40 @@ static void sub_wall(SphEngine* e, cudaStream_t s)
     if (nw > 0)
         note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
             eng_of<T>(e), make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_rp ^ 1,
-            1, 1, 1);
+            1, 1, 1, e->cur_v ^ 1);
 }
 
 template <class T, int D>
-static void sub_momentum(SphEngine* e, T half, cudaStream_t s)
+static void sub_momentum(SphEngine* e, T half, T next_full, bool fuse, cudaStream_t s)
 {
     Eng<T> E = eng_of<T>(e);
     const int cv = e->cur_v;
+    fuse = fuse && e->nf > 0;
     if (e->nf > 0)
         note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, make_phys<T>(phys_of_engine(e)), cv, e->cur_rp ^ 1, 1, half, 2);
+            E, make_phys<T>(phys_of_engine(e)), cv, e->cur_rp ^ 1, 1, half, 2,
+            grid_of_engine<T>(e), fuse ? 1 : 0, next_full);
     else if (e->n > 0)
         cudaMemcpyAsync(E.vel[cv ^ 1], E.vel[cv], sizeof(vec4<T>) * (size_t)e->n,
                         cudaMemcpyDeviceToDevice, s);
     e->cur_v = cv ^ 1;
     e->cur_rp ^= 1;
+    if (fuse) {
+        e->cur_pos ^= 1;
+        e->drifted = 1;
+    }
 }
 
-// ev (optional, 6 events) brackets: kick+drift | list filter + fix-ups |
-// continuity+DU | wall pressure | momentum+kick (bench.py per-kernel timing)
+// One sub-step; fuse: its momentum sweep also applies the next sub-step's
+// kick + drift.  ev (optional, 6 events) brackets: kick+drift | list filter
+// + fix-ups | continuity+DU | wall pressure | momentum+kick (bench.py timing)
 template <class T, int D>
-static int substep_impl(SphEngine* e, double half_d, double full_d, cudaEvent_t* ev,
-                        cudaStream_t s)
+static void substep_parts(SphEngine* e, T half, T full, bool fuse, cudaEvent_t* ev,
+                          cudaStream_t s)
 {
-    const T half = T(half_d), full = T(full_d);
     if (ev) cudaEventRecord(ev[0], s);
-    sub_kick_drift<T, D>(e, half, full, s);
+    if (!e->drifted) sub_kick_drift<T, D>(e, half, full, s);
+    e->drifted = 0;
     if (ev) cudaEventRecord(ev[1], s);
     mark_and_fix<T, D>(e, s);
     if (ev) cudaEventRecord(ev[2], s);
@@ -797,8 +997,15 @@ static int substep_impl(SphEngine* e, double half_d, double full_d, cudaEvent_t*
     if (ev) cudaEventRecord(ev[3], s);
     sub_wall<T, D>(e, s);
     if (ev) cudaEventRecord(ev[4], s);
-    sub_momentum<T, D>(e, half, s);
+    sub_momentum<T, D>(e, half, full, fuse, s);
     if (ev) cudaEventRecord(ev[5], s);
+}
+
+template <class T, int D>
+static int substep_impl(SphEngine* e, double half_d, double full_d, cudaEvent_t* ev,
+                        cudaStream_t s)
+{
+    substep_parts<T, D>(e, T(half_d), T(full_d), false, ev, s);
     return check_launch("engine_substep");
 }
 
@@ -825,6 +1032,51 @@ extern "C" int sph_engine_substep_timed(SphEngine* e, double half_dt, double ful
     return rc ? rc : check_launch("engine_substep_timed");
 }
 
+// physics.py:522-548 for the nsub sub-steps of one advective step
+template <class T, int D>
+static int substeps_impl(SphEngine* e, double half_d, double full_d, int nsub, float* ms,
+                         cudaStream_t s)
+{
+    const T half = T(half_d), full = T(full_d);
+    cudaEvent_t ev[6];
+    if (ms) {
+        for (int k = 0; k < 6; k++) cudaEventCreate(&ev[k]);
+        for (int k = 0; k < 5; k++) ms[k] = 0.0f;
+    }
+    for (int k = 0; k < nsub; k++) {
+        substep_parts<T, D>(e, half, full, k + 1 < nsub, ms ? ev : nullptr, s);
+        if (ms) {
+            cudaEventSynchronize(ev[5]);
+            for (int q = 0; q < 5; q++) {
+                float t = 0.0f;
+                cudaEventElapsedTime(&t, ev[q], ev[q + 1]);
+                ms[q] += t;
+            }
+        }
+    }
+    if (ms)
+        for (int k = 0; k < 6; k++) cudaEventDestroy(ev[k]);
+    return check_launch("engine_substeps");
+}
+
+extern "C" int sph_engine_substeps(SphEngine* e, double half_dt, double full_dt, int32_t nsub,
+                                   cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc || (rc = require_lists(e))) return rc;
+    if (nsub < 0 || e->drifted) return SPH_ERR_INVALID;
+    return SPH_DISPATCH(e, substeps_impl, e, half_dt, full_dt, (int)nsub, (float*)nullptr, s);
+}
+
+extern "C" int sph_engine_substeps_timed(SphEngine* e, double half_dt, double full_dt,
+                                         int32_t nsub, float* ms_out, cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc || (rc = require_lists(e))) return rc;
+    if (nsub < 0 || e->drifted) return SPH_ERR_INVALID;
+    return SPH_DISPATCH(e, substeps_impl, e, half_dt, full_dt, (int)nsub, ms_out, s);
+}
+
 template <class T, int D>
 static int phase_impl(SphEngine* e, int phase, double half_d, double full_d, cudaStream_t s)
 {
@@ -836,7 +1088,7 @@ static int phase_impl(SphEngine* e, int phase, double half_d, double full_d, cud
         sub_continuity<T, D>(e, full, s);
         break;
     case SPH_PHASE_WALL: sub_wall<T, D>(e, s); break;
-    case SPH_PHASE_MOMENTUM: sub_momentum<T, D>(e, half, s); break;
+    case SPH_PHASE_MOMENTUM: sub_momentum<T, D>(e, half, T(0), false, s); break;
     case SPH_PHASE_INIT_WALL: init_wall<T, D>(e, s); break;
     case SPH_PHASE_INIT_MOMENTUM: init_momentum<T, D>(e, s); break;
     default: set_error("engine_phase: unknown phase"); return SPH_ERR_INVALID;

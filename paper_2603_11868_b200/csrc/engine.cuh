@@ -29,7 +29,9 @@ constexpr uint32_t kInvalidCell = 0xffffffffu;   // list is not a valid skin lis
 template <class T>
 struct Eng {
     int64_t n, nf, nw, nf_pad;
-    vec4<T>* pos; vec4<T>* vel[2]; vec2<T>* rp[2]; vec2<T>* rq; vec4<T>* dvdt; T* drho;
+    vec4<T>* pos;        // the current position buffer
+    vec4<T>* pos_next;   // the other one (fused kick+drift writes it)
+    vec4<T>* vel[2]; vec2<T>* rp[2]; vec2<T>* rq; vec4<T>* dvdt; T* drho;
     uint32_t* id; uint32_t* nnb; uint32_t* refpos;
     T* rho_scratch_id; uint32_t* oflow_id; uint32_t* wall_id; T* vol_id;
     const uint8_t* owned_id;
@@ -44,7 +46,8 @@ inline Eng<T> eng_of(const SphEngine* e)
 {
     Eng<T> g;
     g.n = e->n; g.nf = e->nf; g.nw = e->n - e->nf; g.nf_pad = (e->nf + 31) / 32 * 32;
-    g.pos = (vec4<T>*)e->pos;
+    g.pos = (vec4<T>*)e->pos[e->cur_pos];
+    g.pos_next = (vec4<T>*)e->pos[e->cur_pos ^ 1];
     g.vel[0] = (vec4<T>*)e->vel[0]; g.vel[1] = (vec4<T>*)e->vel[1];
     g.rp[0] = (vec2<T>*)e->rp[0]; g.rp[1] = (vec2<T>*)e->rp[1];
     g.rq = (vec2<T>*)e->rq;
@@ -87,7 +90,7 @@ template <class T>
 inline EngAcc<T> acc_of_engine(const SphEngine* e)
 {
     EngAcc<T> acc;
-    acc.pos = (const vec4<T>*)e->pos;
+    acc.pos = (const vec4<T>*)e->pos[e->cur_pos];
     acc.id = e->id;
     acc.offs_f = e->offs_f;
     acc.offs_w = e->offs_w;

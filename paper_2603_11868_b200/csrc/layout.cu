@@ -51,7 +51,7 @@ __global__ void k_push_gather(Eng<T> E, const uint32_t* __restrict__ perm, const
     A4.x = dvdt[r * D]; A4.y = dvdt[r * D + 1]; A4.z = D == 3 ? dvdt[r * D + 2] : T(0);
     A4.w = T(0);
     vec2<T> RP; RP.x = rho[r]; RP.y = p[r];
-    E.pos[i] = P4;
+    E.pos[i] = P4; E.pos_next[i] = P4;   // walls stay valid in both buffers
     E.vel[0][i] = V4; E.vel[1][i] = V4;
     E.rp[0][i] = RP; E.rp[1][i] = RP;
     E.dvdt[i] = A4;
@@ -322,6 +322,8 @@ static int push_impl(SphEngine* e, const void* x, const void* v, const void* rho
     }
     e->cur_v = 0;
     e->cur_rp = 0;
+    e->cur_pos = 0;
+    e->drifted = 0;
     e->lists_ready = 0;
     return check_launch("engine_push");
 }
@@ -393,7 +395,7 @@ static int rebuild_impl(SphEngine* e, cudaStream_t s)
     // the gathered fluid prefix goes back into the primary arrays; the wall
     // suffix there is untouched (walls never move)
     const size_t es = sizeof(T);
-    cudaMemcpyAsync(e->pos, pos_o, 4 * es * (size_t)nf, cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(e->pos[e->cur_pos], pos_o, 4 * es * (size_t)nf, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(e->dvdt, dvdt_o, 4 * es * (size_t)nf, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(e->drho, drho_o, es * (size_t)nf, cudaMemcpyDeviceToDevice, s);
     cudaMemcpyAsync(e->id, id_o, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, s);

@@ -420,7 +420,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
     n = max(int(n_cap), 1)
     tiles = max((nf_cap + 31) // 32 + (nw_cap + 31) // 32, 1)
     T = {}
-    for k in ("pos", "vel0", "vel1", "dvdt"):
+    for k in ("pos0", "pos1", "vel0", "vel1", "dvdt"):
         T[k] = torch.empty((n, 4), dtype=tdt, device=dev)
     for k in ("rp0", "rp1", "rq"):
         T[k] = torch.empty((n, 2), dtype=tdt, device=dev)
@@ -443,7 +443,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
     E = _native.SphEngine()
     E.ncells, E.dim = ncells, d
     E.key_bits = max(1, int(ncells - 1).bit_length())
-    E.pos = T["pos"].data_ptr()
+    E.pos[0], E.pos[1] = T["pos0"].data_ptr(), T["pos1"].data_ptr()
     E.vel[0], E.vel[1] = T["vel0"].data_ptr(), T["vel1"].data_ptr()
     E.rp[0], E.rp[1] = T["rp0"].data_ptr(), T["rp1"].data_ptr()
     E.rq = T["rq"].data_ptr()
@@ -561,8 +561,8 @@ class Simulation:
                             force_scalars(reg, self.grid), reg.singular("g"))
         engine_set_counts(E, n, nf)
         torch = torch_mod()
-        self._dev = {"device": T["pos"].device, "E": E, "T": T, "tdtype": T["pos"].dtype,
-                     "stream": stream_ptr(T["pos"].device),
+        self._dev = {"device": T["pos0"].device, "E": E, "T": T, "tdtype": T["pos0"].dtype,
+                     "stream": stream_ptr(T["pos0"].device),
                      "stats_host": torch.empty(T["stats"].shape, dtype=torch.uint8,
                                                pin_memory=True)}
 
@@ -712,17 +712,14 @@ class Simulation:
         t0 = time.perf_counter()
         E = ctypes.byref(d["E"])
         if self.kernel_times is None:
-            for _ in range(nsub):
-                rc = L.sph_engine_substep(E, half, full, d["stream"])
-                if rc:
-                    _native.check(rc, "engine_substep")
+            rc = L.sph_engine_substeps(E, half, full, nsub, d["stream"])
+            _native.check(rc, "engine_substeps")
         else:   # per-kernel CUDA-event timing (bench.py roofline pass)
             ms = (ctypes.c_float * 5)()
-            for _ in range(nsub):
-                rc = L.sph_engine_substep_timed(E, half, full, ms, d["stream"])
-                _native.check(rc, "engine_substep_timed")
-                for k, name in enumerate(SUBSTEP_KERNELS):
-                    self.kernel_times.setdefault(name, []).append(ms[k])
+            rc = L.sph_engine_substeps_timed(E, half, full, nsub, ms, d["stream"])
+            _native.check(rc, "engine_substeps_timed")
+            for k, name in enumerate(SUBSTEP_KERNELS):   # per sub-step average
+                self.kernel_times.setdefault(name, []).append(ms[k] / nsub)
         self._call("sph_engine_stats", ctypes.c_int32(_native.STATS_NORMS))
         stats = self._read_stats()
         self.phase_seconds["interactions"] += time.perf_counter() - t0

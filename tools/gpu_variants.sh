@@ -1,6 +1,7 @@
 # build-variant sweep on the GPU box: tests with the in-tree library, then
 # short benches of the in-tree library and each build/variants/<tag>/ library
 set -x
+shopt -s nullglob
 cd $GRAFT_REPO_ROOT
 timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/v_tests.log 2>&1; echo tests=$?
 for c in ${CONFIGS:-2d1m 3d4m}; do
