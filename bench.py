@@ -70,16 +70,16 @@ def kernel_bytes(name, d, nf, nw, nnb_f, nnb_w, nnb_wf):
     """Compulsory DRAM bytes of one launch: each field the kernel must read
     once, each field it must write once (fp32 run, uint32 index); gathered
     neighbour data is assumed cache-resident (SURVEY.md section 8d model)."""
-    if name == "kick_drift":       # read x v a, write x v
+    if name == "kick_drift":       # read x v a, write x v (first sub-step only)
         return nf * 20 * d
-    if name == "list_filter":      # read x, cell0, disp, counts, list; write mask, count
-        return (nf + nw) * (4 * d + 4 + 4 + 4 + 4 + 4 + 4) + 4 * (nnb_f + nnb_wf)
+    if name == "list_filter":      # k_mark: read cell0, disp (fix-ups extra)
+        return (nf + nw) * 8
     if name == "continuity_du":    # read x v rho m + list, write drho rho p
         return nf * (8 * d + 8 + 4 + 12) + 4 * nnb_f
     if name == "wall_pressure":    # read x + list, write rho p nnb drho
         return nw * (4 * d + 4 + 16) + 4 * nnb_wf
-    if name == "momentum_kick":    # read x v rho p m + list, write dvdt v nnb
-        return nf * (8 * d + 12 + 4 + 8 * d + 4) + 4 * nnb_f
+    if name == "momentum_kick":    # read x v rho p m + list, write dvdt v x (SURVEY 8d)
+        return nf * (20 * d + 20) + 4 * nnb_f
     raise KeyError(name)
 
 
@@ -266,11 +266,15 @@ def gpu_arm(args, rank, world, local_rank):
     peaks, peak_src = measured_peaks()
     bytes_dom = kernel_bytes(dominant, d, nf, nw, nnb_f, 0, nnb_wf)
     achieved = bytes_dom / kt[dominant] / 1e9
-    traffic = None
+    traffic, issue = None, None
     prof_json = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof_json):
         with open(prof_json) as fh:
-            traffic = json.load(fh).get(args.config, {}).get(dominant)
+            ent = json.load(fh).get(args.config, {}).get(dominant)
+        if isinstance(ent, dict):
+            traffic = ent.get("dram_bytes")
+            issue = ent.get("issue_active_pct")
+            issue = issue / 100.0 if issue is not None else None
 
     # end-to-end through the public API with host (pinned) buffers
     e2e = None
@@ -306,6 +310,7 @@ def gpu_arm(args, rank, world, local_rank):
             "bound": "hbm", "kernel": dominant, "achieved": achieved,
             "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+            "issue_active_frac": issue,
             "peak_source": peak_src,
             "algorithmic_bytes_per_launch": bytes_dom,
             "launch_ms": 1e3 * kt[dominant],
@@ -313,8 +318,10 @@ def gpu_arm(args, rank, world, local_rank):
             "profiled_step_ms": 1e3 * prof_step_s,
             "step_model_bytes_per_update": b_full,
             "step_model_frac": value / world * b_full / (peaks["hbm_gbs"] * 1e9),
-            "note": "sweeps are FP64/issue bound in bit-exact mode (SURVEY 8d); "
-                    "see profiles/ for ncu pipe utilisation"},
+            "note": "the sweeps are instruction-issue bound in bit-exact mode "
+                    "(SURVEY 8d): issue_active_frac (ncu smsp__issue_active, "
+                    "profiles/ncu_traffic.json) is their binding roof; traffic = "
+                    "ncu dram bytes per launch"},
         "cpu_baseline": cpu,
         "e2e": e2e,
     }

@@ -34,6 +34,9 @@
 #ifndef SPH_MOM_MINB
 #define SPH_MOM_MINB 8       // the momentum sweep holds more live state
 #endif
+#ifndef SPH_MOM_WALK
+#define SPH_MOM_WALK sweep_list   // sweep_list_pf (one pair ahead) measured slower
+#endif
 #ifndef SPH_FILTER_KF
 #define SPH_FILTER_KF 4      // list entries in flight per filter trip
 #endif
@@ -62,6 +65,43 @@ __device__ __forceinline__ void sweep_list(const Eng<T>& E, int64_t slot, int cn
         if (t0 + 1 < cnt) body(t0 + 1, load(q.y));
         if (t0 + 2 < cnt) body(t0 + 2, load(q.z));
         if (t0 + 3 < cnt) body(t0 + 3, load(q.w));
+    }
+}
+
+// The same walk software-pipelined by one neighbour: the next neighbour's
+// data is requested before the current pair is computed (more registers,
+// more independent work in flight per warp).
+template <class T, class Load, class Body>
+__device__ __forceinline__ void sweep_list_pf(const Eng<T>& E, int64_t slot, int cnt, Load load,
+                                              Body body)
+{
+    if (cnt <= 0) return;
+    const int4* __restrict__ q4 = reinterpret_cast<const int4*>(E.elist + ell_base(slot));
+    int4 q = q4[0];
+    auto cur = load(q.x);
+    for (int t0 = 0; t0 < cnt; t0 += 4) {
+        const int4 qn = (t0 + 4 < cnt) ? q4[((t0 >> 2) + 1) * 32] : q;
+        {
+            const auto nx = load(t0 + 1 < cnt ? q.y : q.x);
+            body(t0, cur);
+            cur = nx;
+        }
+        if (t0 + 1 < cnt) {
+            const auto nx = load(t0 + 2 < cnt ? q.z : q.x);
+            body(t0 + 1, cur);
+            cur = nx;
+        }
+        if (t0 + 2 < cnt) {
+            const auto nx = load(t0 + 3 < cnt ? q.w : q.x);
+            body(t0 + 2, cur);
+            cur = nx;
+        }
+        if (t0 + 3 < cnt) {
+            const auto nx = load(t0 + 4 < cnt ? qn.x : q.x);
+            body(t0 + 3, cur);
+            cur = nx;
+        }
+        q = qn;
     }
 }
 
@@ -685,7 +725,7 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
             const T pi_rr = RQI.y;
             T a[3] = {P.g[0], P.g[1], P.g[2]};
             auto loadf = [&](int j) { return NbrPVR<T>{pos[j], vel[j], rq[j]}; };
-            sweep_list<T>(E, i, acnt, loadf, [&](int, const NbrPVR<T>& nb) {
+            SPH_MOM_WALK<T>(E, i, acnt, loadf, [&](int, const NbrPVR<T>& nb) {
                 T xj[3], vj[3], dx[3], r2, vx;
                 to3<T>(nb.p, xj);
                 to3<T>(nb.v, vj);

@@ -1,6 +1,7 @@
-"""Per-launch DRAM traffic of the engine's sub-step kernels from `ncu --set
-full` captures -> profiles/ncu_traffic.json (read by bench.py's roofline
-`traffic` field).
+"""Per-launch DRAM traffic, issue-slot utilisation and instruction count of
+the engine's kernels from `ncu --set full` captures ->
+profiles/ncu_traffic.json (read by bench.py's roofline `traffic` and
+`issue_active_frac` fields).
 
 usage: python tools/ncu_traffic.py OUT.json CONFIG=REP.ncu-rep [CONFIG=REP ...]
 """
@@ -35,8 +36,16 @@ def traffic(path):
             continue
         b = (_val(r, hdr, units, "dram__bytes_read.sum")
              + _val(r, hdr, units, "dram__bytes_write.sum"))
-        acc.setdefault(NAMES[base], []).append(b)
-    return {k: sum(v) / len(v) for k, v in acc.items()}
+        issue = _val(r, hdr, units, "smsp__issue_active.avg.pct_of_peak_sustained_active")
+        inst = _val(r, hdr, units, "smsp__inst_executed.sum")
+        acc.setdefault(NAMES[base], []).append((b, issue, inst))
+    out = {}
+    for k, v in acc.items():
+        m = len(v)
+        out[k] = {"dram_bytes": sum(x[0] for x in v) / m,
+                  "issue_active_pct": sum(x[1] for x in v) / m,
+                  "warp_inst": sum(x[2] for x in v) / m, "launches": m}
+    return out
 
 
 def main(out, specs):
