@@ -34,6 +34,9 @@
 #ifndef SPH_MOM_MINB
 #define SPH_MOM_MINB 8       // the momentum sweep holds more live state
 #endif
+#ifndef SPH_SKIN_THREADS_PER_SM
+#define SPH_SKIN_THREADS_PER_SM 1536   // skin-list build occupancy (register cap)
+#endif
 #ifndef SPH_MOM_WALK
 #define SPH_MOM_WALK sweep_list   // sweep_list_pf (one pair ahead) measured slower
 #endif
@@ -214,17 +217,79 @@ template <> struct SkinTile<float, 3> { static constexpr int kThreads = 256, kCa
 template <> struct SkinTile<double, 2> { static constexpr int kThreads = 128, kCands = 256; };
 template <> struct SkinTile<double, 3> { static constexpr int kThreads = 256, kCands = 512; };
 
+// Ascending bitonic sort of the P (power of two, >= 64) keys in shared
+// memory: stages whose partner distance is < 64 run in registers on 64-key
+// chunks (2 per lane, shuffles), the wider ones as shared-memory passes.
+template <class K>
+__device__ __forceinline__ void chunk_bitonic(K (&v)[2], int base, int k, int jtop, unsigned lane)
+{
+    for (int j = jtop; j > 0; j >>= 1) {
+        if (j >= 2) {
+#pragma unroll
+            for (int r = 0; r < 2; r++) {
+                const K o = __shfl_xor_sync(0xffffffffu, v[r], j >> 1);
+                const int e = base + 2 * (int)lane + r;
+                const bool up = (e & k) == 0, lower = (e & j) == 0;
+                // keep the smaller iff lower == up
+                v[r] = ((o < v[r]) == (lower == up)) ? o : v[r];
+            }
+        } else {
+            const int e = base + 2 * (int)lane;
+            const bool up = (e & k) == 0;
+            const K x0 = v[0], x1 = v[1];
+            const bool sw = (x0 > x1) == up;
+            v[0] = sw ? x1 : x0;
+            v[1] = sw ? x0 : x1;
+        }
+    }
+}
+
+template <int NT, class K>
+__device__ __forceinline__ void block_bitonic(K* key, int P)
+{
+    constexpr int NW = NT / 32;
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    for (int c = warp; c < (P >> 6); c += NW) {   // chunks of 64: k = 2 .. 64
+        const int base = c << 6;
+        K v[2] = {key[base + 2 * lane], key[base + 2 * lane + 1]};
+        for (int k = 2; k <= 64; k <<= 1) chunk_bitonic(v, base, k, k >> 1, lane);
+        key[base + 2 * lane] = v[0];
+        key[base + 2 * lane + 1] = v[1];
+    }
+    __syncthreads();
+    for (int k = 128; k <= P; k <<= 1) {
+        for (int j = k >> 1; j >= 64; j >>= 1) {
+            for (int q = threadIdx.x; q < (P >> 1); q += NT) {
+                const int lo = ((q & ~(j - 1)) << 1) | (q & (j - 1)), hi = lo + j;
+                const K x0 = key[lo], x1 = key[hi];
+                if ((x0 > x1) == ((lo & k) == 0)) { key[lo] = x1; key[hi] = x0; }
+            }
+            __syncthreads();
+        }
+        for (int c = warp; c < (P >> 6); c += NW) {
+            const int base = c << 6;
+            K v[2] = {key[base + 2 * lane], key[base + 2 * lane + 1]};
+            chunk_bitonic(v, base, k, 32, lane);
+            key[base + 2 * lane] = v[0];
+            key[base + 2 * lane + 1] = v[1];
+        }
+        __syncthreads();
+    }
+}
+
 template <class T, int D>
-__global__ void __launch_bounds__(SkinTile<T, D>::kThreads, 2048 / SkinTile<T, D>::kThreads)
-k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E, int64_t ncells)
+__global__ void __launch_bounds__(SkinTile<T, D>::kThreads, SPH_SKIN_THREADS_PER_SM / SkinTile<T, D>::kThreads)
+k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E, int64_t ncells,
+            const uint32_t* __restrict__ phys_of_id)
 {
     constexpr int NT = SkinTile<T, D>::kThreads, NW = NT / 32, kC = SkinTile<T, D>::kCands;
-    __shared__ unsigned long long skey[kC];
-    __shared__ vec4<T> spos[kC];
+    __shared__ uint32_t sj[kC];        // candidate ids, sorted; then their indices j
+    __shared__ vec4<T> spos[kC];       // positions in sorted order
     __shared__ uint32_t run_start[2 * 9], run_pre[2 * 9 + 1];
     const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const unsigned lt = lanemask_lt();
     const int64_t nf = E.nf;
+    const T inf = T(INFINITY);
     for (int64_t c = blockIdx.x; c < ncells; c += gridDim.x) {
         const uint32_t f0 = E.offs_f[c], f1 = E.offs_f[c + 1];
         const uint32_t w0 = E.offs_w[c], w1 = E.offs_w[c + 1];
@@ -278,77 +343,108 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E, int64_t ncel
         }
         __syncthreads();
         const int M = (int)run_pre[nruns];
-        if (M <= kC) {
-            int P = 32;
-            while (P < M) P <<= 1;
-            for (int k = tid; k < P; k += NT) {
-                unsigned long long key = ~0ull;
-                if (k < M) {
-                    int r = 0;
-                    while (r + 1 < nruns && run_pre[r + 1] <= (uint32_t)k) r++;
-                    const uint32_t j = run_start[r] + ((uint32_t)k - run_pre[r]);
-                    key = ((unsigned long long)E.id[j] << 32) | j;
-                }
-                skey[k] = key;
-            }
+        if (M > kC) {   // oversized block: per-particle path (k_skin_big)
+            if (tid == 0) E.queue[atomicAdd(E.qcount, 1u)] = (uint32_t)c;
             __syncthreads();
-            for (int k = 2; k <= P; k <<= 1) {          // ascending bitonic by id
-                for (int j = k >> 1; j > 0; j >>= 1) {
-                    for (int q = tid; q < (P >> 1); q += NT) {
-                        const int lo = ((q & ~(j - 1)) << 1) | (q & (j - 1)), hi = lo + j;
-                        const unsigned long long x0 = skey[lo], x1 = skey[hi];
-                        if ((x0 > x1) == ((lo & k) == 0)) { skey[lo] = x1; skey[hi] = x0; }
-                    }
-                    __syncthreads();
+            continue;
+        }
+        int P = 64;
+        while (P < M) P <<= 1;
+        for (int k = tid; k < P; k += NT) {
+            uint32_t key = 0xffffffffu;
+            if (k < M) {
+                int r = 0;
+                while (r + 1 < nruns && run_pre[r + 1] <= (uint32_t)k) r++;
+                key = E.id[run_start[r] + ((uint32_t)k - run_pre[r])];
+            }
+            sj[k] = key;
+        }
+        __syncthreads();
+        block_bitonic<NT>(sj, P);   // ids are unique: a total order
+        const int Mp = (M + 31) & ~31;
+        for (int k = tid; k < Mp; k += NT) {
+            vec4<T> p;
+            if (k < M) {
+                const uint32_t j = phys_of_id[sj[k]];
+                sj[k] = j;
+                p = E.pos[j];
+            } else {   // padding: never within reach
+                p.x = inf; p.y = inf; p.z = inf; p.w = T(0);
+                sj[k] = 0;
+            }
+            spos[k] = p;
+        }
+        __syncthreads();
+        // two particles of the cell per warp pass: each candidate's shared
+        // data is read once for both
+        for (int t = 2 * warp; t < nt; t += 2 * NW) {
+            const bool hasB = t + 1 < nt;
+            const bool flA = t < ntf, flB = t + 1 < ntf;
+            const int64_t iA = flA ? (int64_t)f0 + t : nf + w0 + (t - ntf);
+            const int64_t iB = hasB ? (flB ? (int64_t)f0 + t + 1 : nf + w0 + (t + 1 - ntf)) : iA;
+            const int64_t slA = flA ? iA : E.nf_pad + (iA - nf);
+            const int64_t slB = flB ? iB : E.nf_pad + (iB - nf);
+            T xa[3], xb[3];
+            to3<T>(E.pos[iA], xa);
+            to3<T>(E.pos[iB], xb);
+            int32_t* __restrict__ lpA = E.lists + ell_base(slA);
+            int32_t* __restrict__ lpB = E.lists + ell_base(slB);
+            int cntA = 0, cntB = 0, naA = 0, naB = 0;
+            for (int base = 0; base < Mp; base += 32) {
+                const int k = base + (int)lane;
+                const uint32_t j = sj[k];
+                T xj[3];
+                to3<T>(spos[k], xj);
+                const T r2a = accept_r2<T, D>(xa, xj);
+                const T r2b = accept_r2<T, D>(xb, xj);
+                const bool jf = (int64_t)j < nf;
+                const bool stA = (flA || jf) && r2a < cs2 && j != (uint32_t)iA;
+                const bool stB = hasB && (flB || jf) && r2b < cs2 && j != (uint32_t)iB;
+                const unsigned bA = __ballot_sync(0xffffffffu, stA);
+                const unsigned bB = __ballot_sync(0xffffffffu, stB);
+                if (stA) {
+                    const int p = cntA + __popc(bA & lt);
+                    if (p < kCap) lpA[ell_off(p)] = (int32_t)j;
+                }
+                if (stB) {
+                    const int p = cntB + __popc(bB & lt);
+                    if (p < kCap) lpB[ell_off(p)] = (int32_t)j;
+                }
+                cntA += __popc(bA);
+                cntB += __popc(bB);
+                if (!flA || !flB) {   // walls: static exact wall-wall count
+                    const bool ctA = !flA && !jf && r2a < g.c2 && r2a > T(0) && j != (uint32_t)iA;
+                    const bool ctB = hasB && !flB && !jf && r2b < g.c2 && r2b > T(0) &&
+                                     j != (uint32_t)iB;
+                    naA += __popc(__ballot_sync(0xffffffffu, ctA));
+                    naB += __popc(__ballot_sync(0xffffffffu, ctB));
                 }
             }
-            for (int k = tid; k < M; k += NT) spos[k] = E.pos[(uint32_t)skey[k]];
-            __syncthreads();
-            for (int t = warp; t < nt; t += NW) {
-                const bool fluid = t < ntf;
-                const int64_t i = fluid ? (int64_t)f0 + t : nf + w0 + (t - ntf);
-                const int64_t slot = fluid ? i : E.nf_pad + (i - nf);
+            if (lane < 2 && (lane == 0 || hasB)) {
+                const int64_t i = lane ? iB : iA;
+                const int64_t slot = lane ? slB : slA;
+                const int cnt = lane ? cntB : cntA;
                 T xi[3];
-                to3<T>(E.pos[i], xi);
+                xi[0] = lane ? xb[0] : xa[0];
+                xi[1] = lane ? xb[1] : xa[1];
+                xi[2] = lane ? xb[2] : xa[2];
                 int cxyz[3];
-                const bool in_cell = cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c;
-                int cnt = 0, nacc = 0;
-                for (int base = 0; base < M; base += 32) {
-                    const int k = base + (int)lane;
-                    bool st = false, ct = false;
-                    uint32_t j = 0;
-                    if (k < M) {
-                        j = (uint32_t)skey[k];
-                        T xj[3];
-                        to3<T>(spos[k], xj);
-                        const T r2 = accept_r2<T, D>(xi, xj);
-                        const bool stores = fluid || (int64_t)j < nf;
-                        if ((int64_t)j != i) {
-                            st = stores && (r2 < cs2);
-                            ct = !stores && (r2 < g.c2) && (r2 > T(0));
-                        }
-                    }
-                    const unsigned bs = __ballot_sync(0xffffffffu, st);
-                    if (st) {
-                        const int p = cnt + __popc(bs & lt);
-                        if (p < kCap) E.lists[ell_index(slot, p)] = (int32_t)j;
-                    }
-                    cnt += __popc(bs);
-                    nacc += __popc(__ballot_sync(0xffffffffu, ct));
-                }
-                if (lane == 0) {
-                    const bool ok = in_cell && cnt <= kCap;
-                    E.cell0[i] = ok ? (uint32_t)c : kInvalidCell;
-                    E.lcount[slot] = ok ? cnt : 0;
-                    E.nww[slot] = nacc;   // walls: static wall-wall count
-                    E.disp[i] = T(0);
-                }
+                const bool ok = cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c && cnt <= kCap;
+                E.cell0[i] = ok ? (uint32_t)c : kInvalidCell;
+                E.lcount[slot] = ok ? cnt : 0;
+                E.nww[slot] = lane ? naB : naA;
+                E.disp[i] = T(0);
             }
-        } else if (tid == 0) {   // oversized block: per-particle path (k_skin_big)
-            E.queue[atomicAdd(E.qcount, 1u)] = (uint32_t)c;
         }
         __syncthreads();   // shared tile reused by the next cell
     }
+}
+
+__global__ void __launch_bounds__(256)
+k_phys_of_id(const uint32_t* __restrict__ id, int64_t n, uint32_t* __restrict__ phys_of_id)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) phys_of_id[id[i]] = (uint32_t)i;
 }
 
 // skin lists of the cells k_skin_tile queued (candidate block above the
@@ -841,7 +937,13 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
         const int64_t want = e->ncells;
         const unsigned blocks = (unsigned)(want < 148 * 16 ? want : 148 * 16);
         cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
-        note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, e->ncells);
+        // physical index of every id (workspace scratch, free between rebuilds)
+        Bump bump(e->ws, e->ws_bytes);
+        uint32_t* phys_of_id = bump.take<uint32_t>(e->n);
+        if (!phys_of_id) return SPH_ERR_WORKSPACE;
+        note_launch(), k_phys_of_id<<<grid_for(e->n, 256), 256, 0, s>>>(e->id, e->n, phys_of_id);
+        note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, e->ncells,
+                                                              phys_of_id);
         note_launch(), k_skin_big<T, D><<<148 * 2, kNlThreads, 0, s>>>(acc, g, cs2, E);
     }
     e->lists_ready = 1;
