@@ -150,16 +150,22 @@ class ClockSampler:
 
 # -- CPU arms -------------------------------------------------------------------
 
-def cpu_oracle_run(name, steps, budget_s):
+def cpu_oracle_run(name, steps, budget_s, warmup=0):
     """Time the oracle port (all host threads) on the same configuration:
-    initialize() untimed, then up to ``steps`` advective steps bounded by
-    ``budget_s`` seconds.  Returns (PU/s, steps_done, seconds, threads)."""
+    initialize() and ``warmup`` steps untimed (bounded by budget_s / 2), then
+    up to ``steps`` advective steps bounded by ``budget_s`` seconds.
+    Returns (PU/s, steps_done, seconds, threads, nsubs)."""
     threads = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     from oracle.oracle import OracleSim
     reg, grid = build_case(name)
     sim = OracleSim.from_registry(reg, grid)
     sim.initialize()
+    t0 = time.perf_counter()
+    for _ in range(warmup):
+        sim.advance()
+        if time.perf_counter() - t0 > budget_s / 2:
+            break
     n = reg.particle_count
     done, total = 0, 0.0
     nsubs = []
@@ -178,10 +184,11 @@ def reference_arm(args, rank, world):
     if rank != 0:
         return
     pus, done, secs, thr, nsubs = cpu_oracle_run(args.config, max(1, args.steps),
-                                                 budget_s=args.cpu_budget)
+                                                 budget_s=args.cpu_budget,
+                                                 warmup=args.warmup)
     line = {
         "impl": "reference", "metric": METRIC, "value": pus, "unit": UNIT,
-        "n_gpus": world, "steps": done, "warmup": 0,
+        "n_gpus": world, "steps": done, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / done, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (mixed f64)",
         "data": "synthetic (reference lattice dam break)",
@@ -189,7 +196,8 @@ def reference_arm(args, rank, world):
         "cpu_baseline": {
             "value": pus, "unit": UNIT, "cores": thr, "kind": "port",
             "sample": f"{done} full advective step(s) (nsub={nsubs}) after an "
-                      f"untimed initialize(), C port of the reference "
+                      f"untimed initialize() + up to {args.warmup} warm-up steps, "
+                      f"C port of the reference "
                       f"(oracle/sph_oracle.c, bit-identical), OpenMP {thr} threads"},
         "e2e": {"value": pus, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
