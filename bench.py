@@ -46,6 +46,20 @@ SUBSTEP_KERNELS = ("kick_drift", "list_filter", "continuity_du", "wall_pressure"
                    "momentum_kick")
 
 
+_OUT_FD = None
+
+
+def emit(line):
+    """The one JSON line on the process's original stdout (NCCL and other
+    libraries may print banners on fd 1; those are diverted to stderr)."""
+    data = (json.dumps(line) + "\n").encode()
+    if _OUT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_OUT_FD, data)
+
+
 def build_case(name):
     from paper_2603_11868_b200 import cases
     spec = CONFIGS[name][1]
@@ -202,7 +216,7 @@ def reference_arm(args, rank, world):
         "e2e": {"value": pus, "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # -- GPU arm --------------------------------------------------------------------
@@ -334,7 +348,7 @@ def gpu_arm(args, rank, world, local_rank):
         "e2e": e2e,
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def slab_arm(args, rank, world, local_rank):
@@ -449,7 +463,7 @@ def slab_arm(args, rank, world, local_rank):
         "e2e": e2e,
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def e2e_run(sim, reg, steps, world, dev):
@@ -497,6 +511,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=60.0)
+    ap.add_argument("--slab", action="store_true",
+                    help="run the slab-decomposition path even on one rank "
+                         "(measures its orchestration overhead)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -505,7 +522,11 @@ def main():
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return
-    if world > 1:
+    if world > 1 or args.slab:
+        global _OUT_FD
+        sys.stdout.flush()
+        _OUT_FD = os.dup(1)
+        os.dup2(2, 1)   # library banners (e.g. "NCCL version") go to stderr
         import torch
         local_rank %= max(1, torch.cuda.device_count())   # ranks sharing a GPU (gloo check)
         torch.cuda.set_device(local_rank)
@@ -513,14 +534,16 @@ def main():
         # NCCL between GPUs; SPH_BENCH_BACKEND=gloo runs the same slab path
         # host-staged (e.g. ranks sharing one GPU to validate it -- not a
         # performance configuration)
+        for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_PORT", "29533")):
+            os.environ.setdefault(k, v)
         torch.distributed.init_process_group(os.environ.get("SPH_BENCH_BACKEND", "nccl"))
     try:
-        if world > 1:
+        if world > 1 or args.slab:
             slab_arm(args, rank, world, local_rank)
         else:
             gpu_arm(args, rank, world, local_rank)
     finally:
-        if world > 1:
+        if world > 1 or args.slab:
             import torch
             torch.distributed.destroy_process_group()
 

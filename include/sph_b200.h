@@ -298,6 +298,45 @@ int sph_engine_pack(const SphEngine* e, int32_t kind, const int32_t* phys, int64
 int sph_engine_unpack(SphEngine* e, int32_t kind, const int32_t* phys, int64_t count,
                       const void* in, cudaStream_t s);
 
+/* Halo plan of one rank for one advective step: per record class (0 = fluid
+ * ghosts, 1 = wall ghosts) the physical indices of the records this rank
+ * sends (its owned particles in the neighbours' halos) and of its ghosts,
+ * each concatenated over the peers in peer order, with per-peer record
+ * offsets; send_buf / recv_buf are device staging of >= 9 run-precision
+ * values per record of the larger class total. */
+#define SPH_MAX_PEERS 8
+typedef struct {
+    int32_t npeers;
+    int32_t peer[SPH_MAX_PEERS];
+    const int32_t* send_phys[2];
+    const int32_t* recv_phys[2];
+    int64_t send_off[2][SPH_MAX_PEERS + 1];
+    int64_t recv_off[2][SPH_MAX_PEERS + 1];
+    void* send_buf;
+    void* recv_buf;
+} SphHaloPlan;
+/* pack every record of class cls into send_buf / unpack recv_buf into the
+ * ghosts (the transport in between is the caller's: NCCL below, or any
+ * host-staged one) */
+int sph_halo_pack(const SphEngine* e, const SphHaloPlan* plan, int32_t kind, int32_t cls,
+                  cudaStream_t s);
+int sph_halo_unpack(SphEngine* e, const SphHaloPlan* plan, int32_t kind, int32_t cls,
+                    cudaStream_t s);
+/* NCCL communicator among the ranks (libnccl.so.2 is opened on first use:
+ * the copy the process already loaded, e.g. torch's, else the system one) */
+size_t sph_comm_id_bytes(void);
+int sph_comm_unique_id(void* id_out);
+int sph_comm_init(const void* id, int32_t nranks, int32_t rank, void** comm_out);
+int sph_comm_destroy(void* comm);
+/* pack, grouped ncclSend/ncclRecv with every peer, unpack -- all on s */
+int sph_halo_exchange(SphEngine* e, void* comm, const SphHaloPlan* plan, int32_t kind,
+                      int32_t cls, cudaStream_t s);
+/* the nsub sub-steps of a slab rank with the halo refreshes between the
+ * phases (XV of fluid ghosts after KICK_DRIFT, RP_NEXT of fluid ghosts after
+ * CONTINUITY, RP_NEXT of wall ghosts after WALL), one host call per step */
+int sph_engine_substeps_slab(SphEngine* e, void* comm, const SphHaloPlan* plan, double half_dt,
+                             double full_dt, int32_t nsub, cudaStream_t s);
+
 #ifdef __cplusplus
 }
 #endif

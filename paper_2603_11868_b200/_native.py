@@ -58,6 +58,16 @@ class SphSweepArgs_f64(C.Structure):
     _fields_ = _sweep_fields(c_f64)
 
 
+class SphHaloPlan(C.Structure):
+    MAX_PEERS = 8
+    _fields_ = [
+        ("npeers", c_i32), ("peer", c_i32 * 8),
+        ("send_phys", C.c_void_p * 2), ("recv_phys", C.c_void_p * 2),
+        ("send_off", (C.c_int64 * 9) * 2), ("recv_off", (C.c_int64 * 9) * 2),
+        ("send_buf", C.c_void_p), ("recv_buf", C.c_void_p),
+    ]
+
+
 class SphStepStats(C.Structure):
     _fields_ = [
         ("vmax_bits", C.c_uint64), ("amax_bits", C.c_uint64),
@@ -128,6 +138,14 @@ _PROTOS = {
     "sph_engine_phase": (c_i32, [_P, c_i32, c_f64, c_f64, _P]),
     "sph_engine_halo_width": (c_i32, [c_i32]),
     "sph_engine_pack": (c_i32, [_P, c_i32, _P, c_i64, _P, _P]),
+    "sph_halo_pack": (c_i32, [_P, _P, c_i32, c_i32, _P]),
+    "sph_halo_unpack": (c_i32, [_P, _P, c_i32, c_i32, _P]),
+    "sph_comm_id_bytes": (c_size, []),
+    "sph_comm_unique_id": (c_i32, [_P]),
+    "sph_comm_init": (c_i32, [_P, c_i32, c_i32, _P]),
+    "sph_comm_destroy": (c_i32, [_P]),
+    "sph_halo_exchange": (c_i32, [_P, _P, _P, c_i32, c_i32, _P]),
+    "sph_engine_substeps_slab": (c_i32, [_P, _P, _P, c_f64, c_f64, c_i32, _P]),
     "sph_engine_unpack": (c_i32, [_P, c_i32, _P, c_i64, _P, _P]),
 }
 for _sfx, _real in (("f32", c_f32), ("f64", c_f64)):

@@ -1,0 +1,184 @@
+// halo.cu -- halo exchange of a slab rank and the
+// one-call-per-step sub-step loop with the exchanges between the phases.
+//
+// Records are packed / unpacked by the engine's kernels (engine.cu k_pack /
+// k_unpack) for all peers at once; NCCL moves each peer's contiguous slice
+// with grouped ncclSend / ncclRecv on the engine's stream, so a sub-step is
+// enqueued without a host round trip.  NCCL is opened with dlopen on first
+// use (no link-time dependency): the copy already in the process (torch's)
+// if there is one, else the system library.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "engine.cuh"
+
+using namespace sph;
+
+namespace {
+
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl()
+{
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return api;
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    api.get_unique_id = (decltype(api.get_unique_id))sym("ncclGetUniqueId");
+    api.comm_init_rank = (decltype(api.comm_init_rank))sym("ncclCommInitRank");
+    api.comm_destroy = (decltype(api.comm_destroy))sym("ncclCommDestroy");
+    api.group_start = (decltype(api.group_start))sym("ncclGroupStart");
+    api.group_end = (decltype(api.group_end))sym("ncclGroupEnd");
+    api.send = (decltype(api.send))sym("ncclSend");
+    api.recv = (decltype(api.recv))sym("ncclRecv");
+    api.error_string = (decltype(api.error_string))sym("ncclGetErrorString");
+    api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.group_start &&
+             api.group_end && api.send && api.recv;
+    return api;
+}
+
+int nccl_check(ncclResult_t r, const char* what)
+{
+    if (r == ncclSuccess) return SPH_OK;
+    static char buf[256];
+    const char* msg = nccl().error_string ? nccl().error_string(r) : "?";
+    snprintf(buf, sizeof(buf), "%s: NCCL error %d (%s)", what, (int)r, msg);
+    set_error(buf);
+    return SPH_ERR_CUDA;
+}
+
+int need_nccl()
+{
+    if (nccl().ok) return SPH_OK;
+    set_error("NCCL (libnccl.so.2) not available");
+    return SPH_ERR_UNSUPPORTED;
+}
+
+int plan_valid(const SphHaloPlan* p)
+{
+    if (!p || p->npeers < 0 || p->npeers > SPH_MAX_PEERS) {
+        set_error("halo plan: bad peer count");
+        return SPH_ERR_INVALID;
+    }
+    return SPH_OK;
+}
+
+}  // namespace
+
+extern "C" int sph_halo_pack(const SphEngine* e, const SphHaloPlan* plan, int32_t kind,
+                             int32_t cls, cudaStream_t s)
+{
+    int rc = plan_valid(plan);
+    if (rc) return rc;
+    if (cls < 0 || cls > 1) return SPH_ERR_INVALID;
+    const int64_t n = plan->send_off[cls][plan->npeers];
+    if (n <= 0) return SPH_OK;
+    return sph_engine_pack(e, kind, plan->send_phys[cls], n, plan->send_buf, s);
+}
+
+extern "C" int sph_halo_unpack(SphEngine* e, const SphHaloPlan* plan, int32_t kind, int32_t cls,
+                               cudaStream_t s)
+{
+    int rc = plan_valid(plan);
+    if (rc) return rc;
+    if (cls < 0 || cls > 1) return SPH_ERR_INVALID;
+    const int64_t n = plan->recv_off[cls][plan->npeers];
+    if (n <= 0) return SPH_OK;
+    return sph_engine_unpack(e, kind, plan->recv_phys[cls], n, plan->recv_buf, s);
+}
+
+extern "C" size_t sph_comm_id_bytes(void) { return sizeof(ncclUniqueId); }
+
+extern "C" int sph_comm_unique_id(void* id_out)
+{
+    int rc = need_nccl();
+    if (rc) return rc;
+    return nccl_check(nccl().get_unique_id((ncclUniqueId*)id_out), "ncclGetUniqueId");
+}
+
+extern "C" int sph_comm_init(const void* id, int32_t nranks, int32_t rank, void** comm_out)
+{
+    int rc = need_nccl();
+    if (rc) return rc;
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t c = nullptr;
+    rc = nccl_check(nccl().comm_init_rank(&c, nranks, uid, rank), "ncclCommInitRank");
+    if (rc) return rc;
+    *comm_out = (void*)c;
+    return SPH_OK;
+}
+
+extern "C" int sph_comm_destroy(void* comm)
+{
+    if (!comm) return SPH_OK;
+    int rc = need_nccl();
+    if (rc) return rc;
+    return nccl_check(nccl().comm_destroy((ncclComm_t)comm), "ncclCommDestroy");
+}
+
+extern "C" int sph_halo_exchange(SphEngine* e, void* comm, const SphHaloPlan* plan,
+                                 int32_t kind, int32_t cls, cudaStream_t s)
+{
+    int rc = plan_valid(plan);
+    if (rc || (rc = need_nccl())) return rc;
+    const int w = sph_engine_halo_width(kind);
+    if (w < 0 || cls < 0 || cls > 1) return SPH_ERR_INVALID;
+    if ((rc = sph_halo_pack(e, plan, kind, cls, s))) return rc;
+    const size_t es = e->f64 ? sizeof(double) : sizeof(float);
+    const ncclDataType_t dt = e->f64 ? ncclFloat64 : ncclFloat32;
+    NcclApi& api = nccl();
+    if ((rc = nccl_check(api.group_start(), "ncclGroupStart"))) return rc;
+    for (int p = 0; p < plan->npeers && !rc; p++) {
+        const int64_t s0 = plan->send_off[cls][p], sn = plan->send_off[cls][p + 1] - s0;
+        const int64_t r0 = plan->recv_off[cls][p], rn = plan->recv_off[cls][p + 1] - r0;
+        if (sn > 0)
+            rc = nccl_check(api.send((const char*)plan->send_buf + (size_t)s0 * w * es,
+                                     (size_t)sn * w, dt, plan->peer[p], (ncclComm_t)comm, s),
+                            "ncclSend");
+        if (!rc && rn > 0)
+            rc = nccl_check(api.recv((char*)plan->recv_buf + (size_t)r0 * w * es,
+                                     (size_t)rn * w, dt, plan->peer[p], (ncclComm_t)comm, s),
+                            "ncclRecv");
+    }
+    const int rc2 = nccl_check(api.group_end(), "ncclGroupEnd");
+    if (rc || rc2) return rc ? rc : rc2;
+    return sph_halo_unpack(e, plan, kind, cls, s);
+}
+
+extern "C" int sph_engine_substeps_slab(SphEngine* e, void* comm, const SphHaloPlan* plan,
+                                        double half_dt, double full_dt, int32_t nsub,
+                                        cudaStream_t s)
+{
+    int rc = plan_valid(plan);
+    if (rc) return rc;
+    for (int k = 0; k < nsub && !rc; k++) {
+        if (!rc) rc = sph_engine_phase(e, SPH_PHASE_KICK_DRIFT, half_dt, full_dt, s);
+        if (!rc) rc = sph_halo_exchange(e, comm, plan, SPH_HALO_XV, 0, s);
+        if (!rc) rc = sph_engine_phase(e, SPH_PHASE_CONTINUITY, half_dt, full_dt, s);
+        if (!rc) rc = sph_halo_exchange(e, comm, plan, SPH_HALO_RP_NEXT, 0, s);
+        if (!rc) rc = sph_engine_phase(e, SPH_PHASE_WALL, half_dt, full_dt, s);
+        if (!rc) rc = sph_halo_exchange(e, comm, plan, SPH_HALO_RP_NEXT, 1, s);
+        if (!rc) rc = sph_engine_phase(e, SPH_PHASE_MOMENTUM, half_dt, full_dt, s);
+    }
+    return rc;
+}

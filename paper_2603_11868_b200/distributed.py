@@ -241,6 +241,8 @@ class DistributedSimulation:
         self._n_owned = 0
         self.migrated = 0      # particles sent to another rank (this rank)
         self.ghost_fluid = 0   # fluid ghosts received at the last step
+        if hasattr(backend, "attach"):
+            backend.attach(comm)
 
     # -- decomposition ----------------------------------------------------------
 
@@ -290,11 +292,11 @@ class DistributedSimulation:
         self.migrated += sum(cnt[q] for q in send_rows)
         recv_counts = self.comm.exchange_counts({q: cnt[q] for q in send_rows})
         got = self._exchange_fields(self.owned, send_rows, recv_counts)
-        new = {f: torch.cat([self.owned[f][keep]] + [got[f][q] for q in sorted(got[f])])
-               for f in FIELDS}
-        # deterministic local order (by id) -- any order gives the same bits
-        order = torch.argsort(new["id"], stable=True)
-        self.owned = {f: new[f][order] for f in FIELDS}
+        # any local order gives the same bits (sums run in id order); kept
+        # particles first, then arrivals by source rank
+        if send_rows or any(got[f] for f in ("id",)):
+            self.owned = {f: torch.cat([self.owned[f][keep]] +
+                                       [got[f][q] for q in sorted(got[f])]) for f in FIELDS}
 
     def _build_local(self):
         """Owned + ghosts (rows [0, n_own) owned, then ghosts grouped by
@@ -333,6 +335,13 @@ class DistributedSimulation:
         ghosts (`which`)."""
         send_rows, ghost_rows = self._sel[which]
         be = self.backend
+        if hasattr(be, "halo_pack"):   # backend-packed buffers (engine)
+            payload = be.halo_pack(kind, which)
+            got = self.comm.exchange(payload,
+                                     {q: int(r.numel()) for q, r in ghost_rows.items()},
+                                     (be.halo_width(kind),), be.halo_dtype)
+            be.halo_unpack(kind, which, got)
+            return
         payload = {q: be.pack(kind, r) for q, r in send_rows.items()}
         got = self.comm.exchange(payload, {q: int(r.numel()) for q, r in ghost_rows.items()},
                                  (be.halo_width(kind),), be.halo_dtype)
@@ -347,6 +356,8 @@ class DistributedSimulation:
         self._migrate()
         local = self._build_local()
         oob = self.backend.load(local, self._n_owned, self.grid)
+        if hasattr(self.backend, "set_halo"):
+            self.backend.set_halo(self._sel)
         self.out_of_bounds += int(self.comm.allreduce_i64([oob])[0])
 
     def initialize(self):
@@ -390,14 +401,18 @@ class DistributedSimulation:
         dts = dt / nsub
         T = self.dtype.type
         half, full = T(0.5 * dts), T(dts)
-        for _ in range(nsub):
-            self.backend.kick_drift(half, full)
-            self._refresh(XV, "fluid")
-            self.backend.continuity_du(full)
-            self._refresh(RP_NEXT, "fluid")
-            self.backend.wall_pressure()
-            self._refresh(RP_NEXT, "wall")
-            self.backend.momentum_kick(half)
+        if getattr(self.backend, "native_loop", False):
+            # the engine enqueues the sub-steps with their NCCL refreshes itself
+            self.backend.substeps(half, full, nsub)
+        else:
+            for _ in range(nsub):
+                self.backend.kick_drift(half, full)
+                self._refresh(XV, "fluid")
+                self.backend.continuity_du(full)
+                self._refresh(RP_NEXT, "fluid")
+                self.backend.wall_pressure()
+                self._refresh(RP_NEXT, "wall")
+                self.backend.momentum_kick(half)
         self.last_nsub = nsub
         self._finish_counts()
         self.step_count += 1
@@ -451,6 +466,9 @@ class EngineBackend:
         self.T = None
         self._caps = (0, 0, 0)
         self._skin_factor = 3.0
+        self.comm_handle = None     # NCCL communicator of the library (NCCL runs)
+        self.native_loop = False
+        self.plan = None
         from ._device import stream_ptr
         self.stream = stream_ptr(self.device)
 
@@ -506,6 +524,102 @@ class EngineBackend:
                 ctypes.c_void_p(oob.data_ptr()), self.stream)
         self._native.check(rc, "cell_keys")
         return keys, oob
+
+    # -- halo plan ----------------------------------------------------------------
+
+    def attach(self, comm):
+        """On NCCL runs the library gets its own communicator over the same
+        ranks and enqueues every sub-step's halo refreshes itself."""
+        if comm.gloo:
+            return
+        L = self.L
+        uid = ctypes.create_string_buffer(int(L.sph_comm_id_bytes()))
+        if comm.rank == 0:
+            self._native.check(L.sph_comm_unique_id(uid), "comm_unique_id")
+        obj = [uid.raw if comm.rank == 0 else None]
+        comm.dist.broadcast_object_list(obj, src=0)
+        uid = ctypes.create_string_buffer(obj[0], len(obj[0]))
+        handle = ctypes.c_void_p()
+        self._native.check(L.sph_comm_init(uid, comm.size, comm.rank, ctypes.byref(handle)),
+                           "comm_init")
+        self.comm_handle = handle
+        self.native_loop = True
+
+    def set_halo(self, sel):
+        """Device halo plan from the orchestrator's row selections:
+        sel[name] = (send rows {q}, ghost rows {q}), name in (fluid, wall)."""
+        torch = _torch()
+        P = self._native.SphHaloPlan()
+        peers = sorted(set(sel["fluid"][0]) | set(sel["fluid"][1]) |
+                       set(sel["wall"][0]) | set(sel["wall"][1]))
+        if len(peers) > P.MAX_PEERS:
+            raise ValueError(f"{len(peers)} halo peers; at most {P.MAX_PEERS}")
+        P.npeers = len(peers)
+        for k, q in enumerate(peers):
+            P.peer[k] = q
+        keep = []
+        most = 1
+        empty = torch.zeros(0, dtype=torch.int64, device=self.device)
+        for c, name in enumerate(("fluid", "wall")):
+            send, recv = sel[name]
+            for side, rows_of, offs in ((0, send, P.send_off), (1, recv, P.recv_off)):
+                parts = [rows_of.get(q, empty) for q in peers]
+                off = 0
+                for k, r in enumerate(parts):
+                    offs[c][k] = off
+                    off += int(r.numel())
+                offs[c][len(peers)] = off
+                most = max(most, off)
+                rows = torch.cat(parts) if parts else empty
+                phys = self.phys_of_row[rows] if rows.numel() else \
+                    torch.zeros(1, dtype=torch.int32, device=self.device)
+                keep.append(phys)
+                if side == 0:
+                    P.send_phys[c] = phys.data_ptr()
+                else:
+                    P.recv_phys[c] = phys.data_ptr()
+        w = 9   # widest record (XV)
+        self._send_buf = torch.empty(most * w, dtype=self.halo_dtype, device=self.device)
+        self._recv_buf = torch.empty(most * w, dtype=self.halo_dtype, device=self.device)
+        P.send_buf = self._send_buf.data_ptr()
+        P.recv_buf = self._recv_buf.data_ptr()
+        self._plan_keep = keep
+        self._peers = peers
+        self.plan = P
+
+    def _plan_call(self, name, kind, cls):
+        rc = getattr(self.L, name)(ctypes.byref(self.E), ctypes.byref(self.plan),
+                                   ctypes.c_int32(kind), ctypes.c_int32(cls), self.stream)
+        self._native.check(rc, name)
+
+    def halo_pack(self, kind, which):
+        """Pack every record of a class; {peer: (n, width) view of the send
+        buffer} for a host-side transport."""
+        cls = 0 if which == "fluid" else 1
+        self._plan_call("sph_halo_pack", kind, cls)
+        w = self.halo_width(kind)
+        out = {}
+        for k, q in enumerate(self._peers):
+            a, b = self.plan.send_off[cls][k], self.plan.send_off[cls][k + 1]
+            if b > a:
+                out[q] = self._send_buf[a * w: b * w].view(b - a, w)
+        return out
+
+    def halo_unpack(self, kind, which, got):
+        cls = 0 if which == "fluid" else 1
+        w = self.halo_width(kind)
+        for k, q in enumerate(self._peers):
+            a, b = self.plan.recv_off[cls][k], self.plan.recv_off[cls][k + 1]
+            if b > a:
+                self._recv_buf[a * w: b * w].copy_(got[q].reshape(-1))
+        self._plan_call("sph_halo_unpack", kind, cls)
+
+    def substeps(self, half, full, nsub):
+        rc = self.L.sph_engine_substeps_slab(ctypes.byref(self.E), self.comm_handle,
+                                             ctypes.byref(self.plan), ctypes.c_double(float(half)),
+                                             ctypes.c_double(float(full)), ctypes.c_int32(nsub),
+                                             self.stream)
+        self._native.check(rc, "engine_substeps_slab")
 
     # -- backend protocol ---------------------------------------------------------
 
