@@ -206,3 +206,62 @@ def test_compute_timestep_across_policies():
     from paper_2603_11868_b200.physics import timestep_formula
     assert vals.pop() == timestep_formula(vm, am, float(reg.singular("h")),
                                           float(reg.singular("c0")), 1e-3)
+
+
+def _cloud(n, dim, dtype, seed, wall_frac=0.0, spread=1.0, coincident=0):
+    """A random particle cloud registry (+ optional walls and coincident
+    pairs) on a grid covering most of it."""
+    from paper_2603_11868_b200.neighborhood import UniformGrid
+    from paper_2603_11868_b200.physics import setup_state_variables
+    from paper_2603_11868_b200.variables import VariableRegistry
+    rng = np.random.default_rng(seed)
+    reg = VariableRegistry(n, dim, dtype=dtype)
+    setup_state_variables(reg)
+    x = rng.random((n, dim)) * spread
+    if coincident and n > 2 * coincident:
+        x[n - coincident:] = x[:coincident]          # exact duplicates
+    reg.raw_view("x")[:] = x
+    reg.raw_view("v")[:] = rng.normal(0, 0.2, (n, dim))
+    reg.raw_view("rho")[:] = 1000.0 + rng.normal(0, 2.0, n)
+    reg.raw_view("m")[:] = 1000.0 * 0.02 ** dim
+    if wall_frac:
+        reg.raw_view("wall")[:] = (rng.random(n) < wall_frac).astype(np.uint32)
+    reg.raw_view("id")[:] = rng.permutation(n).astype(np.uint32)
+    for k, val in (("rho0", 1000.0), ("c0", 20.0), ("h", 0.026), ("dp", 0.02),
+                   ("alpha_visc", 0.02)):
+        reg.register_singular(k, val)
+    g = np.zeros(dim)
+    g[-1] = -9.81
+    reg.register_singular("g", g)
+    grid = UniformGrid.from_bounds(np.full(dim, 0.05), np.full(dim, 0.95) * spread, 0.052)
+    return reg, grid
+
+
+@pytest.mark.parametrize("dim,dtype", [(2, np.float32), (3, np.float32), (3, np.float64)])
+def test_engine_vs_oracle_random_clouds_with_walls_and_duplicates(dim, dtype):
+    """Scrambled ids, a quarter walls scattered through the fluid, exactly
+    coincident particles (r2 = 0: never neighbours, but inside skin lists)."""
+    n = 4000 if dim == 2 else 6000
+    reg, grid = _cloud(n, dim, dtype, seed=11 + dim, wall_frac=0.25,
+                       spread=1.0 if dim == 2 else 0.5, coincident=50)
+    _oracle_vs_engine(reg, grid, 6)
+
+
+def test_engine_walls_only_and_single_particle():
+    """Degenerate sizes: no fluid at all; one fluid particle (no neighbours)."""
+    reg, grid = _cloud(500, 2, np.float32, seed=3)
+    reg.raw_view("wall")[:] = 1
+    _oracle_vs_engine(reg, grid, 3)
+    reg, grid = _cloud(1, 2, np.float32, seed=4)
+    _oracle_vs_engine(reg, grid, 3)
+
+
+def test_engine_empty_registry():
+    reg, grid = _cloud(0, 2, np.float32, seed=5)
+    osim = O.OracleSim.from_registry(reg, grid)
+    sim = Simulation(reg, grid, CUDA)
+    osim.initialize()
+    sim.initialize()
+    for _ in range(2):
+        assert sim.advance() == osim.advance()
+    assert sim.interaction_count == osim.interaction_count == 0
