@@ -267,6 +267,12 @@ int sph_engine_substep_timed(SphEngine* e, double half_dt, double full_dt, float
  * flags & 2: recompute the exact vmax/amax (physics.py:390-391) and the
  * stability inputs (physics.py:554-564) into e->stats */
 int sph_engine_stats(SphEngine* e, int flags, cudaStream_t s);
+/* physics.py:589-606 sample_pressure, device half: records (registry
+ * position, x, y, z, m, rho, p) as binary64 of the fluid particles with
+ * |x - loc| < radius (binary64), at most cap of them (*count = all found;
+ * loc: host array of 3) */
+int sph_engine_probe(const SphEngine* e, const double* loc, double radius, double* out,
+                     int32_t cap, unsigned int* count, cudaStream_t s);
 
 /* ---- multi-rank slab decomposition ------------------------
  * The sub-step and initialize split at the points where halo data must be

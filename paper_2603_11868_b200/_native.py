@@ -136,6 +136,7 @@ _PROTOS = {
     "sph_engine_substeps": (c_i32, [_P, c_f64, c_f64, c_i32, _P]),
     "sph_engine_substeps_timed": (c_i32, [_P, c_f64, c_f64, c_i32, _P, _P]),
     "sph_engine_phase": (c_i32, [_P, c_i32, c_f64, c_f64, _P]),
+    "sph_engine_probe": (c_i32, [_P, _P, c_f64, _P, c_i32, _P, _P]),
     "sph_engine_halo_width": (c_i32, [c_i32]),
     "sph_engine_pack": (c_i32, [_P, c_i32, _P, c_i64, _P, _P]),
     "sph_halo_pack": (c_i32, [_P, _P, c_i32, c_i32, _P]),

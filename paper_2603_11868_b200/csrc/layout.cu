@@ -241,9 +241,56 @@ __global__ void k_stats(Eng<T> E, int cv, int crp)
     }
 }
 
+// physics.py:589-606 sample_pressure, device half: the fluid particles
+// within reach of a probe (binary64 distance, conservatively widened; the
+// host applies the reference's exact test), one record each:
+// (registry position, x, y, z, m, rho, p) as binary64 (exact widening)
+template <class T, int D>
+__global__ void k_probe(Eng<T> E, int crp, double lx, double ly, double lz, double r2max,
+                        double* __restrict__ out, int cap, unsigned int* __restrict__ count)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= E.nf) return;
+    const vec4<T> P4 = E.pos[i];
+    const double dx = dsub(double(P4.x), lx), dy = dsub(double(P4.y), ly);
+    double r2 = dadd(dmul(dx, dx), dmul(dy, dy));
+    if (D == 3) {
+        const double dz = dsub(double(P4.z), lz);
+        r2 = dadd(r2, dmul(dz, dz));
+    }
+    if (!(r2 < r2max)) return;
+    const unsigned k = atomicAdd(count, 1u);
+    if ((int)k >= cap) return;
+    const vec2<T> RP = E.rp[crp][i];
+    double* o = out + 7 * (size_t)k;
+    o[0] = double(E.refpos[i]);
+    o[1] = double(P4.x); o[2] = double(P4.y); o[3] = D == 3 ? double(P4.z) : 0.0;
+    o[4] = double(P4.w); o[5] = double(RP.x); o[6] = double(RP.y);
+}
+
 }  // namespace sph
 
 using namespace sph;
+
+template <class T, int D>
+static int probe_impl(const SphEngine* e, const double* loc, double radius, double* out,
+                      int32_t cap, unsigned int* count, cudaStream_t s)
+{
+    cudaMemsetAsync(count, 0, sizeof(unsigned int), s);
+    if (e->nf > 0)
+        note_launch(), k_probe<T, D><<<grid_for(e->nf, 256), 256, 0, s>>>(
+            eng_of<T>(e), e->cur_rp, loc[0], loc[1], D == 3 ? loc[2] : 0.0, radius * radius,
+            out, cap, count);
+    return check_launch("engine_probe");
+}
+
+extern "C" int sph_engine_probe(const SphEngine* e, const double* loc, double radius, double* out,
+                                int32_t cap, unsigned int* count, cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc) return rc;
+    return SPH_DISPATCH(e, probe_impl, e, loc, radius, out, cap, count, s);
+}
 
 static size_t engine_sort_bytes(int64_t n)
 {

@@ -748,6 +748,32 @@ class Simulation:
                 f"runaway velocity {vmax_f:.3g} at step {self.step_count}")
         return dt
 
+    def probe_candidates(self, location, reach, cap=1 << 16):
+        """Fluid particles within (a conservatively widened) reach of a point,
+        as registry-ordered host arrays (x, m, rho, p) in the run dtype, or
+        None when there are more than cap of them."""
+        torch = torch_mod()
+        d = self._dev
+        loc = np.zeros(3, np.float64)
+        loc[:self.registry.dim] = np.asarray(location, np.float64)
+        if "probe" not in d or d["probe"].shape[0] < cap * 7:
+            d["probe"] = torch.empty(cap * 7, dtype=torch.float64, device=d["device"])
+            d["probe_n"] = torch.zeros(1, dtype=torch.int32, device=d["device"])
+        rc = _native.lib().sph_engine_probe(
+            ctypes.byref(d["E"]), loc.ctypes.data_as(ctypes.c_void_p),
+            ctypes.c_double(reach * (1.0 + 1e-9) + 1e-300), ptr(d["probe"]), cap,
+            ptr(d["probe_n"]), d["stream"])
+        _native.check(rc, "engine_probe")
+        k = int(d["probe_n"].item())
+        if k > cap:
+            return None
+        rec = d["probe"][: 7 * k].view(k, 7).cpu().numpy()
+        rec = rec[np.argsort(rec[:, 0], kind="stable")]
+        dt = self.registry.dtype
+        dim = self.registry.dim
+        return (rec[:, 1:1 + dim].astype(dt), rec[:, 4].astype(dt), rec[:, 5].astype(dt),
+                rec[:, 6].astype(dt))
+
     def _stability_check(self, c0):
         """physics.py:554-564 on the registry state."""
         rho = self.registry.view("rho")
@@ -781,11 +807,9 @@ def total_energy(registry):
     return ke + pe + ce
 
 
-def sample_pressure(registry, location):
-    x = registry.view("x")
-    wall = registry.view("wall")
-    h = float(registry.singular("h"))
-    d = registry.dim
+def _shepard_probe(x, wall, m, rho, p, h, d, location):
+    """physics.py:589-606 on arrays in registry order (the masked sums are
+    numpy's, in that order)."""
     loc = np.asarray(location, dtype=np.float64)
     diff = x.astype(np.float64) - loc
     r = np.sqrt((diff * diff).sum(axis=1))
@@ -793,8 +817,27 @@ def sample_pressure(registry, location):
     if not mask.any():
         return 0.0
     w = np.array([kernel_W(ri, h, d) for ri in r[mask]])
-    vol = (registry.view("m")[mask] / registry.view("rho")[mask]).astype(np.float64)
+    vol = (m[mask] / rho[mask]).astype(np.float64)
     den = float((w * vol).sum())
     if den == 0.0:
         return 0.0
-    return float((registry.view("p")[mask] * w * vol).sum() / den)
+    return float((p[mask] * w * vol).sum() / den)
+
+
+def sample_pressure(registry, location):
+    """Shepard-interpolated fluid pressure at a point (physics.py:589-606).
+
+    While a device engine holds the state, only the fluid particles near the
+    probe are fetched (sph_engine_probe) -- in registry order, so the
+    reference's computation on them gives the same bits -- instead of pulling
+    every field to the host."""
+    h = float(registry.singular("h"))
+    d = registry.dim
+    eng = getattr(registry, "_engine", None)
+    if eng is not None and getattr(eng, "_host_stale", False):
+        sub = eng.probe_candidates(location, 2.0 * h)
+        if sub is not None:
+            x, m, rho, p = sub
+            return _shepard_probe(x, np.zeros(len(m), np.uint32), m, rho, p, h, d, location)
+    return _shepard_probe(registry.view("x"), registry.view("wall"), registry.view("m"),
+                          registry.view("rho"), registry.view("p"), h, d, location)
