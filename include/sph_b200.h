@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 3
+#define SPH_ABI_VERSION 4
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -177,6 +177,8 @@ typedef struct {
     unsigned int oob_walls;           /* wall clamps (counted once, at push)   */
     unsigned int nfix;                /* exact list rebuilds (skin fallbacks)  */
     unsigned int nan_flags;           /* bit0: a NaN rho, bit1: a NaN |v|^2    */
+    unsigned int push_error;          /* push: ids not a permutation of 0..n-1 */
+    unsigned int fluid_seen;          /* push: particles with wall == 0        */
     unsigned int reserved;
 } SphStepStats;
 

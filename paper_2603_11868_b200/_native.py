@@ -75,7 +75,8 @@ class SphStepStats(C.Structure):
         ("v2max_key", C.c_uint64), ("dmax_bits", C.c_uint64),
         ("overflow", C.c_uint32), ("oob", C.c_uint32),
         ("oob_walls", C.c_uint32), ("nfix", C.c_uint32),
-        ("nan_flags", C.c_uint32), ("reserved", C.c_uint32),
+        ("nan_flags", C.c_uint32), ("push_error", C.c_uint32),
+        ("fluid_seen", C.c_uint32), ("reserved", C.c_uint32),
     ]
 
 
@@ -101,7 +102,7 @@ class SphEngine(C.Structure):
     ]
 
 
-ABI_VERSION = 3   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 4   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)

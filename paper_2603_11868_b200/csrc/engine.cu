@@ -213,7 +213,15 @@ __device__ __forceinline__ void enqueue(uint32_t* queue, uint32_t* qcount, bool 
 // Blocks larger than the tile fall back to the per-particle collector.
 template <class T, int D> struct SkinTile;
 template <> struct SkinTile<float, 2> { static constexpr int kThreads = 128, kCands = 256; };
-template <> struct SkinTile<float, 3> { static constexpr int kThreads = 256, kCands = 1024; };
+#ifndef SPH_SKIN3_THREADS
+#define SPH_SKIN3_THREADS 128
+#endif
+#ifndef SPH_SKIN3_CANDS
+#define SPH_SKIN3_CANDS 768
+#endif
+template <> struct SkinTile<float, 3> {
+    static constexpr int kThreads = SPH_SKIN3_THREADS, kCands = SPH_SKIN3_CANDS;
+};
 template <> struct SkinTile<double, 2> { static constexpr int kThreads = 128, kCands = 256; };
 template <> struct SkinTile<double, 3> { static constexpr int kThreads = 256, kCands = 512; };
 
@@ -284,7 +292,9 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
             const uint32_t* __restrict__ phys_of_id)
 {
     constexpr int NT = SkinTile<T, D>::kThreads, NW = NT / 32, kC = SkinTile<T, D>::kCands;
-    __shared__ uint32_t sj[kC];        // candidate ids, sorted; then their indices j
+    constexpr int kP = kC <= 64 ? 64 : (kC <= 128 ? 128 : (kC <= 256 ? 256 : (kC <= 512 ? 512
+                                     : (kC <= 1024 ? 1024 : 2048))));
+    __shared__ uint32_t sj[kP];        // candidate ids, sorted; then their indices j
     __shared__ vec4<T> spos[kC];       // positions in sorted order
     __shared__ uint32_t run_start[2 * 9], run_pre[2 * 9 + 1];
     const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
@@ -1135,12 +1145,19 @@ static void sub_wall(SphEngine* e, cudaStream_t s)
         launch_wall<T, D>(e, e->cur_rp ^ 1, 1, 1, 1, e->cur_v ^ 1, s);
 }
 
+// zero_walls: the reference's momentum body writes dvdt = 0 for walls
+// (physics.py:128-131); only a host edit can make it non-zero, and nothing
+// reads it within a step, so once per step suffices
 template <class T, int D>
-static void sub_momentum(SphEngine* e, T half, T next_full, bool fuse, cudaStream_t s)
+static void sub_momentum(SphEngine* e, T half, T next_full, bool fuse, bool zero_walls,
+                         cudaStream_t s)
 {
     Eng<T> E = eng_of<T>(e);
     const int cv = e->cur_v;
     fuse = fuse && e->nf > 0;
+    if (zero_walls && e->n > e->nf)
+        cudaMemsetAsync((char*)e->dvdt + sizeof(vec4<T>) * (size_t)e->nf, 0,
+                        sizeof(vec4<T>) * (size_t)(e->n - e->nf), s);
     if (e->nf > 0)
         note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
             E, make_phys<T>(phys_of_engine(e)), cv, e->cur_rp ^ 1, 1, half, 2,
@@ -1173,7 +1190,7 @@ static void substep_parts(SphEngine* e, T half, T full, bool fuse, cudaEvent_t* 
     if (ev) cudaEventRecord(ev[3], s);
     sub_wall<T, D>(e, s);
     if (ev) cudaEventRecord(ev[4], s);
-    sub_momentum<T, D>(e, half, full, fuse, s);
+    sub_momentum<T, D>(e, half, full, fuse, !fuse, s);
     if (ev) cudaEventRecord(ev[5], s);
 }
 
@@ -1264,7 +1281,7 @@ static int phase_impl(SphEngine* e, int phase, double half_d, double full_d, cud
         sub_continuity<T, D>(e, full, s);
         break;
     case SPH_PHASE_WALL: sub_wall<T, D>(e, s); break;
-    case SPH_PHASE_MOMENTUM: sub_momentum<T, D>(e, half, T(0), false, s); break;
+    case SPH_PHASE_MOMENTUM: sub_momentum<T, D>(e, half, T(0), false, true, s); break;
     case SPH_PHASE_INIT_WALL: init_wall<T, D>(e, s); break;
     case SPH_PHASE_INIT_MOMENTUM: init_momentum<T, D>(e, s); break;
     default: set_error("engine_phase: unknown phase"); return SPH_ERR_INVALID;

@@ -13,6 +13,29 @@
 
 namespace sph {
 
+// push-time registry checks (the former host-side O(n) scans): ids must be
+// a permutation of 0..n-1 (counted by id), and the fluid count is reported
+__global__ void k_id_count(const uint32_t* __restrict__ id, const uint32_t* __restrict__ wall,
+                           int64_t n, uint32_t* __restrict__ cnt, SphStepStats* st)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool fluid = false;
+    if (r < n) {
+        const uint32_t pid = id[r];
+        if (pid < (uint64_t)n) atomicAdd(&cnt[pid], 1u);
+        else st->push_error = 1;
+        fluid = wall[r] == 0;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, fluid);
+    if (lane_id() == 0 && b) atomicAdd(&st->fluid_seen, (unsigned)__popc(b));
+}
+
+__global__ void k_id_check(const uint32_t* __restrict__ cnt, int64_t n, SphStepStats* st)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n && cnt[r] != 1u) st->push_error = 1;
+}
+
 template <class T, int D>
 __global__ void k_push_keys(const T* __restrict__ x, const uint32_t* __restrict__ wall, int64_t n,
                             GridP<T> g, int key_bits, uint32_t* __restrict__ keys,
@@ -60,6 +83,7 @@ __global__ void k_push_gather(Eng<T> E, const uint32_t* __restrict__ perm, const
     E.id[i] = pid;
     E.nnb[i] = nnb[r];
     E.refpos[i] = r;
+    if (pid >= (uint64_t)E.n) return;   // reported by k_id_count (push_error)
     E.rho_scratch_id[pid] = rho_scratch[r];
     E.oflow_id[pid] = oflow[r];
     E.wall_id[pid] = wall[r];
@@ -346,6 +370,11 @@ static int push_impl(SphEngine* e, const void* x, const void* v, const void* rho
     const int64_t n = e->n;
     cudaMemsetAsync(e->stats, 0, sizeof(SphStepStats), s);
     if (n > 0) {
+        uint32_t* cnt = bump.take<uint32_t>(n);
+        if (!cnt) return SPH_ERR_WORKSPACE;
+        cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)n, s);
+        note_launch(), k_id_count<<<grid_for(n, 256), 256, 0, s>>>(id, wall, n, cnt, e->stats);
+        note_launch(), k_id_check<<<grid_for(n, 256), 256, 0, s>>>(cnt, n, e->stats);
         note_launch(), k_push_keys<T, D><<<grid_for(n, 256), 256, 0, s>>>(
             (const T*)x, wall, n, g, e->key_bits, sb.k0, &e->stats->oob_walls);
         int which = 0;

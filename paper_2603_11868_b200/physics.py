@@ -568,22 +568,24 @@ class Simulation:
 
     def _push(self):
         """Registry -> device SoA (physics layout, cell order)."""
-        torch = torch_mod()
         reg = self.registry
-        ids = reg.raw_view("id")
-        n = reg.particle_count
-        if n and (ids.min() != 0 or ids.max() != n - 1
-                  or np.bincount(ids.astype(np.int64), minlength=n).max() != 1):
-            raise ValueError("registry ids must be a permutation of 0..N-1")
-        if self._dev is None or int((reg.raw_view("wall") == 0).sum()) != self._dev["E"].nf:
+        if self._dev is None:
             self._alloc()
         d = self._dev
         st = Staging(d["device"])
         devs = [st.to_dev(reg.raw_view(f)) for f in _ENGINE_FIELDS]
-        rc = _native.lib().sph_engine_push(ctypes.byref(d["E"]),
-                                           *[ptr(t) for t in devs], d["stream"])
-        _native.check(rc, "engine_push")
-        stats = self._read_stats()
+        # the id-permutation check and the fluid count run on the device
+        for attempt in range(2):
+            rc = _native.lib().sph_engine_push(ctypes.byref(d["E"]),
+                                               *[ptr(t) for t in devs], d["stream"])
+            _native.check(rc, "engine_push")
+            stats = self._read_stats()
+            if stats.push_error:
+                raise ValueError("registry ids must be a permutation of 0..N-1")
+            if stats.fluid_seen == d["E"].nf or attempt:
+                break
+            self._alloc()       # the wall flags changed: resize the list storage
+            d = self._dev
         self._oob_walls = stats.oob_walls
         del devs, st
         self._host_dirty = False

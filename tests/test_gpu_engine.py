@@ -265,3 +265,27 @@ def test_engine_empty_registry():
     for _ in range(2):
         assert sim.advance() == osim.advance()
     assert sim.interaction_count == osim.interaction_count == 0
+
+
+def test_push_checks_ids_and_follows_wall_flag_edits():
+    """The registry checks run on the device at push: a non-permutation of
+    ids raises ValueError; edited wall flags resize the engine."""
+    reg, grid = _cloud(2000, 2, np.float32, seed=21, wall_frac=0.2)
+    sim = Simulation(reg, grid, CUDA)
+    sim.initialize()
+    sim.advance()
+    ids = reg.view("id")
+    saved = ids.copy()
+    ids[0] = ids[1]
+    with pytest.raises(ValueError):
+        sim.advance()
+    reg.view("id")[:] = saved
+    wall = reg.view("wall")
+    wall[:60] ^= 1
+    osim = O.OracleSim.from_registry(reg, grid)
+    osim.st.step_count = sim.step_count
+    osim.st.time = sim.time
+    for _ in range(3):
+        assert sim.advance() == osim.advance()
+    for f in FIELDS:
+        assert reg.view(f).tobytes() == osim.f[f].tobytes(), f
