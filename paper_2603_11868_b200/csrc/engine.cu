@@ -37,6 +37,9 @@
 #ifndef SPH_SKIN_THREADS_PER_SM
 #define SPH_SKIN_THREADS_PER_SM 1536   // skin-list build occupancy (register cap)
 #endif
+#ifndef SPH_SKINW_MINB
+#define SPH_SKINW_MINB 4     // warp-per-cell skin build: blocks per SM (register cap)
+#endif
 #ifndef SPH_MOM_WALK
 #define SPH_MOM_WALK sweep_list   // sweep_list_pf (one pair ahead) measured slower
 #endif
@@ -212,7 +215,15 @@ __device__ __forceinline__ void enqueue(uint32_t* queue, uint32_t* qcount, bool 
 // survivors are already in ascending id, so no per-particle sort is needed.
 // Blocks larger than the tile fall back to the per-particle collector.
 template <class T, int D> struct SkinTile;
-template <> struct SkinTile<float, 2> { static constexpr int kThreads = 128, kCands = 256; };
+#ifndef SPH_SKIN2_THREADS
+#define SPH_SKIN2_THREADS 128
+#endif
+#ifndef SPH_SKIN2_CANDS
+#define SPH_SKIN2_CANDS 256
+#endif
+template <> struct SkinTile<float, 2> {
+    static constexpr int kThreads = SPH_SKIN2_THREADS, kCands = SPH_SKIN2_CANDS;
+};
 #ifndef SPH_SKIN3_THREADS
 #define SPH_SKIN3_THREADS 128
 #endif
@@ -474,6 +485,212 @@ k_phys_of_id(const uint32_t* __restrict__ id, int64_t n, uint32_t* __restrict__ 
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) phys_of_id[id[i]] = (uint32_t)i;
+}
+
+// Ascending bitonic sort of 32*PER keys held blocked in a warp (lane owns
+// elements lane*PER .. lane*PER+PER-1).
+template <int PER, class K>
+__device__ __forceinline__ void warp_sort_blocked(K (&v)[PER], unsigned lane)
+{
+    constexpr int N = 32 * PER;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= PER) {
+#pragma unroll
+                for (int r = 0; r < PER; r++) {
+                    const K o = __shfl_xor_sync(0xffffffffu, v[r], j / PER);
+                    const int e = (int)lane * PER + r;
+                    const bool up = (e & k) == 0, lower = (e & j) == 0;
+                    v[r] = ((o < v[r]) == (lower == up)) ? o : v[r];
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < PER; r++) {
+                    if (r & j) continue;
+                    const int e = (int)lane * PER + r;
+                    const bool up = (e & k) == 0;
+                    const K a = v[r], b = v[r ^ j];
+                    const bool sw = (a > b) == up;
+                    v[r] = sw ? b : a;
+                    v[r ^ j] = sw ? a : b;
+                }
+            }
+        }
+    }
+}
+
+// Skin lists of small candidate blocks (<= 128, the 2D case): a warp per
+// cell with the sort in registers and the candidates in a per-warp shared
+// tile, no block barriers; larger blocks are passed on to k_skin_tile.
+template <class T, int D, int PER>
+__device__ __forceinline__ void skin_warp_load_sort(const Eng<T>& E, int M, int nruns,
+                                                    uint32_t s0, uint32_t pre, unsigned lane,
+                                                    uint32_t* sj)
+{
+    uint32_t v[PER];
+    int base[PER];
+#pragma unroll
+    for (int q = 0; q < PER; q++) base[q] = -1;
+    for (int r = 0; r < nruns; r++) {   // the last run starting at or before e holds e
+        const uint32_t rp = __shfl_sync(0xffffffffu, pre, r);
+        const uint32_t rs = __shfl_sync(0xffffffffu, s0, r);
+#pragma unroll
+        for (int q = 0; q < PER; q++) {
+            const uint32_t e = lane * PER + q;
+            if (rp <= e) base[q] = (int)(rs + (e - rp));
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < PER; q++) {
+        const int e = (int)lane * PER + q;
+        v[q] = (e < M) ? E.id[base[q]] : 0xffffffffu;
+    }
+    warp_sort_blocked<PER>(v, lane);
+#pragma unroll
+    for (int q = 0; q < PER; q++) sj[lane * PER + q] = v[q];
+    __syncwarp();
+}
+
+template <class T, int D>
+__global__ void __launch_bounds__(256, SPH_SKINW_MINB)
+k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cells,
+            const uint32_t* __restrict__ ncells_p, const uint32_t* __restrict__ phys_of_id,
+            uint32_t* __restrict__ big, uint32_t* __restrict__ nbig)
+{
+    constexpr int NW = 8, kW = 128;
+    __shared__ uint32_t wsj[NW][kW];
+    __shared__ vec4<T> wpos[NW][kW];
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
+    uint32_t* sj = wsj[warp];
+    vec4<T>* spos = wpos[warp];
+    const int64_t nf = E.nf;
+    const T inf = T(INFINITY);
+    const uint32_t ncells = *(volatile const uint32_t*)ncells_p;
+    for (uint32_t ci = blockIdx.x * NW + warp; ci < ncells; ci += gridDim.x * NW) {
+        const int64_t c = cells[ci];
+        const uint32_t f0 = E.offs_f[c], f1 = E.offs_f[c + 1];
+        const uint32_t w0 = E.offs_w[c], w1 = E.offs_w[c + 1];
+        const int ntf = (int)(f1 - f0), nt = ntf + (int)(w1 - w0);
+        int cc[3];
+        if (D == 3) {
+            cc[2] = (int)(c % g.s[2]);
+            cc[1] = (int)((c / g.s[2]) % g.s[1]);
+            cc[0] = (int)(c / ((int64_t)g.s[1] * g.s[2]));
+        } else {
+            cc[1] = (int)(c % g.s[1]);
+            cc[0] = (int)(c / g.s[1]);
+            cc[2] = 0;
+        }
+        const int xlo = max(cc[0] - 1, 0), xhi = min(cc[0] + 1, g.s[0] - 1);
+        const int ylo = max(cc[1] - 1, 0), yhi = min(cc[1] + 1, g.s[1] - 1);
+        const int zlo = D == 3 ? max(cc[2] - 1, 0) : 0;
+        const int zhi = D == 3 ? min(cc[2] + 1, g.s[2] - 1) : 0;
+        const int nyr = D == 3 ? (yhi - ylo + 1) : 1;
+        const int rps = (xhi - xlo + 1) * nyr;
+        const int nruns = 2 * rps;
+        int64_t s0 = 0, s1 = 0;
+        if ((int)lane < nruns) {
+            const int seg = (int)lane / rps, rr = (int)lane - seg * rps;
+            const int ax = xlo + rr / nyr, ay = ylo + rr % nyr;
+            uint32_t klo, khi;
+            if (D == 3) {
+                const uint32_t rowk = ((uint32_t)ax * g.s[1] + ay) * g.s[2];
+                klo = rowk + zlo;
+                khi = rowk + zhi;
+            } else {
+                klo = (uint32_t)ax * g.s[1] + ylo;
+                khi = (uint32_t)ax * g.s[1] + yhi;
+            }
+            if (seg == 0) { s0 = E.offs_f[klo]; s1 = E.offs_f[khi + 1]; }
+            else { s0 = nf + E.offs_w[klo]; s1 = nf + E.offs_w[khi + 1]; }
+        }
+        const uint32_t len = (uint32_t)(s1 - s0);
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (unsigned)o) incl += t;
+        }
+        const int M = (int)__shfl_sync(0xffffffffu, incl, 31);
+        if (M > kW) {
+            if (lane == 0) big[atomicAdd(nbig, 1u)] = (uint32_t)c;
+            continue;
+        }
+        if (M <= 64)
+            skin_warp_load_sort<T, D, 2>(E, M, nruns, (uint32_t)s0, incl - len, lane, sj);
+        else
+            skin_warp_load_sort<T, D, 4>(E, M, nruns, (uint32_t)s0, incl - len, lane, sj);
+        const int Mp = (M + 31) & ~31;
+        for (int k = (int)lane; k < Mp; k += 32) {
+            vec4<T> p;
+            if (k < M) {
+                const uint32_t j = phys_of_id[sj[k]];
+                sj[k] = j;
+                p = E.pos[j];
+            } else {
+                p.x = inf; p.y = inf; p.z = inf; p.w = T(0);
+                sj[k] = 0;
+            }
+            spos[k] = p;
+        }
+        __syncwarp();
+        for (int t = 0; t < nt; t += 2) {
+            const bool hasB = t + 1 < nt;
+            const bool flA = t < ntf, flB = t + 1 < ntf;
+            const int64_t iA = flA ? (int64_t)f0 + t : nf + w0 + (t - ntf);
+            const int64_t iB = hasB ? (flB ? (int64_t)f0 + t + 1 : nf + w0 + (t + 1 - ntf)) : iA;
+            const int64_t slA = flA ? iA : E.nf_pad + (iA - nf);
+            const int64_t slB = flB ? iB : E.nf_pad + (iB - nf);
+            T xa[3], xb[3];
+            to3<T>(E.pos[iA], xa);
+            to3<T>(E.pos[iB], xb);
+            int32_t* __restrict__ lpA = E.lists + ell_base(slA);
+            int32_t* __restrict__ lpB = E.lists + ell_base(slB);
+            int cntA = 0, cntB = 0, naA = 0, naB = 0;
+            for (int base = 0; base < Mp; base += 32) {
+                const int k = base + (int)lane;
+                const uint32_t j = sj[k];
+                T xj[3];
+                to3<T>(spos[k], xj);
+                const T r2a = accept_r2<T, D>(xa, xj);
+                const T r2b = accept_r2<T, D>(xb, xj);
+                const bool jf = (int64_t)j < nf;
+                const bool stA = (flA || jf) && r2a < cs2 && j != (uint32_t)iA;
+                const bool stB = hasB && (flB || jf) && r2b < cs2 && j != (uint32_t)iB;
+                const unsigned bA = __ballot_sync(0xffffffffu, stA);
+                const unsigned bB = __ballot_sync(0xffffffffu, stB);
+                if (stA) lpA[ell_off(cntA + __popc(bA & lt))] = (int32_t)j;   // M <= 128 < kCap
+                if (stB) lpB[ell_off(cntB + __popc(bB & lt))] = (int32_t)j;
+                cntA += __popc(bA);
+                cntB += __popc(bB);
+                if (!flA || !flB) {
+                    const bool ctA = !flA && !jf && r2a < g.c2 && r2a > T(0) && j != (uint32_t)iA;
+                    const bool ctB = hasB && !flB && !jf && r2b < g.c2 && r2b > T(0) &&
+                                     j != (uint32_t)iB;
+                    naA += __popc(__ballot_sync(0xffffffffu, ctA));
+                    naB += __popc(__ballot_sync(0xffffffffu, ctB));
+                }
+            }
+            if (lane < 2 && (lane == 0 || hasB)) {
+                const int64_t i = lane ? iB : iA;
+                const int64_t slot = lane ? slB : slA;
+                T xi[3];
+                xi[0] = lane ? xb[0] : xa[0];
+                xi[1] = lane ? xb[1] : xa[1];
+                xi[2] = lane ? xb[2] : xa[2];
+                int cxyz[3];
+                const bool ok = cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c;
+                E.cell0[i] = ok ? (uint32_t)c : kInvalidCell;
+                E.lcount[slot] = ok ? (lane ? cntB : cntA) : 0;
+                E.nww[slot] = lane ? naB : naA;
+                E.disp[i] = T(0);
+            }
+        }
+        __syncwarp();
+    }
 }
 
 // skin lists of the cells k_skin_tile queued (candidate block above the
@@ -970,14 +1187,24 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
         Bump bump(e->ws, e->ws_bytes);
         uint32_t* phys_of_id = bump.take<uint32_t>(e->n);
         uint32_t* cells = bump.take<uint32_t>(e->n);   // nonempty cells <= n
-        uint32_t* ncells = bump.take<uint32_t>(1);
-        if (!ncells) return SPH_ERR_WORKSPACE;
+        uint32_t* big = bump.take<uint32_t>(e->n);     // cells with > 128 candidates
+        uint32_t* counts = bump.take<uint32_t>(2);
+        if (!counts) return SPH_ERR_WORKSPACE;
         note_launch(), k_phys_of_id<<<grid_for(e->n, 256), 256, 0, s>>>(e->id, e->n, phys_of_id);
-        cudaMemsetAsync(ncells, 0, sizeof(uint32_t), s);
+        cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), s);
         note_launch(), k_nonempty_cells<<<grid_for(e->ncells, 256), 256, 0, s>>>(
-            e->offs_f, e->offs_w, e->ncells, cells, ncells);
-        note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, cells, ncells,
-                                                              phys_of_id);
+            e->offs_f, e->offs_w, e->ncells, cells, counts);
+        if (D == 2) {   // 2D blocks hold ~60 candidates: a warp per cell
+            const int64_t wb = (want + 7) / 8;
+            note_launch(), k_skin_warp<T, D><<<(unsigned)(wb < 148 * 8 ? wb : 148 * 8), 256, 0,
+                                               s>>>(g, cs2, E, cells, counts, phys_of_id, big,
+                                                    counts + 1);
+            note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, big,
+                                                                  counts + 1, phys_of_id);
+        } else {        // 3D blocks hold ~450: a thread block per cell
+            note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, cells, counts,
+                                                                  phys_of_id);
+        }
         note_launch(), k_skin_big<T, D><<<148 * 2, kNlThreads, 0, s>>>(acc, g, cs2, E);
     }
     e->lists_ready = 1;
