@@ -40,6 +40,12 @@
 #ifndef SPH_SKINW_MINB
 #define SPH_SKINW_MINB 4     // warp-per-cell skin build: blocks per SM (register cap)
 #endif
+#ifndef SPH_CONT_ILP
+#define SPH_CONT_ILP 0       // continuity: two accepted pairs per basic block
+#endif
+#ifndef SPH_MOM_ILP
+#define SPH_MOM_ILP 1        // momentum: two pairs per basic block (1: in 2D, 2: always)
+#endif
 #ifndef SPH_MOM_WALK
 #define SPH_MOM_WALK sweep_list   // sweep_list_pf (one pair ahead) measured slower
 #endif
@@ -137,7 +143,7 @@ template <class T> struct NbrPR { vec4<T> p; vec2<T> rp; };
 // list entries + positions in flight (phase 1, bits in a register), then the
 // accepted neighbours are visited in list (= ascending id) order with the
 // next one's data prefetched (phase 2).  Rejected entries cost only phase 1.
-template <class T, int D, class Load, class Body>
+template <class T, int D, bool PAIRS = false, class Load, class Body>
 __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const T (&xi)[3],
                                             T c2, int nl, Load load, Body body)
 {
@@ -182,11 +188,24 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
             if (!more) break;
         }
 #else
-        while (m) {
-            const int u = __ffs(m) - 1;
-            m &= m - 1;
-            const int j = lp[ell_off(w0 + u)];
-            body(j, load(j));
+        if constexpr (PAIRS) {   // two accepted neighbours per call: independent chains
+            while (m) {
+                const int ua = __ffs(m) - 1;
+                m &= m - 1;
+                const bool hb = m != 0;
+                const int ub = hb ? __ffs(m) - 1 : ua;
+                m &= m - 1;
+                const int ja = lp[ell_off(w0 + ua)];
+                const int jb = hb ? lp[ell_off(w0 + ub)] : ja;
+                body(ja, load(ja), jb, load(jb), hb);
+            }
+        } else {
+            while (m) {
+                const int u = __ffs(m) - 1;
+                m &= m - 1;
+                const int j = lp[ell_off(w0 + u)];
+                body(j, load(j));
+            }
         }
 #endif
     }
@@ -949,15 +968,39 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
         int4* __restrict__ eq = reinterpret_cast<int4*>(E.elist + ell_base(i));
         int e0 = 0, e1 = 0, e2 = 0;
         cnt = 0;
-        filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf, [&](int j, const NbrPV<T>& nb) {
+        auto store = [&](int j) {
             const int r = cnt & 3;
             if (r == 0) e0 = j;
             else if (r == 1) e1 = j;
             else if (r == 2) e2 = j;
             else if (cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, j);
-            pair(cnt, nb);
             cnt++;
+        };
+#if SPH_CONT_ILP
+        auto term = [&](const NbrPV<T>& nb) {
+            T xj[3], vj[3], dx[3], r2, vx;
+            to3<T>(nb.p, xj);
+            to3<T>(nb.v, vj);
+            pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
+            return continuity_term<T>(r2, vx, nb.v.w, P);
+        };
+        filter_walk<T, D, true>(E, i, xi, g.c2, E.lcount[i], loadf,
+                                [&](int ja, const NbrPV<T>& na, int jb, const NbrPV<T>& nb,
+                                    bool hb) {
+            const double ta = term(na), tb = term(nb);
+            store(ja);
+            acc = dadd(acc, ta);
+            if (hb) {
+                store(jb);
+                acc = dadd(acc, tb);
+            }
         });
+#else
+        filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf, [&](int j, const NbrPV<T>& nb) {
+            store(j);
+            pair(cnt, nb);
+        });
+#endif
         if ((cnt & 3) && cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, 0);
         if (cnt > kCap) {
             E.acount[i] = -1;
@@ -1067,6 +1110,46 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
             const T pi_rr = RQI.y;
             T a[3] = {P.g[0], P.g[1], P.g[2]};
             auto loadf = [&](int j) { return NbrPVR<T>{pos[j], vel[j], rq[j]}; };
+#if SPH_MOM_ILP
+            if (SPH_MOM_ILP > 1 || D == 2) {
+            // two pairs per basic block: their terms are independent chains the
+            // scheduler interleaves; accumulation stays in list order
+            auto terms = [&](const NbrPVR<T>& nb, double (&t)[3]) {
+                T xj[3], vj[3], dx[3], r2, vx;
+                to3<T>(nb.p, xj);
+                to3<T>(nb.v, vj);
+                pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
+                momentum_terms<T, D>(r2, vx, dx, rho_i, pi_rr, nb.rp.x, nb.rp.y, nb.p.w, P, t);
+            };
+            if (acnt > 0) {
+                const int4* __restrict__ q4 = reinterpret_cast<const int4*>(E.elist + ell_base(i));
+                int4 qn = q4[0];
+                for (int t0 = 0; t0 < acnt; t0 += 4) {
+                    const int4 q = qn;
+                    if (t0 + 4 < acnt) qn = q4[((t0 >> 2) + 1) * 32];
+                    {
+                        const bool hb = t0 + 1 < acnt;
+                        const NbrPVR<T> na = loadf(q.x), nb = loadf(hb ? q.y : q.x);
+                        double ta[3], tb[3];
+                        terms(na, ta);
+                        terms(nb, tb);
+                        momentum_accumulate<T, D>(ta, a);
+                        if (hb) momentum_accumulate<T, D>(tb, a);
+                    }
+                    if (t0 + 2 < acnt) {
+                        const bool hb = t0 + 3 < acnt;
+                        const NbrPVR<T> na = loadf(q.z), nb = loadf(hb ? q.w : q.z);
+                        double ta[3], tb[3];
+                        terms(na, ta);
+                        terms(nb, tb);
+                        momentum_accumulate<T, D>(ta, a);
+                        if (hb) momentum_accumulate<T, D>(tb, a);
+                    }
+                }
+            }
+            } else
+#endif
+            {
             SPH_MOM_WALK<T>(E, i, acnt, loadf, [&](int, const NbrPVR<T>& nb) {
                 T xj[3], vj[3], dx[3], r2, vx;
                 to3<T>(nb.p, xj);
@@ -1074,6 +1157,7 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
                 pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
                 momentum_pair<T, D>(r2, vx, dx, rho_i, pi_rr, nb.rp.x, nb.rp.y, nb.p.w, P, a);
             });
+            }
             vec4<T> A4;
             A4.x = a[0]; A4.y = a[1]; A4.z = D == 3 ? a[2] : T(0); A4.w = T(0);
             E.dvdt[i] = A4;
