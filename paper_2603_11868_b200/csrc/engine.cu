@@ -29,7 +29,7 @@
 #define SPH_SWEEP_MINB 12    // min resident blocks of the sweeps (register cap)
 #endif
 #ifndef SPH_CONT_MINB
-#define SPH_CONT_MINB 12
+#define SPH_CONT_MINB (D == 3 ? 10 : 12)
 #endif
 #ifndef SPH_MOM_MINB
 #define SPH_MOM_MINB 8       // the momentum sweep holds more live state
@@ -39,6 +39,9 @@
 #endif
 #ifndef SPH_SKINW_MINB
 #define SPH_SKINW_MINB 4     // warp-per-cell skin build: blocks per SM (register cap)
+#endif
+#ifndef SPH_CONT_FILTER_QUADS      // continuity: visit accepted entries per list quad
+#define SPH_CONT_FILTER_QUADS (D == 3)   // (measured: 3D -4.5%, 2D +23%)
 #endif
 #ifndef SPH_CONT_ILP
 #define SPH_CONT_ILP 0       // continuity: two accepted pairs per basic block
@@ -208,6 +211,35 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
             }
         }
 #endif
+    }
+}
+
+// Exact filter of slot's skin list quad by quad: the 4 entries' positions
+// are gathered together, tested (0 < r2 < c^2, binary32), and each accepted
+// neighbour is visited right away with the position already in registers
+// (body(j, pos_j)); visits stay in list (= ascending id) order.
+template <class T, int D, class Body>
+__device__ __forceinline__ void filter_quads(const Eng<T>& E, int64_t slot, const T (&xi)[3], T c2,
+                                             int nl, Body body)
+{
+    if (nl <= 0) return;
+    const int4* __restrict__ q4 = reinterpret_cast<const int4*>(E.lists + ell_base(slot));
+    int4 qn = q4[0];
+    for (int u0 = 0; u0 < nl; u0 += 4) {
+        const int4 q = qn;
+        if (u0 + 4 < nl) qn = q4[((u0 >> 2) + 1) * 32];
+        const int jj[4] = {q.x, u0 + 1 < nl ? q.y : -1, u0 + 2 < nl ? q.z : -1,
+                           u0 + 3 < nl ? q.w : -1};
+        vec4<T> pj[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) pj[k] = E.pos[jj[k] >= 0 ? jj[k] : 0];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            T xj[3];
+            to3<T>(pj[k], xj);
+            const T r2 = accept_r2<T, D>(xi, xj);
+            if (jj[k] >= 0 && (r2 < c2) && (r2 > T(0))) body(jj[k], pj[k]);
+        }
     }
 }
 
@@ -976,6 +1008,12 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
             else if (cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, j);
             cnt++;
         };
+        if (SPH_CONT_FILTER_QUADS) {
+            filter_quads<T, D>(E, i, xi, g.c2, E.lcount[i], [&](int j, const vec4<T>& pj) {
+                store(j);
+                pair(cnt, NbrPV<T>{pj, vel[j]});
+            });
+        } else {
 #if SPH_CONT_ILP
         auto term = [&](const NbrPV<T>& nb) {
             T xj[3], vj[3], dx[3], r2, vx;
@@ -1001,6 +1039,7 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
             pair(cnt, nb);
         });
 #endif
+        }
         if ((cnt & 3) && cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, 0);
         if (cnt > kCap) {
             E.acount[i] = -1;
