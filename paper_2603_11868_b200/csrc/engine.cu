@@ -35,7 +35,7 @@
 #define SPH_MOM_MINB 8       // the momentum sweep holds more live state
 #endif
 #ifndef SPH_SKIN_THREADS_PER_SM
-#define SPH_SKIN_THREADS_PER_SM 1536   // skin-list build occupancy (register cap)
+#define SPH_SKIN_THREADS_PER_SM 1024   // skin-list build occupancy (register cap)
 #endif
 #ifndef SPH_SKINW_MINB
 #define SPH_SKINW_MINB 4     // warp-per-cell skin build: blocks per SM (register cap)
