@@ -29,12 +29,33 @@ def test_library_builds_and_exports_every_declared_symbol():
     assert lib.sph_abi_version() == 4
 
 
-def test_struct_layouts_match_header():
+def test_struct_layouts_match_header(tmp_path):
+    """Every ctypes mirror has the C compiler's size and field offsets for
+    the header's structs (gcc on include/sph_b200.h, no GPU needed)."""
+    import subprocess
     from paper_2603_11868_b200 import _native
-    # 14 pointers, 6 reals, 3 int64, 8 reals, int64, 2 int32
-    assert ctypes.sizeof(_native.SphSweepArgs_f32) == 14 * 8 + 6 * 4 + 24 + 8 * 4 + 16
-    assert ctypes.sizeof(_native.SphSweepArgs_f64) == 14 * 8 + 6 * 8 + 24 + 8 * 8 + 16
-    assert ctypes.sizeof(_native.SphStepStats) == 6 * 8 + 6 * 4
+    structs = {"SphSweepArgs_f32": _native.SphSweepArgs_f32,
+               "SphSweepArgs_f64": _native.SphSweepArgs_f64,
+               "SphStepStats": _native.SphStepStats, "SphEngine": _native.SphEngine,
+               "SphHaloPlan": _native.SphHaloPlan}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sph_b200.h"',
+             'int main(void) {']
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} size %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name} {f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                    str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout
+    for line in out.splitlines():
+        name, field, value = line.split()
+        cls = structs[name]
+        got = ctypes.sizeof(cls) if field == "size" else getattr(cls, field).offset
+        assert got == int(value), (name, field)
 
 
 def test_workspace_queries_need_no_gpu():
