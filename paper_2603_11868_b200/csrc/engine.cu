@@ -15,14 +15,19 @@
 // exact list rebuilt for that sub-step (k_fix_build), so the result never
 // depends on the skin choice -- only the speed does.
 //
+// Per advective step: k_skin_warp (2D: a warp per cell) / k_skin_tile (a
+// block per cell) / k_skin_big (oversized blocks) build the skin lists.
 // One acoustic sub-step (physics.py:522-548):
 //   k_kick_drift  KICK + DRIFT, displacement bounds, cell-change marks
+//                 (first sub-step only; later ones come fused in k_mom)
 //   k_mark        queue particles whose skin list is no longer valid
 //   k_fix_build   exact ordered lists for the queued particles
 //   k_cont_du     skin-list filter + CONTINUITY + DENSITY_UPDATE (fluid);
 //                 writes the exact lists the momentum sweep reads
 //   k_wall        skin-list filter + WALL_PRESSURE (walls)
-//   k_mom         MOMENTUM + KICK               (fluid)
+//   k_mom         MOMENTUM + KICK (fluid), + the next sub-step's KICK + DRIFT
+//
+// Tuning knobs below were chosen by measurement.
 #include "engine.cuh"
 
 #ifndef SPH_SWEEP_MINB
@@ -43,20 +48,8 @@
 #ifndef SPH_CONT_FILTER_QUADS      // continuity: visit accepted entries per list quad
 #define SPH_CONT_FILTER_QUADS (D == 3)   // (measured: 3D -4.5%, 2D +23%)
 #endif
-#ifndef SPH_CONT_ILP
-#define SPH_CONT_ILP 0       // continuity: two accepted pairs per basic block
-#endif
 #ifndef SPH_MOM_ILP
 #define SPH_MOM_ILP 1        // momentum: two pairs per basic block (1: in 2D, 2: always)
-#endif
-#ifndef SPH_MOM_WALK
-#define SPH_MOM_WALK sweep_list   // sweep_list_pf (one pair ahead) measured slower
-#endif
-#ifndef SPH_FILTER_KF
-#define SPH_FILTER_KF 4      // list entries in flight per filter trip
-#endif
-#ifndef SPH_PREFETCH
-#define SPH_PREFETCH 0       // prefetch the next neighbour's data in the sweeps
 #endif
 
 namespace sph {
@@ -80,43 +73,6 @@ __device__ __forceinline__ void sweep_list(const Eng<T>& E, int64_t slot, int cn
         if (t0 + 1 < cnt) body(t0 + 1, load(q.y));
         if (t0 + 2 < cnt) body(t0 + 2, load(q.z));
         if (t0 + 3 < cnt) body(t0 + 3, load(q.w));
-    }
-}
-
-// The same walk software-pipelined by one neighbour: the next neighbour's
-// data is requested before the current pair is computed (more registers,
-// more independent work in flight per warp).
-template <class T, class Load, class Body>
-__device__ __forceinline__ void sweep_list_pf(const Eng<T>& E, int64_t slot, int cnt, Load load,
-                                              Body body)
-{
-    if (cnt <= 0) return;
-    const int4* __restrict__ q4 = reinterpret_cast<const int4*>(E.elist + ell_base(slot));
-    int4 q = q4[0];
-    auto cur = load(q.x);
-    for (int t0 = 0; t0 < cnt; t0 += 4) {
-        const int4 qn = (t0 + 4 < cnt) ? q4[((t0 >> 2) + 1) * 32] : q;
-        {
-            const auto nx = load(t0 + 1 < cnt ? q.y : q.x);
-            body(t0, cur);
-            cur = nx;
-        }
-        if (t0 + 1 < cnt) {
-            const auto nx = load(t0 + 2 < cnt ? q.z : q.x);
-            body(t0 + 1, cur);
-            cur = nx;
-        }
-        if (t0 + 2 < cnt) {
-            const auto nx = load(t0 + 3 < cnt ? q.w : q.x);
-            body(t0 + 2, cur);
-            cur = nx;
-        }
-        if (t0 + 3 < cnt) {
-            const auto nx = load(t0 + 4 < cnt ? qn.x : q.x);
-            body(t0 + 3, cur);
-            cur = nx;
-        }
-        q = qn;
     }
 }
 
@@ -146,7 +102,7 @@ template <class T> struct NbrPR { vec4<T> p; vec2<T> rp; };
 // list entries + positions in flight (phase 1, bits in a register), then the
 // accepted neighbours are visited in list (= ascending id) order with the
 // next one's data prefetched (phase 2).  Rejected entries cost only phase 1.
-template <class T, int D, bool PAIRS = false, class Load, class Body>
+template <class T, int D, class Load, class Body>
 __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const T (&xi)[3],
                                             T c2, int nl, Load load, Body body)
 {
@@ -172,45 +128,12 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
             }
         }
         if (!m) continue;
-#if SPH_PREFETCH
-        int u = __ffs(m) - 1;
-        m &= m - 1;
-        int j = lp[ell_off(w0 + u)];
-        auto nxt = load(j);
-        while (true) {
-            const auto cur = nxt;
-            const int jc = j;
-            const bool more = m != 0;
-            if (more) {
-                u = __ffs(m) - 1;
-                m &= m - 1;
-                j = lp[ell_off(w0 + u)];
-                nxt = load(j);
-            }
-            body(jc, cur);
-            if (!more) break;
+        while (m) {
+            const int u = __ffs(m) - 1;
+            m &= m - 1;
+            const int j = lp[ell_off(w0 + u)];
+            body(j, load(j));
         }
-#else
-        if constexpr (PAIRS) {   // two accepted neighbours per call: independent chains
-            while (m) {
-                const int ua = __ffs(m) - 1;
-                m &= m - 1;
-                const bool hb = m != 0;
-                const int ub = hb ? __ffs(m) - 1 : ua;
-                m &= m - 1;
-                const int ja = lp[ell_off(w0 + ua)];
-                const int jb = hb ? lp[ell_off(w0 + ub)] : ja;
-                body(ja, load(ja), jb, load(jb), hb);
-            }
-        } else {
-            while (m) {
-                const int u = __ffs(m) - 1;
-                m &= m - 1;
-                const int j = lp[ell_off(w0 + u)];
-                body(j, load(j));
-            }
-        }
-#endif
     }
 }
 
@@ -1014,31 +937,11 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
                 pair(cnt, NbrPV<T>{pj, vel[j]});
             });
         } else {
-#if SPH_CONT_ILP
-        auto term = [&](const NbrPV<T>& nb) {
-            T xj[3], vj[3], dx[3], r2, vx;
-            to3<T>(nb.p, xj);
-            to3<T>(nb.v, vj);
-            pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-            return continuity_term<T>(r2, vx, nb.v.w, P);
-        };
-        filter_walk<T, D, true>(E, i, xi, g.c2, E.lcount[i], loadf,
-                                [&](int ja, const NbrPV<T>& na, int jb, const NbrPV<T>& nb,
-                                    bool hb) {
-            const double ta = term(na), tb = term(nb);
-            store(ja);
-            acc = dadd(acc, ta);
-            if (hb) {
-                store(jb);
-                acc = dadd(acc, tb);
-            }
-        });
-#else
-        filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf, [&](int j, const NbrPV<T>& nb) {
-            store(j);
-            pair(cnt, nb);
-        });
-#endif
+            filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf,
+                              [&](int j, const NbrPV<T>& nb) {
+                store(j);
+                pair(cnt, nb);
+            });
         }
         if ((cnt & 3) && cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, 0);
         if (cnt > kCap) {
@@ -1189,7 +1092,7 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
             } else
 #endif
             {
-            SPH_MOM_WALK<T>(E, i, acnt, loadf, [&](int, const NbrPVR<T>& nb) {
+            sweep_list<T>(E, i, acnt, loadf, [&](int, const NbrPVR<T>& nb) {
                 T xj[3], vj[3], dx[3], r2, vx;
                 to3<T>(nb.p, xj);
                 to3<T>(nb.v, vj);

@@ -35,7 +35,6 @@ struct WarpBuf;
 constexpr size_t kWarpBufBytes = sizeof(uint32_t) * (2 * kCap + 4);
 constexpr size_t kNlSmem = sizeof(int32_t) * kCap * kStagePitch + kWarpBufBytes * kNlWarps +
                            sizeof(int) * 64;
-constexpr int kMaskWords = kCap / 32;   // 256-bit filter mask per particle
 
 template <class T>
 struct GridP {
@@ -53,11 +52,6 @@ __device__ __forceinline__ int ell_off(int t) { return (t >> 2) * 128 + (t & 3);
 __device__ __forceinline__ size_t ell_index(int64_t slot, int t)
 {
     return ell_base(slot) + (size_t)ell_off(t);
-}
-// filter-mask word w of slot s at [s/32][w][s%32]
-__device__ __forceinline__ size_t mask_index(int64_t slot, int w)
-{
-    return (size_t)(slot >> 5) * (kMaskWords * 32) + (size_t)w * 32 + (size_t)(slot & 31);
 }
 
 // ascending bitonic sort of sb[0..np), np a power of two in [64, 256]
