@@ -158,6 +158,26 @@ int sph_gather(void* dst, const void* src, const int64_t* perm, int64_t n, int e
                cudaStream_t s);
 
 /* ---------------------------------------------------------------------------
+ * Case placement on the device (cases.py:129-161 _lattice, _tank_wall_points,
+ * _box_points; the obstacle cut of build_case_dambreak, cases.py:227-233).
+ * Lattice points anchor[k] + (i_k + 0.5)*dp (binary64) over the index box
+ * lo[k] <= i_k < hi[k] (host arrays of d), kept by mode and compacted in the
+ * lattice's C order (last axis fastest, np.meshgrid(indexing="ij").ravel())
+ * into out (dev, (count, d) binary64; NULL = count only).  *count (dev int64)
+ * receives the number kept; *ilast_max (dev u64, caller-zeroed) the
+ * order-preserving key (i ^ 2^63) of the largest kept last-axis index.
+ * -------------------------------------------------------------------------*/
+#define SPH_LATTICE_ALL 0      /* every point (_lattice, _box_points)                 */
+#define SPH_LATTICE_TANK 1     /* _tank_wall_points' outside test, counts[0..d)       */
+#define SPH_LATTICE_NOT_IN 2   /* not strictly inside the open box (box_lo, box_hi)   */
+size_t sph_lattice_workspace_bytes(int32_t d, const int64_t* lo, const int64_t* hi);
+int sph_lattice_points(int32_t d, const int64_t* lo, const int64_t* hi, double dp,
+                       const double* anchor, int32_t mode, const int64_t* counts,
+                       const double* box_lo, const double* box_hi, double* out,
+                       int64_t* count, unsigned long long* ilast_max, void* ws,
+                       size_t ws_bytes, cudaStream_t s);
+
+/* ---------------------------------------------------------------------------
  * Device-resident step engine: the B200 restatement of Simulation.advance
  * (physics.py:489-552).  Particles live in two segments -- fluid [0, nf),
  * walls [nf, n) -- each ordered by grid cell; the fluid segment is re-sorted

@@ -109,6 +109,7 @@ STATS_NORMS = 2
 PHASE_KICK_DRIFT, PHASE_CONTINUITY, PHASE_WALL, PHASE_MOMENTUM = 0, 1, 2, 3
 PHASE_INIT_WALL, PHASE_INIT_MOMENTUM = 4, 5
 HALO_XV, HALO_RP_NEXT, HALO_RP_CUR = 0, 1, 2
+LATTICE_ALL, LATTICE_TANK, LATTICE_NOT_IN = 0, 1, 2
 
 # name -> (restype, argtypes)
 _P = c_void_p
@@ -149,6 +150,9 @@ _PROTOS = {
     "sph_halo_exchange": (c_i32, [_P, _P, _P, c_i32, c_i32, _P]),
     "sph_engine_substeps_slab": (c_i32, [_P, _P, _P, c_f64, c_f64, c_i32, _P]),
     "sph_engine_unpack": (c_i32, [_P, c_i32, _P, c_i64, _P, _P]),
+    "sph_lattice_workspace_bytes": (c_size, [c_i32, _P, _P]),
+    "sph_lattice_points": (c_i32, [c_i32, _P, _P, c_f64, _P, c_i32, _P, _P, _P, _P,
+                                   _P, _P, _P, c_size, _P]),
 }
 for _sfx, _real in (("f32", c_f32), ("f64", c_f64)):
     for _k in ("continuity", "momentum", "wall_pressure", "density_summation",

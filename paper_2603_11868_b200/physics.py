@@ -550,11 +550,12 @@ class Simulation:
 
     # -- device state ---------------------------------------------------------
 
-    def _alloc(self):
+    def _alloc(self, nf=None):
         reg = self.registry
         if self.grid.dim != reg.dim:
             raise ValueError("grid and registry dimensions differ")
-        nf = int((reg.raw_view("wall") == 0).sum())
+        if nf is None:
+            nf = int((reg.raw_view("wall") == 0).sum())
         n = reg.particle_count
         E, T = engine_alloc(device_of(self.policy), n, nf, n - nf, reg.dim,
                             reg.dtype == np.float64, self.grid,
@@ -566,14 +567,15 @@ class Simulation:
                      "stats_host": torch.empty(T["stats"].shape, dtype=torch.uint8,
                                                pin_memory=True)}
 
-    def _push(self):
+    def _push(self, devs=None, nf=None):
         """Registry -> device SoA (physics layout, cell order)."""
         reg = self.registry
         if self._dev is None:
-            self._alloc()
+            self._alloc(nf)
         d = self._dev
         st = Staging(d["device"])
-        devs = [st.to_dev(reg.raw_view(f)) for f in _ENGINE_FIELDS]
+        if devs is None:
+            devs = [st.to_dev(reg.raw_view(f)) for f in _ENGINE_FIELDS]
         # the id-permutation check and the fluid count run on the device
         for attempt in range(2):
             rc = _native.lib().sph_engine_push(ctypes.byref(d["E"]),
@@ -584,13 +586,33 @@ class Simulation:
                 raise ValueError("registry ids must be a permutation of 0..N-1")
             if stats.fluid_seen == d["E"].nf or attempt:
                 break
-            self._alloc()       # the wall flags changed: resize the list storage
+            self._alloc(int(stats.fluid_seen))   # the wall flags changed: resize
             d = self._dev
         self._oob_walls = stats.oob_walls
         del devs, st
         self._host_dirty = False
         self._host_stale = False
         self._norms = None
+
+    def load_device_state(self, state):
+        """Start from registry-order device tensors (``cases.build_case_device``;
+        the fields of the registry, uint32 ones as int32) instead of the host
+        registry: the engine becomes authoritative and the host registry is
+        filled only when a view is requested."""
+        n = self.registry.particle_count
+        devs = []
+        for f in _ENGINE_FIELDS:
+            t = state[f]
+            shape = self.registry.raw_view(f).shape
+            if tuple(t.shape) != tuple(shape) or not t.is_cuda or not t.is_contiguous():
+                raise TypeError(f"device state field {f!r}: expected a contiguous "
+                                f"CUDA tensor of shape {shape}")
+            devs.append(t)
+        nf = int((state["wall"] == 0).sum().item()) if n else 0
+        if self._dev is not None and self._dev["device"] != devs[0].device:
+            raise TypeError("device state lives on another device")
+        self._push(devs, nf)
+        self._host_stale = True     # the host registry has not seen this state
 
     def _ensure_device(self):
         if self._host_dirty:
