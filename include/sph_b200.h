@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 4
+#define SPH_ABI_VERSION 5
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -239,6 +239,11 @@ typedef struct {
     int32_t drifted;                  /* next sub-step's kick+drift already applied */
     int32_t f64;                      /* 0: f32 run, 1: f64 run */
     int32_t lists_ready;
+    /* periodic box (beyond the reference): per axis the
+     * period L (run precision value; 0 = bounded as in the reference).  A
+     * periodic axis wraps over [origin, origin + L), needs shape >= 3 and
+     * L <= shape * cell_size; only libsphb200_periodic.so accepts L > 0. */
+    double period[3];
 } SphEngine;
 
 size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64);

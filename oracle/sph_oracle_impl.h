@@ -31,6 +31,59 @@ typedef struct {
     R *rho_new;
 } FN(orc_args);
 
+/* ---- periodic boxes: NOT in the reference ---------------
+ * The builder's own extension, restated here so the CUDA periodic build has
+ * a checker (parity of this part is against this restatement only).  Per
+ * axis k: L > 0 makes the axis periodic over [lo, hi) (hi = RN(lo + L),
+ * both run precision, set by the caller).  Pair differences take the
+ * minimum image (dx > L/2: dx - L; dx < -L/2: dx + L; one rounding), the
+ * 3^d block wraps on periodic axes (shape >= 3), and a drift leaving
+ * [lo, hi) re-enters by one +-L.  All zero = the reference's bounded box. */
+static R FN(box_L)[3], FN(box_hL)[3], FN(box_lo)[3], FN(box_hi)[3];
+
+void FN(orc_set_box)(const R *L, const R *lo, const R *hi, int d)
+{
+    for (int k = 0; k < 3; k++) {
+        FN(box_L)[k] = (L && k < d) ? L[k] : (R)0;
+        FN(box_hL)[k] = (R)(FN(box_L)[k] * (R)0.5);
+        FN(box_lo)[k] = (L && k < d) ? lo[k] : (R)0;
+        FN(box_hi)[k] = (L && k < d) ? hi[k] : (R)0;
+    }
+}
+
+static inline R FN(min_image)(R dx, int k)
+{
+    R L = FN(box_L)[k];
+    if (L > (R)0) {
+        if (dx > FN(box_hL)[k]) dx = (R)(dx - L);
+        else if (dx < -FN(box_hL)[k]) dx = (R)(dx + L);
+    }
+    return dx;
+}
+
+static inline R FN(wrap_coord)(R x, int k)
+{
+    R L = FN(box_L)[k];
+    if (L > (R)0) {
+        if (x >= FN(box_hi)[k]) x = (R)(x - L);
+        else if (x < FN(box_lo)[k]) x = (R)(x + L);
+    }
+    return x;
+}
+
+/* the cells of axis k around c: *n of them into a[] (wrapped or clamped) */
+static inline int FN(block_axis)(int64_t c, int64_t s, int k, int64_t *a)
+{
+    if (FN(box_L)[k] > (R)0) {
+        a[0] = c == 0 ? s - 1 : c - 1; a[1] = c; a[2] = c + 1 == s ? 0 : c + 1;
+        return 3;
+    }
+    int n = 0;
+    for (int64_t t = c - 1; t <= c + 1; t++)
+        if (t >= 0 && t < s) a[n++] = t;
+    return n;
+}
+
 /* neighborhood.py:76-84  _cell_coord: floor((x - origin) / cell_size),
  * clamped to [0, ncells-1]; *clamped set on a clamp. */
 static inline int64_t FN(cell_coord)(R x, R origin, R cell_size,
@@ -83,28 +136,29 @@ int FN(orc_collect_neighbors)(int64_t i, const R *pos, int d,
     int cl = 0;
     int64_t cx = FN(cell_coord)(pos[i * d + 0], origin[0], cell_size, shape[0], &cl);
     int64_t cy = FN(cell_coord)(pos[i * d + 1], origin[1], cell_size, shape[1], &cl);
-    int64_t cz = 0, zlo = 0, zhi = 1;
-    if (d == 3) {
+    int64_t cz = 0;
+    if (d == 3)
         cz = FN(cell_coord)(pos[i * d + 2], origin[2], cell_size, shape[2], &cl);
-        zlo = cz - 1 > 0 ? cz - 1 : 0;
-        zhi = cz + 2 < shape[2] ? cz + 2 : shape[2];
-    }
-    int64_t xlo = cx - 1 > 0 ? cx - 1 : 0, xhi = cx + 2 < shape[0] ? cx + 2 : shape[0];
-    int64_t ylo = cy - 1 > 0 ? cy - 1 : 0, yhi = cy + 2 < shape[1] ? cy + 2 : shape[1];
-    for (int64_t ax = xlo; ax < xhi; ax++)
-        for (int64_t ay = ylo; ay < yhi; ay++)
-            for (int64_t az = zlo; az < zhi; az++) {
+    /* the clamped (or, on periodic axes, wrapped) 3^d block */
+    int64_t bx[3], by[3], bz[3] = {0, 0, 0};
+    int nx = FN(block_axis)(cx, shape[0], 0, bx);
+    int ny = FN(block_axis)(cy, shape[1], 1, by);
+    int nz = d == 3 ? FN(block_axis)(cz, shape[2], 2, bz) : 1;
+    for (int tx = 0; tx < nx; tx++)
+        for (int ty = 0; ty < ny; ty++)
+            for (int tz = 0; tz < nz; tz++) {
+                int64_t ax = bx[tx], ay = by[ty], az = bz[tz];
                 int64_t lin = (d == 3) ? (ax * shape[1] + ay) * shape[2] + az
                                        : ax * shape[1] + ay;
                 for (int64_t s = offsets[lin]; s < offsets[lin + 1]; s++) {
                     int64_t j = pids[s];
                     if (j == i) continue;
                     R r2;
-                    R dx = (R)(pos[i * d + 0] - pos[j * d + 0]);
-                    R dy = (R)(pos[i * d + 1] - pos[j * d + 1]);
+                    R dx = FN(min_image)((R)(pos[i * d + 0] - pos[j * d + 0]), 0);
+                    R dy = FN(min_image)((R)(pos[i * d + 1] - pos[j * d + 1]), 1);
                     r2 = (R)((R)(dx * dx) + (R)(dy * dy));
                     if (d == 3) {
-                        R dz = (R)(pos[i * d + 2] - pos[j * d + 2]);
+                        R dz = FN(min_image)((R)(pos[i * d + 2] - pos[j * d + 2]), 2);
                         r2 = (R)(r2 + (R)(dz * dz));
                     }
                     if (r2 < c2 && (double)r2 > 0.0) {
@@ -124,7 +178,7 @@ static inline void FN(pair_geometry)(int64_t i, int64_t j, int d, const R *x,
     R r2 = (R)(x[i * d] - x[i * d]);
     R vx = r2;
     for (int k = 0; k < d; k++) {
-        R dxk = (R)(x[i * d + k] - x[j * d + k]);
+        R dxk = FN(min_image)((R)(x[i * d + k] - x[j * d + k]), k);
         r2 = (R)(r2 + (R)(dxk * dxk));
         vx = (R)(vx + (R)((R)(v[i * d + k] - v[j * d + k]) * dxk));
     }
@@ -220,7 +274,7 @@ static void FN(momentum_one)(const FN(orc_args) *a, int64_t i)
         double f = (double)(R)(-a->m[j]) * pij;
         f = f * fac;
         for (int k = 0; k < d; k++) {
-            R dxk = (R)(a->x[i * d + k] - a->x[j * d + k]);
+            R dxk = FN(min_image)((R)(a->x[i * d + k] - a->x[j * d + k]), k);
             a->dvdt[i * d + k] = (R)((double)a->dvdt[i * d + k] + f * (double)dxk);
         }
     }
@@ -266,7 +320,7 @@ static void FN(density_summation_one)(const FN(orc_args) *a, int64_t i)
         int64_t j = buf[t] & 0xFFFFFFFFLL;
         R r2 = (R)(a->x[i * d] - a->x[i * d]);
         for (int k = 0; k < d; k++) {
-            R dxk = (R)(a->x[i * d + k] - a->x[j * d + k]);
+            R dxk = FN(min_image)((R)(a->x[i * d + k] - a->x[j * d + k]), k);
             r2 = (R)(r2 + (R)(dxk * dxk));
         }
         R r = SQRT(r2);
@@ -295,7 +349,7 @@ static void FN(shepard_one)(const FN(orc_args) *a, int64_t i)
         int64_t j = buf[t] & 0xFFFFFFFFLL;
         R r2 = (R)(a->x[i * d] - a->x[i * d]);
         for (int k = 0; k < d; k++) {
-            R dxk = (R)(a->x[i * d + k] - a->x[j * d + k]);
+            R dxk = FN(min_image)((R)(a->x[i * d + k] - a->x[j * d + k]), k);
             r2 = (R)(r2 + (R)(dxk * dxk));
         }
         R r = SQRT(r2);
@@ -339,7 +393,7 @@ void FN(orc_drift)(int64_t n, int d, R *x, const R *v, const uint32_t *wall,
     for (int64_t i = 0; i < n; i++) {
         if (wall[i] != 0) continue;
         for (int k = 0; k < d; k++)
-            x[i * d + k] = (R)(x[i * d + k] + (R)(dt * v[i * d + k]));
+            x[i * d + k] = FN(wrap_coord)((R)(x[i * d + k] + (R)(dt * v[i * d + k])), k);
     }
 }
 

@@ -99,10 +99,11 @@ class SphEngine(C.Structure):
         ("c0", c_f64), ("rho0", c_f64), ("alpha_visc", c_f64), ("eps_h2", c_f64),
         ("skin", c_f64),
         ("cur_v", c_i32), ("cur_rp", c_i32), ("cur_pos", c_i32), ("drifted", c_i32), ("f64", c_i32), ("lists_ready", c_i32),
+        ("period", c_f64 * 3),
     ]
 
 
-ABI_VERSION = 4   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 5   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)
@@ -172,19 +173,25 @@ for _sfx, _real in (("f32", c_f32), ("f64", c_f64)):
 EXPORTED = tuple(sorted(_PROTOS))
 
 _LIB = None
+_LIB_PERIODIC = None
 
 
-def library_path():
-    """The in-tree library; SPH_B200_LIB overrides it (A/B variant builds)."""
+def library_path(periodic=False):
+    """The in-tree library; SPH_B200_LIB overrides it (A/B variant builds).
+    periodic: the periodic-box build (libsphb200_periodic.so)."""
+    if periodic:
+        return os.environ.get("SPH_B200_LIB_PERIODIC") or _build.LIB_PERIODIC
     return os.environ.get("SPH_B200_LIB") or _build.LIB
 
 
-def load(path=None):
+def load(path=None, periodic=False):
     """Load the shared library and declare prototypes (no GPU needed)."""
-    global _LIB
-    if _LIB is not None and path is None:
-        return _LIB
-    p = path or library_path()
+    global _LIB, _LIB_PERIODIC
+    if path is None:
+        cached = _LIB_PERIODIC if periodic else _LIB
+        if cached is not None:
+            return cached
+    p = path or library_path(periodic)
     if not os.path.exists(p):
         raise NativeUnavailable(
             f"{p} is missing: run `python -m paper_2603_11868_b200.build` "
@@ -197,17 +204,26 @@ def load(path=None):
     if lib.sph_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libsphb200.so ABI version mismatch")
     if path is None:
-        _LIB = lib
+        if periodic:
+            _LIB_PERIODIC = lib
+        else:
+            _LIB = lib
     return lib
 
 
-def lib():
-    return load()
+def lib(periodic=False):
+    return load(periodic=periodic)
 
 
 def last_error():
-    msg = lib().sph_last_error()
-    return msg.decode() if msg else ""
+    """The last error message of the loaded libraries (bounded, periodic)."""
+    msgs = []
+    for L in (_LIB, _LIB_PERIODIC):
+        if L is not None:
+            m = L.sph_last_error()
+            if m:
+                msgs.append(m.decode())
+    return "; ".join(msgs)
 
 
 def check(rc, what):

@@ -21,6 +21,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(OUT_DIR, "libsphb200.so")
+# the same sources with periodic boxes compiled in (common.cuh SPH_PERIODIC)
+LIB_PERIODIC = os.path.join(OUT_DIR, "libsphb200_periodic.so")
+PERIODIC_FLAGS = ("-DSPH_PERIODIC=1",)
 OBJ_DIR = os.path.join(ROOT, "build", "obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -59,7 +62,14 @@ def _stale(target, deps):
 
 
 def build_library(force=False, verbose=False, extra_flags=(), out=None):
-    """Build the library (to `out`, default the in-tree path)."""
+    """Build the library (to `out`, default the in-tree path; the default
+    build also produces the periodic-box variant)."""
+    if out is None and not extra_flags:
+        _build_one(force, verbose, PERIODIC_FLAGS, LIB_PERIODIC)
+    return _build_one(force, verbose, extra_flags, out)
+
+
+def _build_one(force, verbose, extra_flags, out):
     deps = _deps()
     target = out or LIB
     if not force and not _stale(target, deps):

@@ -45,6 +45,72 @@ template <> struct RN<double> {
     static __device__ __forceinline__ double sqrt_ru(double a) { return __dsqrt_ru(a); }
     static constexpr double kOnePlus2Eps = 1.0000000000000004;   // 1 + 2^-51
 };
+// ---- periodic boxes (not in the reference) --------------
+// libsphb200_periodic.so is the same sources built with -DSPH_PERIODIC=1.
+// Per axis k: L[k] > 0 makes the axis periodic with period L[k] over the
+// interval [lo[k], hi[k]) (hi = RN(lo + L)); pair differences take the
+// minimum image (dx > L/2: dx - L, dx < -L/2: dx + L, one binary32/64 op)
+// and a drift leaving [lo, hi) re-enters by one +-L.  All values are the run
+// precision, computed on the host (oracle/sph_oracle_impl.h restates the
+// same operations).  The box lives in constant memory of the translation
+// unit that launches the engine kernels (engine.cu sets it on the caller's
+// stream at every engine entry); the bounded build compiles none of this.
+#ifndef SPH_PERIODIC
+#define SPH_PERIODIC 0
+#endif
+#if SPH_PERIODIC
+struct PerBox {
+    float Lf[3], hLf[3], lof[3], hif[3];
+    double Ld[3], hLd[3], lod[3], hid[3];
+};
+static __constant__ PerBox c_box;
+template <class T> struct BoxOf;
+template <> struct BoxOf<float> {
+    static __device__ __forceinline__ float L(int k) { return c_box.Lf[k]; }
+    static __device__ __forceinline__ float hL(int k) { return c_box.hLf[k]; }
+    static __device__ __forceinline__ float lo(int k) { return c_box.lof[k]; }
+    static __device__ __forceinline__ float hi(int k) { return c_box.hif[k]; }
+};
+template <> struct BoxOf<double> {
+    static __device__ __forceinline__ double L(int k) { return c_box.Ld[k]; }
+    static __device__ __forceinline__ double hL(int k) { return c_box.hLd[k]; }
+    static __device__ __forceinline__ double lo(int k) { return c_box.lod[k]; }
+    static __device__ __forceinline__ double hi(int k) { return c_box.hid[k]; }
+};
+#endif
+
+// minimum image of a pair difference along axis k (identity when bounded)
+template <class T>
+__device__ __forceinline__ T min_image(T dx, int k)
+{
+#if SPH_PERIODIC
+    const T L = BoxOf<T>::L(k), hL = BoxOf<T>::hL(k);
+    if (L > T(0)) {
+        if (dx > hL) dx = RN<T>::sub(dx, L);
+        else if (dx < -hL) dx = RN<T>::add(dx, L);
+    }
+#else
+    (void)k;
+#endif
+    return dx;
+}
+
+// a drifted coordinate back into the periodic interval (identity when bounded)
+template <class T>
+__device__ __forceinline__ T wrap_coord(T x, int k)
+{
+#if SPH_PERIODIC
+    const T L = BoxOf<T>::L(k);
+    if (L > T(0)) {
+        if (x >= BoxOf<T>::hi(k)) x = RN<T>::sub(x, L);
+        else if (x < BoxOf<T>::lo(k)) x = RN<T>::add(x, L);
+    }
+#else
+    (void)k;
+#endif
+    return x;
+}
+
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }

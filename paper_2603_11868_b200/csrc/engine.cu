@@ -302,6 +302,11 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
             cc[0] = (int)(c / g.s[1]);
             cc[2] = 0;
         }
+#if SPH_PERIODIC
+        const PerBlock pb = per_block<T, D>(g, cc);
+        const int rps = per_runs(pb);
+        const int nruns = acc.nsegs() * rps;
+#else
         const int xlo = max(cc[0] - 1, 0), xhi = min(cc[0] + 1, g.s[0] - 1);
         const int ylo = max(cc[1] - 1, 0), yhi = min(cc[1] + 1, g.s[1] - 1);
         const int zlo = D == 3 ? max(cc[2] - 1, 0) : 0;
@@ -309,12 +314,16 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         const int nyr = D == 3 ? (yhi - ylo + 1) : 1;
         const int rps = (xhi - xlo + 1) * nyr;
         const int nruns = 2 * rps;
+#endif
         if (warp == 0) {   // run bounds of both segments + exclusive prefix
             int64_t s0 = 0, s1 = 0;
             if ((int)lane < nruns) {
                 const int seg = (int)lane / rps, rr = (int)lane - seg * rps;
-                const int ax = xlo + rr / nyr, ay = ylo + rr % nyr;
                 uint32_t klo, khi;
+#if SPH_PERIODIC
+                per_run<T, D>(g, pb, rr, klo, khi);
+#else
+                const int ax = xlo + rr / nyr, ay = ylo + rr % nyr;
                 if (D == 3) {
                     const uint32_t rowk = ((uint32_t)ax * g.s[1] + ay) * g.s[2];
                     klo = rowk + zlo;
@@ -323,6 +332,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                     klo = (uint32_t)ax * g.s[1] + ylo;
                     khi = (uint32_t)ax * g.s[1] + yhi;
                 }
+#endif
                 acc.run(seg, klo, khi, s0, s1);
             }
             const uint32_t len = (uint32_t)(s1 - s0);
@@ -558,6 +568,11 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
             cc[0] = (int)(c / g.s[1]);
             cc[2] = 0;
         }
+#if SPH_PERIODIC
+        const PerBlock pb = per_block<T, D>(g, cc);
+        const int rps = per_runs(pb);
+        const int nruns = (E.nw > 0 ? 2 : 1) * rps;
+#else
         const int xlo = max(cc[0] - 1, 0), xhi = min(cc[0] + 1, g.s[0] - 1);
         const int ylo = max(cc[1] - 1, 0), yhi = min(cc[1] + 1, g.s[1] - 1);
         const int zlo = D == 3 ? max(cc[2] - 1, 0) : 0;
@@ -565,11 +580,15 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
         const int nyr = D == 3 ? (yhi - ylo + 1) : 1;
         const int rps = (xhi - xlo + 1) * nyr;
         const int nruns = 2 * rps;
+#endif
         int64_t s0 = 0, s1 = 0;
         if ((int)lane < nruns) {
             const int seg = (int)lane / rps, rr = (int)lane - seg * rps;
-            const int ax = xlo + rr / nyr, ay = ylo + rr % nyr;
             uint32_t klo, khi;
+#if SPH_PERIODIC
+            per_run<T, D>(g, pb, rr, klo, khi);
+#else
+            const int ax = xlo + rr / nyr, ay = ylo + rr % nyr;
             if (D == 3) {
                 const uint32_t rowk = ((uint32_t)ax * g.s[1] + ay) * g.s[2];
                 klo = rowk + zlo;
@@ -578,6 +597,7 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
                 klo = (uint32_t)ax * g.s[1] + ylo;
                 khi = (uint32_t)ax * g.s[1] + yhi;
             }
+#endif
             if (seg == 0) { s0 = E.offs_f[klo]; s1 = E.offs_f[khi + 1]; }
             else { s0 = nf + E.offs_w[klo]; s1 = nf + E.offs_w[khi + 1]; }
         }
@@ -727,11 +747,26 @@ __device__ __forceinline__ void kick_drift_one(vec4<T>& P4, vec4<T>& V4, const v
     if (D == 3) P4.z = RN<T>::add(P4.z, RN<T>::mul(full, V4.z));
 }
 
+// a drifted position back into the periodic box (no-op when bounded)
+template <class T, int D>
+__device__ __forceinline__ void wrap_position(vec4<T>& P4)
+{
+#if SPH_PERIODIC
+    P4.x = wrap_coord<T>(P4.x, 0);
+    P4.y = wrap_coord<T>(P4.y, 1);
+    if (D == 3) P4.z = wrap_coord<T>(P4.z, 2);
+#else
+    (void)P4;
+#endif
+}
+
 // skin-list bookkeeping of a drift xo -> xn: the path length bound (upward
-// rounded |xn - xo| added to disp) and the list-cell check; returns the bound
+// rounded |xn - xo| added to disp; xn unwrapped) and the list-cell check of
+// the position xc (xn, wrapped into a periodic box); returns the bound
 template <class T, int D>
 __device__ __forceinline__ T drift_bookkeeping(const Eng<T>& E, const GridP<T>& g, int64_t i,
-                                               const T (&xo)[3], const T (&xn)[3])
+                                               const T (&xo)[3], const T (&xn)[3],
+                                               const T (&xc)[3])
 {
     T s2 = T(0);
 #pragma unroll
@@ -742,7 +777,7 @@ __device__ __forceinline__ T drift_bookkeeping(const Eng<T>& E, const GridP<T>& 
     const T dnew = RN<T>::add_ru(E.disp[i], RN<T>::sqrt_ru(s2));
     E.disp[i] = dnew;
     int c[3];
-    if (cell_key_of<T, D>(xn, g, c) != E.cell0[i]) E.cell0[i] = kInvalidCell;
+    if (cell_key_of<T, D>(xc, g, c) != E.cell0[i]) E.cell0[i] = kInvalidCell;
     return dnew;
 }
 
@@ -766,10 +801,12 @@ k_kick_drift(Eng<T> E, int cv, int crp, GridP<T> g, T half, T full)
         V4.w = RN<T>::div(P4.w, E.rp[crp][i].x);
         const T xo[3] = {P4.x, P4.y, P4.z};
         kick_drift_one<T, D>(P4, V4, A4, half, full);
+        const T xn[3] = {P4.x, P4.y, P4.z};
+        wrap_position<T, D>(P4);
         E.vel[cv][i] = V4;
         E.pos[i] = P4;
-        const T xn[3] = {P4.x, P4.y, P4.z};
-        dnew = drift_bookkeeping<T, D>(E, g, i, xo, xn);
+        const T xc[3] = {P4.x, P4.y, P4.z};
+        dnew = drift_bookkeeping<T, D>(E, g, i, xo, xn, xc);
     }
     const unsigned long long b = warp_max_u64(dbits(double(dnew)));
     if (lane_id() == 0 && b) atomicMax(&E.stats->dmax_bits, b);
@@ -1114,9 +1151,11 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
                     const T xo[3] = {P4.x, P4.y, P4.z};
                     kick_drift_one<T, D>(P4, V4, A4, half, full);
                     V4.w = RN<T>::div(P4.w, rho_i);   // rho after this sub-step's DU
-                    E.pos_next[i] = P4;
                     const T xn[3] = {P4.x, P4.y, P4.z};
-                    dnew = drift_bookkeeping<T, D>(E, g, i, xo, xn);
+                    wrap_position<T, D>(P4);
+                    E.pos_next[i] = P4;
+                    const T xc[3] = {P4.x, P4.y, P4.z};
+                    dnew = drift_bookkeeping<T, D>(E, g, i, xo, xn, xc);
                 }
                 E.vel[cv ^ 1][i] = V4;
             }
@@ -1239,7 +1278,7 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
 
 extern "C" int sph_engine_build_lists(SphEngine* e, double skin, cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc) return rc;
     return SPH_DISPATCH(e, build_lists_impl, e, skin, s);
 }
@@ -1342,7 +1381,7 @@ static int initialize_impl(SphEngine* e, cudaStream_t s)
 
 extern "C" int sph_engine_initialize(SphEngine* e, cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc || (rc = require_lists(e))) return rc;
     return SPH_DISPATCH(e, initialize_impl, e, s);
 }
@@ -1362,7 +1401,7 @@ static int shepard_impl(SphEngine* e, cudaStream_t s)
 
 extern "C" int sph_engine_shepard(SphEngine* e, cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc || (rc = require_lists(e))) return rc;
     return SPH_DISPATCH(e, shepard_impl, e, s);
 }
@@ -1457,7 +1496,7 @@ static int substep_impl(SphEngine* e, double half_d, double full_d, cudaEvent_t*
 
 extern "C" int sph_engine_substep(SphEngine* e, double half_dt, double full_dt, cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc || (rc = require_lists(e))) return rc;
     return SPH_DISPATCH(e, substep_impl, e, half_dt, full_dt, (cudaEvent_t*)nullptr, s);
 }
@@ -1465,7 +1504,7 @@ extern "C" int sph_engine_substep(SphEngine* e, double half_dt, double full_dt, 
 extern "C" int sph_engine_substep_timed(SphEngine* e, double half_dt, double full_dt,
                                         float* ms_out, cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc || (rc = require_lists(e))) return rc;
     cudaEvent_t ev[6];
     for (int k = 0; k < 6; k++) cudaEventCreate(&ev[k]);
@@ -1508,7 +1547,7 @@ static int substeps_impl(SphEngine* e, double half_d, double full_d, int nsub, f
 extern "C" int sph_engine_substeps(SphEngine* e, double half_dt, double full_dt, int32_t nsub,
                                    cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc || (rc = require_lists(e))) return rc;
     if (nsub < 0 || e->drifted) return SPH_ERR_INVALID;
     return SPH_DISPATCH(e, substeps_impl, e, half_dt, full_dt, (int)nsub, (float*)nullptr, s);
@@ -1517,7 +1556,7 @@ extern "C" int sph_engine_substeps(SphEngine* e, double half_dt, double full_dt,
 extern "C" int sph_engine_substeps_timed(SphEngine* e, double half_dt, double full_dt,
                                          int32_t nsub, float* ms_out, cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc || (rc = require_lists(e))) return rc;
     if (nsub < 0 || e->drifted) return SPH_ERR_INVALID;
     return SPH_DISPATCH(e, substeps_impl, e, half_dt, full_dt, (int)nsub, ms_out, s);
@@ -1545,7 +1584,7 @@ static int phase_impl(SphEngine* e, int phase, double half_d, double full_d, cud
 extern "C" int sph_engine_phase(SphEngine* e, int32_t phase, double half_dt, double full_dt,
                                 cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc || (rc = require_lists(e))) return rc;
     return SPH_DISPATCH(e, phase_impl, e, phase, half_dt, full_dt, s);
 }
@@ -1641,7 +1680,7 @@ static int unpack_impl(SphEngine* e, int kind, const int32_t* phys, int64_t coun
 extern "C" int sph_engine_pack(const SphEngine* e, int32_t kind, const int32_t* phys,
                                int64_t count, void* out, cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc) return rc;
     if (sph_engine_halo_width(kind) < 0 || count < 0) return SPH_ERR_INVALID;
     return SPH_DISPATCH(e, pack_impl, e, kind, phys, count, out, s);
@@ -1650,7 +1689,7 @@ extern "C" int sph_engine_pack(const SphEngine* e, int32_t kind, const int32_t* 
 extern "C" int sph_engine_unpack(SphEngine* e, int32_t kind, const int32_t* phys, int64_t count,
                                  const void* in, cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = engine_begin(e, s);
     if (rc) return rc;
     if (sph_engine_halo_width(kind) < 0 || count < 0) return SPH_ERR_INVALID;
     return SPH_DISPATCH(e, unpack_impl, e, kind, phys, count, in, s);

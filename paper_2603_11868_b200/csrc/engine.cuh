@@ -95,6 +95,9 @@ inline EngAcc<T> acc_of_engine(const SphEngine* e)
     acc.offs_f = e->offs_f;
     acc.offs_w = e->offs_w;
     acc.nf = e->nf;
+#if SPH_PERIODIC
+    acc.segs = e->n > e->nf ? 2 : 1;
+#endif
     return acc;
 }
 
@@ -132,6 +135,64 @@ inline int engine_validate(const SphEngine* e)
         set_error("engine: grid or particle count too large for 32-bit keys");
         return SPH_ERR_UNSUPPORTED;
     }
+    bool periodic = false, last_periodic = false;
+    for (int k = 0; k < e->dim; k++) {
+        if (!(e->period[k] >= 0.0)) return SPH_ERR_INVALID;
+        if (e->period[k] > 0.0) {
+            periodic = true;
+            last_periodic = k == e->dim - 1;
+            // the cells must tile the period: the last one reaches the period
+            // end and is at least a cutoff wide (wrap-around blocks are exact)
+            const double L = e->period[k], s = (double)e->shape[k];
+            if (e->shape[k] < 3 || L > s * e->cell_size * (1.0 + 1e-12) ||
+                L < (s - 1.0) * e->cell_size + e->cutoff) {
+                set_error("engine: a periodic axis needs >= 3 cells tiling the period");
+                return SPH_ERR_INVALID;
+            }
+        }
+    }
+#if SPH_PERIODIC
+    // wall-free periodic boxes only (the tested configuration; a warp also
+    // enumerates at most 18 key runs per block, engine.cu k_skin_tile)
+    (void)last_periodic;
+    if (periodic && e->n > e->nf) {
+        set_error("engine: periodic boxes are supported for wall-free cases");
+        return SPH_ERR_UNSUPPORTED;
+    }
+#else
+    (void)last_periodic;
+    if (periodic) {
+        set_error("engine: periodic boxes need libsphb200_periodic.so");
+        return SPH_ERR_UNSUPPORTED;
+    }
+#endif
+    return SPH_OK;
+}
+
+// validation + the periodic box of this translation unit's kernels, set on
+// the caller's stream (engine.cu entry points)
+inline int engine_begin(const SphEngine* e, cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc) return rc;
+#if SPH_PERIODIC
+    PerBox b;
+    for (int k = 0; k < 3; k++) {
+        const bool p = k < e->dim && e->period[k] > 0.0;
+        // run-precision values: lo = origin, hi = RN(lo + L), L/2 exact
+        const float lf = p ? (float)e->period[k] : 0.f, of = p ? (float)e->origin[k] : 0.f;
+        const double ld = p ? e->period[k] : 0.0, od = p ? e->origin[k] : 0.0;
+        volatile float hf = of + lf;
+        volatile double hd = od + ld;
+        b.Lf[k] = lf; b.hLf[k] = lf * 0.5f; b.lof[k] = of; b.hif[k] = hf;
+        b.Ld[k] = ld; b.hLd[k] = ld * 0.5; b.lod[k] = od; b.hid[k] = hd;
+    }
+    if (cudaMemcpyToSymbolAsync(c_box, &b, sizeof(b), 0, cudaMemcpyHostToDevice, s) !=
+        cudaSuccess)
+        return check_launch("engine periodic box");
+#else
+    (void)s;
+#endif
     return SPH_OK;
 }
 

@@ -41,6 +41,79 @@ struct GridP {
     T o[3]; T cs; T c2; int s[3];
 };
 
+#if SPH_PERIODIC
+// The 3^d block of cell cc with periodic axes wrapped: a
+// periodic column axis (all but the last) contributes cc-1, cc, cc+1 mod s;
+// along the last axis each column is one key run [zlo, zhi] plus, at a
+// periodic edge, a one-cell run zw on the far side.  Periodic axes have
+// s >= 3 (no cell repeats); bounded axes clamp like neighborhood.py:188-196.
+struct PerBlock {
+    int ax0, ax1, ax2, ay0, ay1, ay2;
+    int nx, ny, nz, zlo, zhi, zw;
+};
+__device__ __forceinline__ int pick3(int a, int b, int c, int i)
+{
+    return i == 0 ? a : (i == 1 ? b : c);
+}
+template <class T>
+__device__ __forceinline__ void per_axis(int c, int s, bool periodic, int& n, int& a0, int& a1,
+                                         int& a2)
+{
+    if (periodic) {
+        n = 3;
+        a0 = c == 0 ? s - 1 : c - 1;
+        a1 = c;
+        a2 = c + 1 == s ? 0 : c + 1;
+    } else {
+        const int lo = max(c - 1, 0), hi = min(c + 1, s - 1);
+        n = hi - lo + 1;
+        a0 = lo; a1 = lo + 1; a2 = lo + 2;
+    }
+}
+template <class T, int D>
+__device__ __forceinline__ PerBlock per_block(const GridP<T>& g, const int (&cc)[3])
+{
+    PerBlock b;
+    per_axis<T>(cc[0], g.s[0], BoxOf<T>::L(0) > T(0), b.nx, b.ax0, b.ax1, b.ax2);
+    if (D == 3) per_axis<T>(cc[1], g.s[1], BoxOf<T>::L(1) > T(0), b.ny, b.ay0, b.ay1, b.ay2);
+    else { b.ny = 1; b.ay0 = b.ay1 = b.ay2 = 0; }
+    constexpr int r = D - 1;
+    const int s = g.s[r];
+    int lo = cc[r] - 1, hi = cc[r] + 1;
+    b.nz = 1;
+    b.zw = 0;
+    if (BoxOf<T>::L(r) > T(0)) {
+        if (lo < 0) { b.nz = 2; b.zw = s - 1; lo = 0; }
+        else if (hi > s - 1) { b.nz = 2; b.zw = 0; hi = s - 1; }
+    } else {
+        lo = max(lo, 0);
+        hi = min(hi, s - 1);
+    }
+    b.zlo = lo;
+    b.zhi = hi;
+    return b;
+}
+__device__ __forceinline__ int per_runs(const PerBlock& b) { return b.nx * b.ny * b.nz; }
+// run rr in [0, per_runs(b)) -> inclusive key range [klo, khi]
+template <class T, int D>
+__device__ __forceinline__ void per_run(const GridP<T>& g, const PerBlock& b, int rr,
+                                        uint32_t& klo, uint32_t& khi)
+{
+    const int col = rr / b.nz, z = rr - col * b.nz;
+    const int cx = col / b.ny, cy = col - cx * b.ny;
+    const int ax = pick3(b.ax0, b.ax1, b.ax2, cx), ay = pick3(b.ay0, b.ay1, b.ay2, cy);
+    const int zl = z ? b.zw : b.zlo, zh = z ? b.zw : b.zhi;
+    if (D == 3) {
+        const uint32_t rowk = ((uint32_t)ax * g.s[1] + ay) * g.s[2];
+        klo = rowk + zl;
+        khi = rowk + zh;
+    } else {
+        klo = (uint32_t)ax * g.s[1] + zl;
+        khi = (uint32_t)ax * g.s[1] + zh;
+    }
+}
+#endif
+
 // Quad tile-ELL: a 32-particle tile stores entry t of particle (lane) s at
 // [s/32][t/4][s%32][t%4], so one int4 load per lane fetches 4 consecutive
 // entries and a warp's int4 loads cover one contiguous 512-byte block.
@@ -220,6 +293,12 @@ struct EngAcc {
     const uint32_t* __restrict__ offs_f;
     const uint32_t* __restrict__ offs_w;
     int64_t nf;
+#if SPH_PERIODIC
+    int segs;   // 1 when there are no walls (keeps periodic blocks within a warp's runs)
+    __device__ __forceinline__ int nsegs() const { return segs; }
+#else
+    __device__ __forceinline__ static constexpr int nsegs() { return kSegs; }
+#endif
     __device__ __forceinline__ void position(int64_t j, T (&x)[3]) const
     {
         vec4<T> p = pos[j];
@@ -243,6 +322,7 @@ struct GenAcc {
     const uint32_t* __restrict__ id;
     const int64_t* __restrict__ offsets;
     const int64_t* __restrict__ pids;
+    __device__ __forceinline__ static constexpr int nsegs() { return kSegs; }
     __device__ __forceinline__ void position(int64_t j, T (&p)[3]) const
     {
         p[0] = x[j * D + 0]; p[1] = x[j * D + 1]; p[2] = D == 3 ? x[j * D + 2] : T(0);
@@ -289,21 +369,29 @@ __device__ __forceinline__ CollectCounts warp_collect(const Acc& acc, const Grid
     const unsigned lt = lanemask_lt();
     int c[3];
     cell_key_of<T, D>(xi, g, c);
+#if SPH_PERIODIC
+    const PerBlock pb = per_block<T, D>(g, c);
+    const int runs_per_seg = per_runs(pb);
+#else
     const int xlo = max(c[0] - 1, 0), xhi = min(c[0] + 1, g.s[0] - 1);
     const int ylo = max(c[1] - 1, 0), yhi = min(c[1] + 1, g.s[1] - 1);
     const int zlo = D == 3 ? max(c[2] - 1, 0) : 0, zhi = D == 3 ? min(c[2] + 1, g.s[2] - 1) : 0;
     const int nxr = xhi - xlo + 1;
     const int nyr = D == 3 ? (yhi - ylo + 1) : 1;
     const int runs_per_seg = nxr * nyr;
-    const int nruns = runs_per_seg * Acc::kSegs;
+#endif
+    const int nruns = runs_per_seg * acc.nsegs();
     // lane r < nruns owns run r: (seg, ax, ay) -> candidate range [s0, s1)
     int64_t s0 = 0, s1 = 0;
     int seg = 0;
     if ((int)lane < nruns) {
         seg = (int)lane / runs_per_seg;
         const int rr = (int)lane - seg * runs_per_seg;
-        const int ax = xlo + rr / nyr, ay = ylo + rr % nyr;
         uint32_t klo, khi;
+#if SPH_PERIODIC
+        per_run<T, D>(g, pb, rr, klo, khi);
+#else
+        const int ax = xlo + rr / nyr, ay = ylo + rr % nyr;
         if (D == 3) {
             const uint32_t rowk = ((uint32_t)ax * g.s[1] + ay) * g.s[2];
             klo = rowk + zlo;
@@ -312,6 +400,7 @@ __device__ __forceinline__ CollectCounts warp_collect(const Acc& acc, const Grid
             klo = (uint32_t)ax * g.s[1] + ylo;
             khi = (uint32_t)ax * g.s[1] + yhi;
         }
+#endif
         acc.run(seg, klo, khi, s0, s1);
     }
     // flatten: exclusive prefix of run lengths

@@ -34,6 +34,9 @@ class UniformGrid:
     origin: np.ndarray
     cell_size: float
     shape: tuple
+    # periodic box (not in the reference): per-axis period,
+    # 0 = bounded.  None: the reference's bounded grid.
+    period: tuple = None
 
     @property
     def dim(self):

@@ -464,7 +464,16 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
     E.cell_size, E.cutoff, E.h, E.alpha_d = float(cs), float(cutoff), float(h), float(alpha_d)
     E.c0, E.rho0, E.alpha_visc, E.eps_h2 = float(c0), float(rho0), float(avisc), float(eps_h2)
     E.f64 = int(f64)
+    per = getattr(grid, "period", None)
+    for k in range(3):   # periodic box (run-precision periods; 0 = bounded)
+        E.period[k] = float((np.float64 if f64 else np.float32)(per[k])) \
+            if per is not None and k < d else 0.0
     return E, T
+
+
+def grid_is_periodic(grid):
+    per = getattr(grid, "period", None)
+    return per is not None and any(float(p) > 0.0 for p in per)
 
 
 def engine_set_counts(E, n, nf):
@@ -511,6 +520,10 @@ class Simulation:
         self.last_nfix = 0
         registry.attach_engine(self)
 
+    def _lib(self):
+        """libsphb200.so, or its periodic-box build for a periodic grid."""
+        return _native.lib(periodic=grid_is_periodic(self.grid))
+
     # -- registry coupling ----------------------------------------------------
 
     def host_modified(self):
@@ -530,7 +543,7 @@ class Simulation:
             host = reg.raw_view(f)
             tdt = torch.int32 if host.dtype == np.uint32 else d["tdtype"]
             outs[f] = torch.empty(host.shape, dtype=tdt, device=d["device"])
-        rc = _native.lib().sph_engine_pull(
+        rc = self._lib().sph_engine_pull(
             ctypes.byref(d["E"]), *[ptr(outs[f]) for f in _ENGINE_FIELDS],
             d["stream"])
         _native.check(rc, "engine_pull")
@@ -578,7 +591,7 @@ class Simulation:
             devs = [st.to_dev(reg.raw_view(f)) for f in _ENGINE_FIELDS]
         # the id-permutation check and the fluid count run on the device
         for attempt in range(2):
-            rc = _native.lib().sph_engine_push(ctypes.byref(d["E"]),
+            rc = self._lib().sph_engine_push(ctypes.byref(d["E"]),
                                                *[ptr(t) for t in devs], d["stream"])
             _native.check(rc, "engine_push")
             stats = self._read_stats()
@@ -620,7 +633,7 @@ class Simulation:
 
     def _call(self, name, *args):
         d = self._dev
-        rc = getattr(_native.lib(), name)(ctypes.byref(d["E"]), *args, d["stream"])
+        rc = getattr(self._lib(), name)(ctypes.byref(d["E"]), *args, d["stream"])
         _native.check(rc, name)
 
     def _read_stats(self):
@@ -692,7 +705,7 @@ class Simulation:
         """One advective step (physics.py:489-552); returns the dt taken."""
         self._ensure_device()
         d = self._dev
-        L = _native.lib()
+        L = self._lib()
         if self.sort_every and self.step_count > 0 \
                 and self.step_count % self.sort_every == 0:
             t0 = time.perf_counter()
@@ -783,7 +796,7 @@ class Simulation:
         if "probe" not in d or d["probe"].shape[0] < cap * 7:
             d["probe"] = torch.empty(cap * 7, dtype=torch.float64, device=d["device"])
             d["probe_n"] = torch.zeros(1, dtype=torch.int32, device=d["device"])
-        rc = _native.lib().sph_engine_probe(
+        rc = self._lib().sph_engine_probe(
             ctypes.byref(d["E"]), loc.ctypes.data_as(ctypes.c_void_p),
             ctypes.c_double(reach * (1.0 + 1e-9) + 1e-300), ptr(d["probe"]), cap,
             ptr(d["probe_n"]), d["stream"])
