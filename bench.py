@@ -39,6 +39,11 @@ CONFIGS = {
              dict(kind="3d", dp=0.00608)),
     "3d16m": ("config 4: 3D Kleefsman dam break at 16M, dp=0.00371 (N=16,005,253)",
               dict(kind="3d", dp=0.00371)),
+    # config 5's per-GPU share (64M on 8 GPUs): not constructible in the
+    # reference (no periodic boundaries); SURVEY.md 8f f4
+    "tg8m": ("config 5 per GPU: 3D periodic Taylor-Green vortex, 200^3 = 8M particles "
+             "(libsphb200_periodic.so; beyond the reference, parity vs the oracle's "
+             "periodic restatement)", dict(kind="tg", n=200)),
 }
 METRIC = "particle-updates/sec (full time step)"
 UNIT = "particle-updates/s"
@@ -63,11 +68,19 @@ def emit(line):
 def build_case(name):
     from paper_2603_11868_b200 import cases
     spec = CONFIGS[name][1]
+    if spec["kind"] == "tg":
+        return cases.build_case(cases.taylor_green_config(3, spec["n"], precision="f32"))
     if spec["kind"] == "2d":
         cfg = cases.CaseConfig(case="dambreak2d", dp=spec["dp"], precision="f32")
     else:
         cfg = cases.kleefsman_config(dp=spec["dp"], precision="f32")
     return cases.build_case(cfg)
+
+
+def data_label(name):
+    if CONFIGS[name][1]["kind"] == "tg":
+        return "synthetic (periodic Taylor-Green lattice, analytic initial field)"
+    return "synthetic (reference lattice dam break, deterministic)"
 
 
 def measured_peaks():
@@ -205,7 +218,7 @@ def reference_arm(args, rank, world):
         "n_gpus": world, "steps": done, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / done, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (mixed f64)",
-        "data": "synthetic (reference lattice dam break)",
+        "data": data_label(args.config),
         "config": {"workload": CONFIGS[args.config][0], "case": args.config},
         "cpu_baseline": {
             "value": pus, "unit": UNIT, "cores": thr, "kind": "port",
@@ -229,8 +242,9 @@ def gpu_arm(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    lib = _native.lib()
+    from paper_2603_11868_b200.physics import grid_is_periodic
     reg, grid = build_case(args.config)
+    lib = _native.lib(periodic=grid_is_periodic(grid))
     n = reg.particle_count
     d = reg.dim
     nw = int((reg.raw_view("wall") != 0).sum())
@@ -320,7 +334,7 @@ def gpu_arm(args, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (mixed f64)",
-        "data": "synthetic (reference lattice dam break, deterministic)",
+        "data": data_label(args.config),
         "config": {"workload": CONFIGS[args.config][0], "case": args.config,
                    "particles": n, "fluid": nf, "wall": nw, "grid_cells": ncells,
                    "nsub_per_step": nsubs, "l2": "flushed between steps (256 MB write)",
@@ -538,7 +552,13 @@ def main():
             os.environ.setdefault(k, v)
         torch.distributed.init_process_group(os.environ.get("SPH_BENCH_BACKEND", "nccl"))
     try:
-        if world > 1 or args.slab:
+        if (world > 1 or args.slab) and CONFIGS[args.config][1]["kind"] == "tg":
+            if rank == 0:
+                emit({"metric": METRIC, "unit": UNIT, "n_gpus": world,
+                      "config": {"workload": CONFIGS[args.config][0]},
+                      "unavailable": "periodic boxes run on one GPU; the slab "
+                                     "decomposition has no wrap-around halos yet"})
+        elif world > 1 or args.slab:
             slab_arm(args, rank, world, local_rank)
         else:
             gpu_arm(args, rank, world, local_rank)

@@ -39,6 +39,9 @@
 #ifndef SPH_MOM_MINB
 #define SPH_MOM_MINB 8       // the momentum sweep holds more live state
 #endif
+#ifndef SPH_MASK_MINB
+#define SPH_MASK_MINB 12     // k_mask (split filtering): quad prefetch + staged stores
+#endif
 #ifndef SPH_SKIN_THREADS_PER_SM
 #define SPH_SKIN_THREADS_PER_SM 1024   // skin-list build occupancy (register cap)
 #endif
@@ -815,7 +818,7 @@ k_kick_drift(Eng<T> E, int cv, int crp, GridP<T> g, T half, T full)
 // exact filter of every valid skin list on current positions -> exact lists and
 // accepted counts; particles whose list is not valid go to the fix queue
 template <class T, int D>
-__global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
+__global__ void __launch_bounds__(kSweepThreads, SPH_MASK_MINB)
 k_mask(Eng<T> E, GridP<T> g, T s_eff)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -930,7 +933,7 @@ __device__ __forceinline__ void flag_overflow(const Eng<T>& E, int64_t i)
 // the momentum sweep reuses); others read the exact list k_fix_build made.
 template <class T, int D>
 __global__ void __launch_bounds__(kSweepThreads, SPH_CONT_MINB)
-k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
+k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full, int exact)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= E.nf) return;
@@ -951,7 +954,7 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
         acc = dadd(acc, continuity_term<T>(r2, vx, nb.v.w, P));   // v.w = m_j/rho_j
     };
     int cnt;
-    if (E.cell0[i] == kInvalidCell) {
+    if (exact || E.cell0[i] == kInvalidCell) {   // exact list from k_mask / k_fix_build
         cnt = E.acount[i];
         if (cnt < 0) { flag_overflow(E, i); return; }
         sweep_list<T>(E, i, cnt, loadf, pair);
@@ -1308,6 +1311,20 @@ static void prepare_lists(const SphEngine* e, cudaStream_t s)
     launch_fix<T, D>(e, s);
 }
 
+// Split filtering: with a wide skin (fast flows; e.g. the periodic
+// Taylor-Green case keeps ~1.6x more skin entries than neighbours in 3D) a
+// fused filter makes every warp run the continuity pair body for the union
+// of its lanes' accepted entries, i.e. nearly every skin entry.  Past this
+// skin/cutoff ratio the sub-step filters all skin lists up front (k_mask,
+// exact lists for every particle) and the sweeps walk exact lists only.
+#ifndef SPH_SPLIT_SKIN_RATIO
+#define SPH_SPLIT_SKIN_RATIO 0.12
+#endif
+static bool split_filter(const SphEngine* e)
+{
+    return e->skin > SPH_SPLIT_SKIN_RATIO * e->cutoff;
+}
+
 // sub-step path: only the invalid lists are rebuilt up front; valid skin
 // lists are filtered inside the continuity / wall sweeps
 template <class T, int D>
@@ -1416,6 +1433,15 @@ static void sub_kick_drift(SphEngine* e, T half, T full, cudaStream_t s)
             eng_of<T>(e), e->cur_v, e->cur_rp, grid_of_engine<T>(e), half, full);
 }
 
+// list upkeep of a sub-step: exact lists for all (split) or for the
+// particles whose skin list is no longer valid
+template <class T, int D>
+static void sub_lists(SphEngine* e, cudaStream_t s)
+{
+    if (split_filter(e)) prepare_lists<T, D>(e, s);
+    else mark_and_fix<T, D>(e, s);
+}
+
 template <class T, int D>
 static void sub_continuity(SphEngine* e, T full, cudaStream_t s)
 {
@@ -1423,7 +1449,8 @@ static void sub_continuity(SphEngine* e, T full, cudaStream_t s)
     const int crp = e->cur_rp;
     if (e->nf > 0)
         note_launch(), k_cont_du<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full);
+            E, make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full,
+            split_filter(e) ? 1 : 0);
     else if (e->n > 0)   // no fluid: the other rp buffer must still carry walls
         cudaMemcpyAsync(E.rp[crp ^ 1], E.rp[crp], sizeof(vec2<T>) * (size_t)e->n,
                         cudaMemcpyDeviceToDevice, s);
@@ -1434,7 +1461,7 @@ static void sub_wall(SphEngine* e, cudaStream_t s)
 {
     const int64_t nw = e->n - e->nf;
     if (nw > 0)
-        launch_wall<T, D>(e, e->cur_rp ^ 1, 1, 1, 1, e->cur_v ^ 1, s);
+        launch_wall<T, D>(e, e->cur_rp ^ 1, 1, 1, split_filter(e) ? 0 : 1, e->cur_v ^ 1, s);
 }
 
 // zero_walls: the reference's momentum body writes dvdt = 0 for walls
@@ -1476,7 +1503,7 @@ static void substep_parts(SphEngine* e, T half, T full, bool fuse, cudaEvent_t* 
     if (!e->drifted) sub_kick_drift<T, D>(e, half, full, s);
     e->drifted = 0;
     if (ev) cudaEventRecord(ev[1], s);
-    mark_and_fix<T, D>(e, s);
+    sub_lists<T, D>(e, s);
     if (ev) cudaEventRecord(ev[2], s);
     sub_continuity<T, D>(e, full, s);
     if (ev) cudaEventRecord(ev[3], s);
@@ -1569,7 +1596,7 @@ static int phase_impl(SphEngine* e, int phase, double half_d, double full_d, cud
     switch (phase) {
     case SPH_PHASE_KICK_DRIFT: sub_kick_drift<T, D>(e, half, full, s); break;
     case SPH_PHASE_CONTINUITY:
-        mark_and_fix<T, D>(e, s);
+        sub_lists<T, D>(e, s);
         sub_continuity<T, D>(e, full, s);
         break;
     case SPH_PHASE_WALL: sub_wall<T, D>(e, s); break;
