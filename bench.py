@@ -65,11 +65,18 @@ def emit(line):
         os.write(_OUT_FD, data)
 
 
-def build_case(name):
+def tg_side(name, world=1):
+    """Weak scaling of config 5: n^3 = world x 200^3 particles (8 GPUs: 400^3
+    = 64M, BASELINE config 5)."""
+    return int(round(CONFIGS[name][1]["n"] * world ** (1.0 / 3.0)))
+
+
+def build_case(name, world=1):
     from paper_2603_11868_b200 import cases
     spec = CONFIGS[name][1]
     if spec["kind"] == "tg":
-        return cases.build_case(cases.taylor_green_config(3, spec["n"], precision="f32"))
+        return cases.build_case(cases.taylor_green_config(3, tg_side(name, world),
+                                                          precision="f32"))
     if spec["kind"] == "2d":
         cfg = cases.CaseConfig(case="dambreak2d", dp=spec["dp"], precision="f32")
     else:
@@ -177,7 +184,7 @@ class ClockSampler:
 
 # -- CPU arms -------------------------------------------------------------------
 
-def cpu_oracle_run(name, steps, budget_s, warmup=0):
+def cpu_oracle_run(name, steps, budget_s, warmup=0, world=1):
     """Time the oracle port (all host threads) on the same configuration:
     initialize() and ``warmup`` steps untimed (bounded by budget_s / 2), then
     up to ``steps`` advective steps bounded by ``budget_s`` seconds.
@@ -185,7 +192,7 @@ def cpu_oracle_run(name, steps, budget_s, warmup=0):
     threads = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(threads))
     from oracle.oracle import OracleSim
-    reg, grid = build_case(name)
+    reg, grid = build_case(name, world if CONFIGS[name][1]["kind"] == "tg" else 1)
     sim = OracleSim.from_registry(reg, grid)
     sim.initialize()
     t0 = time.perf_counter()
@@ -212,7 +219,7 @@ def reference_arm(args, rank, world):
         return
     pus, done, secs, thr, nsubs = cpu_oracle_run(args.config, max(1, args.steps),
                                                  budget_s=args.cpu_budget,
-                                                 warmup=args.warmup)
+                                                 warmup=args.warmup, world=world)
     line = {
         "impl": "reference", "metric": METRIC, "value": pus, "unit": UNIT,
         "n_gpus": world, "steps": done, "warmup": args.warmup,
@@ -375,9 +382,11 @@ def slab_arm(args, rank, world, local_rank):
                                                    EngineBackend, SlabLayout, cell_plane)
     from paper_2603_11868_b200.physics import force_scalars
 
+    from paper_2603_11868_b200.physics import grid_is_periodic
     dev = torch.device("cuda", local_rank)
-    lib = _native.lib()
-    reg, grid = build_case(args.config)
+    weak = CONFIGS[args.config][1]["kind"] == "tg"   # config 5: fixed work per GPU
+    reg, grid = build_case(args.config, world if weak else 1)
+    lib = _native.lib(periodic=grid_is_periodic(grid))
     n = reg.particle_count
     d = reg.dim
     nw = int((reg.raw_view("wall") != 0).sum())
@@ -456,12 +465,13 @@ def slab_arm(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32 (mixed f64)",
-        "data": "synthetic (reference lattice dam break, deterministic)",
+        "scaling": "weak" if weak else "strong", "vs_baseline": None,
+        "dtype": "f32 (mixed f64)", "data": data_label(args.config),
         "config": {"workload": CONFIGS[args.config][0], "case": args.config,
                    "particles": n, "fluid": nf, "wall": nw, "grid_cells": ncells,
                    "nsub_per_step": nsubs, "l2": "flushed between steps (256 MB write)",
-                   "parallelism": f"slabs x{world} (axis-0, 2-plane halos, NCCL P2P)",
+                   "parallelism": f"slabs x{world} (axis-0, 2-plane halos, NCCL P2P"
+                                  + (", periodic ring)" if weak else ")"),
                    "slab_cuts": [int(c) for c in sim.layout.cuts],
                    "sub_step_updates_per_s": n * sum(nsubs) / total},
         "gpu_launches": int(launches),
@@ -552,13 +562,7 @@ def main():
             os.environ.setdefault(k, v)
         torch.distributed.init_process_group(os.environ.get("SPH_BENCH_BACKEND", "nccl"))
     try:
-        if (world > 1 or args.slab) and CONFIGS[args.config][1]["kind"] == "tg":
-            if rank == 0:
-                emit({"metric": METRIC, "unit": UNIT, "n_gpus": world,
-                      "config": {"workload": CONFIGS[args.config][0]},
-                      "unavailable": "periodic boxes run on one GPU; the slab "
-                                     "decomposition has no wrap-around halos yet"})
-        elif world > 1 or args.slab:
+        if world > 1 or args.slab:
             slab_arm(args, rank, world, local_rank)
         else:
             gpu_arm(args, rank, world, local_rank)

@@ -94,6 +94,9 @@ class SlabLayout:
     """Plane cuts: rank r owns planes [cuts[r], cuts[r+1])."""
     cuts: np.ndarray
     nplanes: int
+    # axis 0 periodic (SURVEY.md 8f f4): the slabs form a ring and halos
+    # wrap around plane 0 / nplanes - 1
+    periodic: bool = False
 
     @property
     def nranks(self):
@@ -136,6 +139,14 @@ class SlabLayout:
     def halo_mask(self, rank, planes):
         """Planes within HALO_PLANES outside rank's slab."""
         a, b = int(self.cuts[rank]), int(self.cuts[rank + 1])
+        if self.periodic:
+            # distance outside the slab measured around the ring
+            P = self.nplanes
+            below = (a - planes) % P      # 1, 2: just below a (wrapping)
+            above = (planes - b) % P      # 0, 1: at or just above b (wrapping)
+            inside = (planes >= a) & (planes < b)
+            return ~inside & (((below >= 1) & (below <= HALO_PLANES)) |
+                              (above < HALO_PLANES))
         return ((planes >= a - HALO_PLANES) & (planes < a)) | \
                ((planes >= b) & (planes < b + HALO_PLANES))
 
@@ -231,7 +242,9 @@ class DistributedSimulation:
         self.cfl_advective = cfl_advective
         self.rebalance_every = rebalance_every
         nplanes = int(grid.shape[0])
-        self.layout = layout or SlabLayout.even(nplanes, comm.size)
+        per = getattr(grid, "period", None)
+        self._periodic0 = per is not None and float(per[0]) > 0.0
+        self.layout = self._ring(layout or SlabLayout.even(nplanes, comm.size))
         self.step_count = 0
         self.time = 0.0
         self.interaction_count = 0
@@ -246,6 +259,12 @@ class DistributedSimulation:
 
     # -- decomposition ----------------------------------------------------------
 
+    def _ring(self, layout):
+        """The layout as a ring of slabs when axis 0 is periodic."""
+        if self._periodic0 and not layout.periodic:
+            return SlabLayout(layout.cuts, layout.nplanes, True)
+        return layout
+
     def _planes(self, x):
         return self.backend.planes(x)
 
@@ -254,7 +273,7 @@ class DistributedSimulation:
         planes = self._planes(self.owned["x"])
         hist = torch.bincount(planes, minlength=int(self.grid.shape[0])).cpu().numpy()
         tot = self.comm.allreduce_i64(hist)
-        self.layout = SlabLayout.balanced(tot, self.comm.size)
+        self.layout = self._ring(SlabLayout.balanced(tot, self.comm.size))
 
     def _exchange_fields(self, fields, send_rows, recv_counts):
         """Rows of every field to each neighbour in ONE message: the fields
@@ -452,7 +471,8 @@ class EngineBackend:
     def __init__(self, scalars, sing, grid, device):
         torch = _torch()
         from . import _native
-        self.L = _native.lib()
+        from .physics import grid_is_periodic
+        self.L = _native.lib(periodic=grid_is_periodic(grid))
         self._native = _native
         self.scalars = scalars
         self.sing = sing

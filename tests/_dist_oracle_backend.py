@@ -25,6 +25,10 @@ class OracleBackend:
         self._inter = 0
         self._ovf = 0
         self.halo_dtype = torch.from_numpy(np.zeros(1, type(scalars[0]))).dtype
+        # periodic grids: the oracle's box for every kernel-level call
+        dt = np.dtype(type(scalars[0]))
+        O.set_box(dt, O.box_arrays(dt, getattr(grid, "period", None), grid.origin, grid.dim),
+                  grid.dim)
 
     def planes(self, x):
         xn = x.numpy()

@@ -24,6 +24,14 @@ def _free_port():
 
 def _case(kind):
     from paper_2603_11868_b200 import cases
+    if kind in ("tg2d", "tg3d"):
+        # periodic Taylor-Green box with a uniform drift so
+        # particles cross the wrap-around boundary between the end slabs
+        d = 2 if kind == "tg2d" else 3
+        cfg = cases.taylor_green_config(d, 40 if d == 2 else 16, precision="f32")
+        reg, grid = cases.build_case(cfg)
+        reg.raw_view("v")[:] += np.asarray([3.0, -2.0, 1.5][:d], np.float32)
+        return reg, grid
     if kind == "2d":
         cfg = cases.CaseConfig(case="dambreak2d", dp=0.05, precision="f32")
     else:
@@ -95,6 +103,9 @@ def _reference(kind, steps, shepard_every=200):
     (2, "2d", 60, 25, 10),
     (3, "2d", 40, 200, 1),
     (2, "3d", 6, 3, 2),
+    (2, "tg2d", 40, 15, 5),
+    (3, "tg2d", 30, 200, 1),
+    (2, "tg3d", 8, 4, 2),
 ])
 def test_slab_decomposition_matches_single_process(world, kind, steps, shep, rebal):
     rec, g, cuts, (migrated, ghosts) = _run(world, kind, steps, shep, rebal)
@@ -119,6 +130,22 @@ def test_slab_layout_balancing_and_halos():
         assert len(halo) <= 2 * HALO_PLANES
     with pytest.raises(ValueError):
         SlabLayout.balanced(np.ones(5), 3)
+
+
+def test_periodic_ring_halos():
+    """Axis-0 periodic layouts: halos wrap around the ring, never include the
+    slab itself, and every plane within 2 of a slab (mod the ring) is in it."""
+    P = 12
+    lay = SlabLayout(np.array([0, 3, 8, 12], np.int64), P, True)
+    planes = np.arange(P)
+    for r in range(3):
+        a, b = lay.cuts[r], lay.cuts[r + 1]
+        halo = set(np.nonzero(lay.halo_mask(r, planes))[0])
+        want = {(a - 1) % P, (a - 2) % P, b % P, (b + 1) % P} - set(range(a, b))
+        assert halo == want, (r, halo, want)
+    import torch
+    t = lay.halo_mask(0, torch.arange(P))
+    assert set(torch.nonzero(t).flatten().tolist()) == {10, 11, 3, 4}
 
 
 def test_cell_plane_matches_kernel_binning():

@@ -67,6 +67,8 @@ def _run(world, kind, steps, shepard_every, rebalance):
     (2, "2d", 60, 25, 10),
     (3, "2d", 30, 200, 1),
     (2, "3d", 6, 3, 2),
+    (2, "tg2d", 40, 15, 5),     # periodic ring of slabs
+    (3, "tg3d", 8, 4, 2),
 ])
 def test_engine_slabs_match_single_process(world, kind, steps, shep, rebal):
     rec, g, (migrated, ghosts) = _run(world, kind, steps, shep, rebal)
