@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 5
+#define SPH_ABI_VERSION 6
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -195,11 +195,11 @@ typedef struct {
     unsigned int overflow;            /* particles over NEIGHBOR_CAPACITY      */
     unsigned int oob;                 /* fluid out-of-bounds clamps            */
     unsigned int oob_walls;           /* wall clamps (counted once, at push)   */
-    unsigned int nfix;                /* exact list rebuilds (skin fallbacks)  */
+    unsigned int nfix;                /* list refreshes (cell change / skin)   */
     unsigned int nan_flags;           /* bit0: a NaN rho, bit1: a NaN |v|^2    */
     unsigned int push_error;          /* push: ids not a permutation of 0..n-1 */
     unsigned int fluid_seen;          /* push: particles with wall == 0        */
-    unsigned int reserved;
+    unsigned int ndisp;               /* of which displacement-triggered       */
 } SphStepStats;
 
 typedef struct {
@@ -244,6 +244,11 @@ typedef struct {
      * periodic axis wraps over [origin, origin + L), needs shape >= 3 and
      * L <= shape * cell_size; only libsphb200_periodic.so accepts L > 0. */
     double period[3];
+    /* per particle (dev, run precision): the value of disp when the
+     * particle's own skin list was last built (a mid-step refresh after a
+     * cell change re-bases it; disp itself always measures the path since
+     * the step's list build, which bounds every neighbour's motion) */
+    void* disp0;
 } SphEngine;
 
 size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64);

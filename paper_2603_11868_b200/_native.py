@@ -76,7 +76,7 @@ class SphStepStats(C.Structure):
         ("overflow", C.c_uint32), ("oob", C.c_uint32),
         ("oob_walls", C.c_uint32), ("nfix", C.c_uint32),
         ("nan_flags", C.c_uint32), ("push_error", C.c_uint32),
-        ("fluid_seen", C.c_uint32), ("reserved", C.c_uint32),
+        ("fluid_seen", C.c_uint32), ("ndisp", C.c_uint32),
     ]
 
 
@@ -100,10 +100,11 @@ class SphEngine(C.Structure):
         ("skin", c_f64),
         ("cur_v", c_i32), ("cur_rp", c_i32), ("cur_pos", c_i32), ("drifted", c_i32), ("f64", c_i32), ("lists_ready", c_i32),
         ("period", c_f64 * 3),
+        ("disp0", P),
     ]
 
 
-ABI_VERSION = 5   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 6   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)

@@ -29,6 +29,7 @@ template <> struct RN<float> {
     static __device__ __forceinline__ float from_d(double a) { return __double2float_rn(a); }
     // upward-rounded ops for rigorous displacement bounds
     static __device__ __forceinline__ float add_ru(float a, float b) { return __fadd_ru(a, b); }
+    static __device__ __forceinline__ float sub_ru(float a, float b) { return __fsub_ru(a, b); }
     static __device__ __forceinline__ float mul_ru(float a, float b) { return __fmul_ru(a, b); }
     static __device__ __forceinline__ float sqrt_ru(float a) { return __fsqrt_ru(a); }
     static constexpr float kOnePlus2Eps = 1.0000002384185791f;   // 1 + 2^-22
@@ -41,6 +42,7 @@ template <> struct RN<double> {
     static __device__ __forceinline__ double sqrt(double a) { return __dsqrt_rn(a); }
     static __device__ __forceinline__ double from_d(double a) { return a; }
     static __device__ __forceinline__ double add_ru(double a, double b) { return __dadd_ru(a, b); }
+    static __device__ __forceinline__ double sub_ru(double a, double b) { return __dsub_ru(a, b); }
     static __device__ __forceinline__ double mul_ru(double a, double b) { return __dmul_ru(a, b); }
     static __device__ __forceinline__ double sqrt_ru(double a) { return __dsqrt_ru(a); }
     static constexpr double kOnePlus2Eps = 1.0000000000000004;   // 1 + 2^-51

@@ -444,6 +444,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                 E.lcount[slot] = ok ? cnt : 0;
                 E.nww[slot] = lane ? naB : naA;
                 E.disp[i] = T(0);
+                E.disp0[i] = T(0);
             }
         }
         __syncthreads();   // shared tile reused by the next cell
@@ -684,6 +685,7 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
                 E.lcount[slot] = ok ? (lane ? cntB : cntA) : 0;
                 E.nww[slot] = lane ? naB : naA;
                 E.disp[i] = T(0);
+                E.disp0[i] = T(0);
             }
         }
         __syncwarp();
@@ -727,6 +729,7 @@ k_skin_big(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E)
                 E.lcount[slot] = stored;
                 E.nww[slot] = cnts.accepted;
                 E.disp[i] = T(0);
+                E.disp0[i] = T(0);
             }
             __syncwarp();
         }
@@ -829,9 +832,10 @@ k_mask(Eng<T> E, GridP<T> g, T s_eff)
         const uint32_t c0 = E.cell0[i];
         if (c0 == kInvalidCell) {
             need = true;
-        } else if (RN<T>::add_ru(E.disp[i], dmax) > s_eff) {
+        } else if (RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax) > s_eff) {
             E.cell0[i] = kInvalidCell;
             need = true;
+            atomicAdd(&E.stats->ndisp, 1u);
         } else {
             T xi[3];
             to3<T>(E.pos[i], xi);
@@ -876,39 +880,86 @@ k_mark(Eng<T> E, T s_eff)
             need = true;
         } else {
             const T dmax = T(__longlong_as_double((long long)E.stats->dmax_bits));
-            if (RN<T>::add_ru(E.disp[i], dmax) > s_eff) {
+            if (RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax) > s_eff) {
                 E.cell0[i] = kInvalidCell;
                 need = true;
+                atomicAdd(&E.stats->ndisp, 1u);
             }
         }
     }
     enqueue(E.queue, E.qcount, need, (uint32_t)i);
 }
 
-// exact ordered lists (neighborhood.py:176-227) for the queued particles;
-// one warp per entry, grid-stride over the device-side queue length
+// List refresh of the queued particles (cell changed, or own displacement
+// + the largest displacement past the skin), one warp each: the skin list
+// of the CURRENT cell's block within cutoff + skin (neighborhood.py:176-227
+// with the skin radius, ascending id), re-based at the current displacement
+// so it stays valid for the rest of the step, plus this sub-step's exact list
+// (its 0 < r2 < c^2 subset, same order).  A particle whose skin candidates
+// exceed the capacity gets the exact list only and stays queued.
 template <class T, int D>
 __global__ void __launch_bounds__(kNlThreads, 4)
-k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E)
+k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E, T cs2)
 {
     __shared__ WarpBuf bufs[kNlWarps];
+    __shared__ uint32_t sorted[kNlWarps][kCap];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
     const uint32_t qn = *(volatile uint32_t*)E.qcount;
     WarpBuf& sb = bufs[warp];
+    uint32_t* srt = sorted[warp];
     for (uint32_t q = blockIdx.x * kNlWarps + warp; q < qn; q += gridDim.x * kNlWarps) {
         const int64_t i = E.queue[q];
         const int64_t slot = slot_of(E, i);
         const bool fluid = i < E.nf;
         T xi[3];
         acc.position(i, xi);
-        CollectCounts cc = warp_collect<T, D, false>(acc, g, i, xi, T(0), fluid ? 3u : 1u, sb);
-        if (cc.accepted > kCap) {
-            if (lane == 0) E.acount[slot] = -1;
-        } else {
+        CollectCounts cc = warp_collect<T, D, true>(acc, g, i, xi, cs2, fluid ? 3u : 1u, sb);
+        if (cc.stored <= kCap) {
             warp_emit_sorted(sb, cc.stored, lane, [&](int pos, uint32_t j) {
-                E.elist[ell_index(slot, pos)] = (int32_t)j;
+                E.lists[ell_index(slot, pos)] = (int32_t)j;
+                srt[pos] = j;
             });
-            if (lane == 0) E.acount[slot] = cc.stored;   // fluid: all; walls: fluid visits
+            // the exact subset in list order
+            int ex = 0;
+            for (int b = 0; b < cc.stored; b += 32) {
+                const int k = b + (int)lane;
+                bool ok = false;
+                uint32_t j = 0;
+                if (k < cc.stored) {
+                    j = srt[k];
+                    T xj[3];
+                    acc.position(j, xj);
+                    const T r2 = accept_r2<T, D>(xi, xj);
+                    ok = (r2 < g.c2) && (r2 > T(0));
+                }
+                const unsigned bl = __ballot_sync(0xffffffffu, ok);
+                if (ok) E.elist[ell_index(slot, ex + __popc(bl & lt))] = (int32_t)j;
+                ex += __popc(bl);
+            }
+            // walls: wall-wall neighbours count toward the capacity (nww)
+            const int total = ex + (fluid ? 0 : cc.accepted);
+            if (lane == 0) {
+                int cxyz[3];
+                E.acount[slot] = total > kCap ? -1 : ex;
+                E.cell0[i] = cell_key_of<T, D>(xi, g, cxyz);
+                E.lcount[slot] = cc.stored;
+                E.nww[slot] = cc.accepted;
+                E.disp0[i] = E.disp[i];
+            }
+        } else {   // skin list over capacity: this sub-step's exact list only
+            __syncwarp();
+            CollectCounts ce = warp_collect<T, D, false>(acc, g, i, xi, T(0), fluid ? 3u : 1u,
+                                                         sb);
+            if (ce.accepted > kCap) {
+                if (lane == 0) E.acount[slot] = -1;
+            } else {
+                warp_emit_sorted(sb, ce.stored, lane, [&](int pos, uint32_t j) {
+                    E.elist[ell_index(slot, pos)] = (int32_t)j;
+                });
+                if (lane == 0) E.acount[slot] = ce.stored;
+            }
+            if (lane == 0) E.cell0[i] = kInvalidCell;
         }
         if (lane == 0) atomicAdd(&E.stats->nfix, 1u);
         __syncwarp();
@@ -1294,7 +1345,7 @@ static void launch_fix(const SphEngine* e, cudaStream_t s)
     EngAcc<T> acc = acc_of_engine<T>(e);
     const int64_t want = (e->n + kNlWarps - 1) / kNlWarps;
     const int blocks = (int)(want < 148 * 8 ? want : 148 * 8);
-    note_launch(), k_fix_build<T, D><<<blocks, kNlThreads, 0, s>>>(acc, g, E);
+    note_launch(), k_fix_build<T, D><<<blocks, kNlThreads, 0, s>>>(acc, g, E, skin_cs2<T>(e));
 }
 
 // exact lists for every particle: filtered skin lists (k_mask), exact

@@ -37,7 +37,7 @@ struct Eng {
     const uint8_t* owned_id;
     uint32_t* offs_f; uint32_t* offs_w;
     int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; int32_t* elist;
-    uint32_t* cell0; T* disp; uint32_t* queue; uint32_t* qcount;
+    uint32_t* cell0; T* disp; T* disp0; uint32_t* queue; uint32_t* qcount;
     SphStepStats* stats;
 };
 
@@ -58,7 +58,8 @@ inline Eng<T> eng_of(const SphEngine* e)
     g.owned_id = e->owned_id;
     g.offs_f = e->offs_f; g.offs_w = e->offs_w;
     g.lists = e->lists; g.lcount = e->lcount; g.acount = e->acount; g.nww = e->nww;
-    g.elist = e->elist; g.cell0 = e->cell0; g.disp = (T*)e->disp; g.queue = e->queue;
+    g.elist = e->elist; g.cell0 = e->cell0; g.disp = (T*)e->disp; g.disp0 = (T*)e->disp0;
+    g.queue = e->queue;
     g.qcount = e->qcount; g.stats = e->stats;
     return g;
 }

@@ -524,6 +524,7 @@ static int stats_impl(SphEngine* e, int flags, cudaStream_t s)
         cudaMemsetAsync(&e->stats->interactions, 0, sizeof(unsigned long long), s);
         cudaMemsetAsync(&e->stats->overflow, 0, 2 * sizeof(unsigned int), s);
         cudaMemsetAsync(&e->stats->nfix, 0, sizeof(unsigned int), s);
+        cudaMemsetAsync(&e->stats->ndisp, 0, sizeof(unsigned int), s);
     }
     if (flags & 2) {
         cudaMemsetAsync(e->stats, 0, 2 * sizeof(unsigned long long), s);   // vmax, amax

@@ -750,8 +750,7 @@ class EngineBackend:
     def counters(self):
         s = self._stats()
         self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_RESET))
-        nfix = int(s.nfix)
-        frac = nfix / max(1, self.n)
+        frac = int(s.ndisp) / max(1, self.n)
         if frac > 2e-2:
             self._skin_factor = min(self._skin_factor * 1.5, 16.0)
         return int(s.interactions), int(s.overflow)

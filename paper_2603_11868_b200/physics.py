@@ -424,7 +424,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
         T[k] = torch.empty((n, 4), dtype=tdt, device=dev)
     for k in ("rp0", "rp1", "rq"):
         T[k] = torch.empty((n, 2), dtype=tdt, device=dev)
-    for k in ("drho", "rho_scratch_id", "vol_id", "disp"):
+    for k in ("drho", "rho_scratch_id", "vol_id", "disp", "disp0"):
         T[k] = torch.empty((n,), dtype=tdt, device=dev)
     for k in ("id", "nnb", "refpos", "oflow_id", "wall_id", "cell0", "queue"):
         T[k] = torch.empty((n,), dtype=i32, device=dev)
@@ -449,7 +449,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
     E.rq = T["rq"].data_ptr()
     for k in ("dvdt", "drho", "id", "nnb", "refpos", "rho_scratch_id",
               "oflow_id", "wall_id", "vol_id", "offs_f", "offs_w", "lists",
-              "lcount", "acount", "nww", "elist", "cell0", "disp", "queue",
+              "lcount", "acount", "nww", "elist", "cell0", "disp", "disp0", "queue",
               "qcount", "ws", "stats"):
         setattr(E, k, T[k].data_ptr())
     E.owned_id = None      # every particle owned (multi-rank runs set it)
@@ -693,9 +693,12 @@ class Simulation:
         cap = (0.45 if self.registry.dim == 3 else 1.0) * cutoff
         return min(self._skin_factor * est + 0.02 * cutoff, cap)
 
-    def _adapt_skin(self, nfix, nsub):
+    def _adapt_skin(self, ndisp, nsub):
+        """Grow the skin when displacement-triggered refreshes are frequent,
+        shrink it towards the 2x-displacement floor otherwise (refreshes
+        after a cell change do not depend on the skin)."""
         n = max(1, self.registry.particle_count)
-        frac = nfix / (n * max(1, nsub))
+        frac = ndisp / (n * max(1, nsub))
         if frac > 2e-3:
             self._skin_factor = min(self._skin_factor * 1.5, 16.0)
         elif frac < 5e-4:
@@ -763,7 +766,7 @@ class Simulation:
         self._host_stale = True
         self.last_nsub = nsub
         self.last_nfix = int(stats.nfix)
-        self._adapt_skin(stats.nfix, nsub)
+        self._adapt_skin(stats.ndisp, nsub)
         self.out_of_bounds += stats.oob + self._oob_walls
         self._finish_counts(stats, check=True)
         self.interaction_count += int(stats.interactions)
