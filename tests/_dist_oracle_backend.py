@@ -27,8 +27,7 @@ class OracleBackend:
         self.halo_dtype = torch.from_numpy(np.zeros(1, type(scalars[0]))).dtype
         # periodic grids: the oracle's box for every kernel-level call
         dt = np.dtype(type(scalars[0]))
-        O.set_box(dt, O.box_arrays(dt, getattr(grid, "period", None), grid.origin, grid.dim),
-                  grid.dim)
+        self.box = O.box_arrays(dt, getattr(grid, "period", None), grid.origin, grid.dim)
 
     def planes(self, x):
         xn = x.numpy()
@@ -77,27 +76,27 @@ class OracleBackend:
         sc = self.sc
         O.sweep("shepard", (f["x"], f["rho"], f["m"], f["wall"], f["id"], self.offsets,
                             self.pids, self.origin, self.shape, f["rho_scratch"],
-                            sc[0], sc[1], sc[2], sc[3]))
+                            sc[0], sc[1], sc[2], sc[3]), box=self.box)
         f["rho"][:] = f["rho_scratch"]
         O.integrate("density_update", (f["rho"], f["p"], f["drho"], f["wall"], dt(0),
-                                       dt(self.sing["c0"]), dt(self.sing["rho0"])))
+                                       dt(self.sing["c0"]), dt(self.sing["rho0"])), box=self.box)
 
     def kick_drift(self, half, full):
         f = self.f
-        O.integrate("kick", (f["v"], f["dvdt"], f["wall"], half))
-        O.integrate("drift", (f["x"], f["v"], f["wall"], full))
+        O.integrate("kick", (f["v"], f["dvdt"], f["wall"], half), box=self.box)
+        O.integrate("drift", (f["x"], f["v"], f["wall"], full), box=self.box)
 
     def continuity_du(self, full):
         f = self.f
         dt = f["x"].dtype.type
-        O.sweep("continuity", self._force())
+        O.sweep("continuity", self._force(), box=self.box)
         self._ovf_check()
         O.integrate("density_update", (f["rho"], f["p"], f["drho"], f["wall"], full,
-                                       dt(self.sing["c0"]), dt(self.sing["rho0"])))
+                                       dt(self.sing["c0"]), dt(self.sing["rho0"])), box=self.box)
 
     def wall_pressure(self, initial=False):
         f = self.f
-        O.sweep("wall_pressure", self._force())
+        O.sweep("wall_pressure", self._force(), box=self.box)
         self._ovf_check()
         n = self.n_own
         w = f["wall"][:n] != 0
@@ -105,14 +104,14 @@ class OracleBackend:
 
     def momentum_kick(self, half):
         f = self.f
-        O.sweep("momentum", self._force())
+        O.sweep("momentum", self._force(), box=self.box)
         self._ovf_check()
         n = self.n_own
         fl = f["wall"][:n] == 0
         s = int(f["nnb"][:n][fl].sum())
         self._inter += s if half is None else 2 * s
         if half is not None:
-            O.integrate("kick", (f["v"], f["dvdt"], f["wall"], half))
+            O.integrate("kick", (f["v"], f["dvdt"], f["wall"], half), box=self.box)
 
     def halo_width(self, kind):
         return 2 * self.f["x"].shape[1] if kind == XV else 2
