@@ -14,7 +14,8 @@ import sys
 # csrc kernel -> bench.py sub-step name (physics.SUBSTEP_KERNELS)
 NAMES = {"k_kick_drift": "kick_drift", "k_cont_du": "continuity_du",
          "k_wall": "wall_pressure", "k_mom": "momentum_kick",
-         "k_skin_tile": "skin_build", "k_skin_warp": "skin_build", "k_mark": "list_filter"}
+         "k_skin_tile": "skin_build", "k_skin_warp": "skin_build", "k_mark": "list_filter",
+         "k_mask": "list_filter"}
 
 
 def _val(r, hdr, units, key):

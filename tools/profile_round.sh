@@ -1,14 +1,16 @@
-# Round profiling: bench lines (default + 3d4m), launch lists, and full ncu
-# captures of the sub-step kernels and the skin build, for profiles/<round>/.
+# Round profiling: bench lines (default + 3d4m + tg8m), launch lists, and full
+# ncu captures of the sub-step kernels and the skin build, for profiles/<round>/.
 set -x
 cd $GRAFT_REPO_ROOT
 R=${ROUND:-r01}
 python bench.py > gpurun_out/${R}_bench_2d1m.json 2> gpurun_out/${R}_bench_2d1m.err
 python bench.py --config 3d4m --no-cpu-baseline > gpurun_out/${R}_bench_3d4m.json 2> gpurun_out/${R}_bench_3d4m.err
-for c in 2d1m 3d4m; do
+python bench.py --config tg8m --no-cpu-baseline > gpurun_out/${R}_bench_tg8m.json 2> gpurun_out/${R}_bench_tg8m.err
+python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/${R}_bench_ref.json 2> gpurun_out/${R}_bench_ref.err
+for c in ${CONFIGS:-2d1m 3d4m tg8m}; do
   python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null || exit 1
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches_$c.csv python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null 2>&1
-  ncu --set full --clock-control none --import-source on -k regex:"k_cont_du|k_mom|k_kick_drift|k_wall|k_mark" -s 30 -c 6 -o gpurun_out/${R}_sweeps_$c python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"k_cont_du|k_mom|k_kick_drift|k_wall|k_mark|k_mask|k_fix_build" -s 30 -c 7 -o gpurun_out/${R}_sweeps_$c python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null 2>&1
   ncu --set full --clock-control none --import-source on -k regex:"k_skin_tile|k_skin_warp|k_radix_scatter|k_fluid_gather" -s 0 -c 6 -o gpurun_out/${R}_step_$c python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null 2>&1
 done
 echo done
