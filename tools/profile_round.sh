@@ -14,3 +14,14 @@ for c in ${CONFIGS:-2d1m 3d4m tg8m}; do
   ncu --set full --clock-control none --import-source on -k regex:"k_skin_tile|k_skin_warp|k_radix_scatter|k_fluid_gather" -s 0 -c 6 -o gpurun_out/${R}_step_$c python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null 2>&1
 done
 echo done
+# summaries on the box (the .ncu-rep files are large): key metrics and
+# the per-kernel traffic table; reports kept only when SPH_KEEP_REPS=1
+for c in ${CONFIGS:-2d1m 3d4m tg8m}; do
+  python tools/launches_summary.py gpurun_out/${R}_launches_$c.csv > gpurun_out/${R}_launches_${c}_summary.txt
+  python tools/ncu_summary.py gpurun_out/${R}_sweeps_$c.ncu-rep > gpurun_out/${R}_ncu_sweeps_$c.txt
+  python tools/ncu_summary.py gpurun_out/${R}_step_$c.ncu-rep > gpurun_out/${R}_ncu_step_$c.txt
+done
+python tools/ncu_traffic.py gpurun_out/${R}_ncu_traffic.json $(for c in ${CONFIGS:-2d1m 3d4m tg8m}; do printf "%s=gpurun_out/%s_sweeps_%s.ncu-rep " $c $R $c; done)
+[ "${SPH_KEEP_REPS:-0}" = 1 ] || rm -f gpurun_out/${R}_*.ncu-rep
+gzip -f gpurun_out/${R}_launches_*.csv
+echo summarised
