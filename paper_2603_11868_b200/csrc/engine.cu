@@ -208,6 +208,42 @@ __device__ __forceinline__ void enqueue(uint32_t* queue, uint32_t* qcount, bool 
 // the sorted candidates past one particle of the cell -- the ballot-compacted
 // survivors are already in ascending id, so no per-particle sort is needed.
 // Blocks larger than the tile fall back to the per-particle collector.
+// Periodic builds: the cell tile stores every candidate at its image
+// nearest the cell's centre, so the skin test is a plain difference (no
+// minimum image per test).  The shifted coordinate RN(x_j +- L) differs from
+// the exact minimum-image difference by a rounding of L-scale values; the
+// periodic skin radius carries a 1e-4 relative margin for it (skin_cs2),
+// far above that error, and the lists are filtered exactly afterwards.
+template <class T, int D>
+__device__ __forceinline__ void tile_image(vec4<T>& p, const int (&cc)[3], const GridP<T>& g)
+{
+#if SPH_PERIODIC
+    T* x = reinterpret_cast<T*>(&p);
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+        const T L = BoxOf<T>::L(k);
+        if (L > T(0)) {
+            const T c = g.o[k] + (T(cc[k]) + T(0.5)) * g.cs;
+            const T d = x[k] - c;
+            if (d > BoxOf<T>::hL(k)) x[k] = x[k] - L;
+            else if (d < -BoxOf<T>::hL(k)) x[k] = x[k] + L;
+        }
+    }
+#else
+    (void)p; (void)cc; (void)g;
+#endif
+}
+
+// the skin test's r2 against a tile candidate (already imaged)
+template <class T, int D>
+__device__ __forceinline__ T tile_r2(const T (&xi)[3], const T (&xj)[3])
+{
+    T r2 = RN<T>::mul(RN<T>::sub(xi[0], xj[0]), RN<T>::sub(xi[0], xj[0]));
+    r2 = RN<T>::add(r2, RN<T>::mul(RN<T>::sub(xi[1], xj[1]), RN<T>::sub(xi[1], xj[1])));
+    if (D == 3) r2 = RN<T>::add(r2, RN<T>::mul(RN<T>::sub(xi[2], xj[2]), RN<T>::sub(xi[2], xj[2])));
+    return r2;
+}
+
 template <class T, int D> struct SkinTile;
 #ifndef SPH_SKIN2_THREADS
 #define SPH_SKIN2_THREADS 128
@@ -395,6 +431,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                 const uint32_t j = phys_of_id[sj[k]];
                 sj[k] = j;
                 p = E.pos[j];
+                tile_image<T, D>(p, cc, g);
             } else {   // padding: never within reach
                 p.x = inf; p.y = inf; p.z = inf; p.w = T(0);
                 sj[k] = 0;
@@ -422,8 +459,16 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                 const uint32_t j = sj[k];
                 T xj[3];
                 to3<T>(spos[k], xj);
+#if SPH_PERIODIC
+                const T r2a = tile_r2<T, D>(xa, xj);
+#else
                 const T r2a = accept_r2<T, D>(xa, xj);
+#endif
+#if SPH_PERIODIC
+                const T r2b = tile_r2<T, D>(xb, xj);
+#else
                 const T r2b = accept_r2<T, D>(xb, xj);
+#endif
                 const bool jf = (int64_t)j < nf;
                 const bool stA = (flA || jf) && r2a < cs2 && j != (uint32_t)iA;
                 const bool stB = hasB && (flB || jf) && r2b < cs2 && j != (uint32_t)iB;
@@ -645,6 +690,7 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
                 const uint32_t j = phys_of_id[sj[k]];
                 sj[k] = j;
                 p = E.pos[j];
+                tile_image<T, D>(p, cc, g);
             } else {
                 p.x = inf; p.y = inf; p.z = inf; p.w = T(0);
                 sj[k] = 0;
@@ -670,8 +716,16 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
                 const uint32_t j = sj[k];
                 T xj[3];
                 to3<T>(spos[k], xj);
+#if SPH_PERIODIC
+                const T r2a = tile_r2<T, D>(xa, xj);
+#else
                 const T r2a = accept_r2<T, D>(xa, xj);
+#endif
+#if SPH_PERIODIC
+                const T r2b = tile_r2<T, D>(xb, xj);
+#else
                 const T r2b = accept_r2<T, D>(xb, xj);
+#endif
                 const bool jf = (int64_t)j < nf;
                 const bool stA = (flA || jf) && r2a < cs2 && j != (uint32_t)iA;
                 const bool stB = hasB && (flB || jf) && r2b < cs2 && j != (uint32_t)iB;
@@ -1292,7 +1346,11 @@ using namespace sph;
 template <class T>
 static T skin_cs2(const SphEngine* e)
 {
+#if SPH_PERIODIC
+    const T cs = T((e->cutoff + e->skin) * (1.0 + 1e-4));   // tile_image margin
+#else
     const T cs = T(e->cutoff + e->skin);
+#endif
     return cs * cs;
 }
 
