@@ -23,7 +23,10 @@
 
 namespace sph {
 
-constexpr int kSweepThreads = 128;
+#ifndef SPH_SWEEP_THREADS
+#define SPH_SWEEP_THREADS 128
+#endif
+constexpr int kSweepThreads = SPH_SWEEP_THREADS;
 constexpr uint32_t kInvalidCell = 0xffffffffu;   // list is not a valid skin list
 
 template <class T>

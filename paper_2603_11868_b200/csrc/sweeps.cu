@@ -411,10 +411,15 @@ __global__ void k_selftest_div(float hf, double hd, int64_t n, uint64_t seed,
          k += (int64_t)gridDim.x * blockDim.x) {
         uint64_t st = seed ^ (uint64_t)k * 0x2545f4914f6cdd1dull;
         const uint64_t u = splitmix64(st);
-        // random significand, exponent spread over +-2^40 around 1
-        const double mag = ldexp(1.0 + (double)(u >> 11) * 0x1.0p-53, (int)(u & 63) - 32);
-        const double a = (u >> 7) & 1 ? -mag : mag;
-        const float af = (float)a;
+        // random significands; binary32 exponents over 2^-64 .. 2^63 and
+        // binary64 ones over 2^-470 .. 2^470, both across the edges of the
+        // reciprocal path's range tests (2^+-59 / 2^+-465)
+        const double sig = 1.0 + (double)(u >> 11) * 0x1.0p-53;
+        const double magf = ldexp(sig, (int)(u & 127) - 64);
+        const double magd = ldexp(sig, (int)((u >> 16) % 941) - 470);
+        const bool neg = (u >> 7) & 1;
+        const float af = (float)(neg ? -magf : magf);
+        const double a = neg ? -magd : magd;
         if (__float_as_uint(fdiv_rcp(af, hf, yf, okf)) != __float_as_uint(__fdiv_rn(af, hf))) nb++;
         if (__double_as_longlong(ddiv_rcp(a, hd, yd, okd)) !=
             __double_as_longlong(__ddiv_rn(a, hd)))
