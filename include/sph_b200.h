@@ -316,6 +316,9 @@ int sph_engine_probe(const SphEngine* e, const double* loc, double radius, doubl
                                        current                                      */
 #define SPH_PHASE_INIT_WALL 4       /* initialize: exact lists + WALL_PRESSURE       */
 #define SPH_PHASE_INIT_MOMENTUM 5   /* initialize: MOMENTUM (no kick)                */
+#define SPH_PHASE_MOMENTUM_NEXT 6   /* MOMENTUM + KICK + the NEXT sub-step's KICK +
+                                       DRIFT of owned fluid (same dt); the next
+                                       KICK_DRIFT phase is then a no-op           */
 int sph_engine_phase(SphEngine* e, int32_t phase, double half_dt, double full_dt,
                      cudaStream_t s);
 /* Halo records of the particles at physical indices phys[0..count), packed

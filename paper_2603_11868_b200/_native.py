@@ -109,7 +109,7 @@ STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)
 PHASE_KICK_DRIFT, PHASE_CONTINUITY, PHASE_WALL, PHASE_MOMENTUM = 0, 1, 2, 3
-PHASE_INIT_WALL, PHASE_INIT_MOMENTUM = 4, 5
+PHASE_INIT_WALL, PHASE_INIT_MOMENTUM, PHASE_MOMENTUM_NEXT = 4, 5, 6
 HALO_XV, HALO_RP_NEXT, HALO_RP_CUR = 0, 1, 2
 LATTICE_ALL, LATTICE_TANK, LATTICE_NOT_IN = 0, 1, 2
 

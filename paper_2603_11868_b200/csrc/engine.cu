@@ -1271,7 +1271,7 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
                 V4.x = RN<T>::add(V4.x, RN<T>::mul(half, A4.x));
                 V4.y = RN<T>::add(V4.y, RN<T>::mul(half, A4.y));
                 if (D == 3) V4.z = RN<T>::add(V4.z, RN<T>::mul(half, A4.z));
-                if (fuse) {
+                if (fuse && is_owned(E, i)) {   // ghosts: the XV refresh brings them
                     vec4<T> P4 = pos[i];
                     const T xo[3] = {P4.x, P4.y, P4.z};
                     kick_drift_one<T, D>(P4, V4, A4, half, full);
@@ -1574,6 +1574,29 @@ static void sub_lists(SphEngine* e, cudaStream_t s)
     else mark_and_fix<T, D>(e, s);
 }
 
+// Walls' continuity operand m/rho from the current (rho, p) buffer.  After a
+// fused MOMENTUM_NEXT phase of a slab rank the KICK_DRIFT phase (which sets
+// it for walls and ghosts) is skipped; k_wall set it for every wall from
+// this rank's own wall pressure, which for WALL GHOSTS is superseded by the
+// owner's (rho, p) refresh -- so it is recomputed here from the refreshed
+// buffer (owned walls get the value they already hold).
+template <class T>
+__global__ void __launch_bounds__(256) k_wall_operands(Eng<T> E, int cv, int crp)
+{
+    const int64_t i = E.nf + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < E.n)
+        reinterpret_cast<T*>(&E.vel[cv][i])[3] = RN<T>::div(E.pos[i].w, E.rp[crp][i].x);
+}
+
+template <class T>
+static void sub_wall_operands(SphEngine* e, cudaStream_t s)
+{
+    const int64_t nw = e->n - e->nf;
+    if (nw > 0)
+        note_launch(), k_wall_operands<T><<<grid_for(nw, 256), 256, 0, s>>>(eng_of<T>(e),
+                                                                          e->cur_v, e->cur_rp);
+}
+
 template <class T, int D>
 static void sub_continuity(SphEngine* e, T full, cudaStream_t s)
 {
@@ -1726,13 +1749,18 @@ static int phase_impl(SphEngine* e, int phase, double half_d, double full_d, cud
 {
     const T half = T(half_d), full = T(full_d);
     switch (phase) {
-    case SPH_PHASE_KICK_DRIFT: sub_kick_drift<T, D>(e, half, full, s); break;
+    case SPH_PHASE_KICK_DRIFT:   // already applied by a MOMENTUM_NEXT phase?
+        if (!e->drifted) sub_kick_drift<T, D>(e, half, full, s);
+        else sub_wall_operands<T>(e, s);
+        e->drifted = 0;
+        break;
     case SPH_PHASE_CONTINUITY:
         sub_lists<T, D>(e, s);
         sub_continuity<T, D>(e, full, s);
         break;
     case SPH_PHASE_WALL: sub_wall<T, D>(e, s); break;
     case SPH_PHASE_MOMENTUM: sub_momentum<T, D>(e, half, T(0), false, true, s); break;
+    case SPH_PHASE_MOMENTUM_NEXT: sub_momentum<T, D>(e, half, full, true, false, s); break;
     case SPH_PHASE_INIT_WALL: init_wall<T, D>(e, s); break;
     case SPH_PHASE_INIT_MOMENTUM: init_momentum<T, D>(e, s); break;
     default: set_error("engine_phase: unknown phase"); return SPH_ERR_INVALID;

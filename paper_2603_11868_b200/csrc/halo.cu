@@ -178,7 +178,12 @@ extern "C" int sph_engine_substeps_slab(SphEngine* e, void* comm, const SphHaloP
         if (!rc) rc = sph_halo_exchange(e, comm, plan, SPH_HALO_RP_NEXT, 0, s);
         if (!rc) rc = sph_engine_phase(e, SPH_PHASE_WALL, half_dt, full_dt, s);
         if (!rc) rc = sph_halo_exchange(e, comm, plan, SPH_HALO_RP_NEXT, 1, s);
-        if (!rc) rc = sph_engine_phase(e, SPH_PHASE_MOMENTUM, half_dt, full_dt, s);
+        // all but the last sub-step: the momentum sweep also applies the next
+        // sub-step's kick + drift to owned fluid (its KICK_DRIFT phase is then
+        // a no-op; the XV refresh after it still updates the ghosts)
+        if (!rc) rc = sph_engine_phase(e, k + 1 < nsub ? SPH_PHASE_MOMENTUM_NEXT
+                                                       : SPH_PHASE_MOMENTUM,
+                                       half_dt, full_dt, s);
     }
     return rc;
 }

@@ -424,14 +424,15 @@ class DistributedSimulation:
             # the engine enqueues the sub-steps with their NCCL refreshes itself
             self.backend.substeps(half, full, nsub)
         else:
-            for _ in range(nsub):
+            for k in range(nsub):
                 self.backend.kick_drift(half, full)
                 self._refresh(XV, "fluid")
                 self.backend.continuity_du(full)
                 self._refresh(RP_NEXT, "fluid")
                 self.backend.wall_pressure()
                 self._refresh(RP_NEXT, "wall")
-                self.backend.momentum_kick(half)
+                # the next sub-step's kick + drift may be fused into this sweep
+                self.backend.momentum_kick(half, full if k + 1 < nsub else None)
         self.last_nsub = nsub
         self._finish_counts()
         self.step_count += 1
@@ -711,9 +712,13 @@ class EngineBackend:
     def wall_pressure(self, initial=False):
         self._phase(self._native.PHASE_INIT_WALL if initial else self._native.PHASE_WALL)
 
-    def momentum_kick(self, half):
+    def momentum_kick(self, half, next_full=None):
+        """MOMENTUM (+ KICK); with next_full also the next sub-step's KICK +
+        DRIFT of owned fluid (its kick_drift call is then a no-op)."""
         if half is None:
             self._phase(self._native.PHASE_INIT_MOMENTUM)
+        elif next_full is not None:
+            self._phase(self._native.PHASE_MOMENTUM_NEXT, half, next_full)
         else:
             self._phase(self._native.PHASE_MOMENTUM, half, 0.0)
 

@@ -102,7 +102,9 @@ class OracleBackend:
         w = f["wall"][:n] != 0
         self._inter += int(f["nnb"][:n][w].sum())
 
-    def momentum_kick(self, half):
+    def momentum_kick(self, half, next_full=None):
+        # next_full: the engine may fuse the next kick + drift; the oracle
+        # composition runs them in the next kick_drift call instead
         f = self.f
         O.sweep("momentum", self._force(), box=self.box)
         self._ovf_check()
