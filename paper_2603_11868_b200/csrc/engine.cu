@@ -33,8 +33,15 @@
 #ifndef SPH_SWEEP_MINB
 #define SPH_SWEEP_MINB 12    // min resident blocks of the sweeps (register cap)
 #endif
-#ifndef SPH_CONT_MINB
-#define SPH_CONT_MINB (D == 3 ? 10 : 12)
+#ifndef SPH_CONT_MINB         // fused skin filter (3D: 8 measured -14% vs 10)
+#define SPH_CONT_MINB (D == 3 ? 8 : 12)
+#endif
+#ifndef SPH_CONT_EXACT_MINB   // exact-list walk (split filtering)
+#if SPH_PERIODIC
+#define SPH_CONT_EXACT_MINB (D == 3 ? 8 : 12)
+#else
+#define SPH_CONT_EXACT_MINB (D == 3 ? 10 : 12)
+#endif
 #endif
 #ifndef SPH_MOM_MINB
 #define SPH_MOM_MINB 8       // the momentum sweep holds more live state
@@ -1053,9 +1060,9 @@ __device__ __forceinline__ void flag_overflow(const Eng<T>& E, int64_t i)
 // fluid only: reads rho of the current buffer, writes (rho, p) to the other.
 // A particle with a valid skin list filters it here (writing the exact list
 // the momentum sweep reuses); others read the exact list k_fix_build made.
-template <class T, int D>
-__global__ void __launch_bounds__(kSweepThreads, SPH_CONT_MINB)
-k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full, int exact)
+template <class T, int D, bool EXACT>
+__global__ void __launch_bounds__(kSweepThreads, EXACT ? SPH_CONT_EXACT_MINB : SPH_CONT_MINB)
+k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= E.nf) return;
@@ -1076,7 +1083,7 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full, int exact)
         acc = dadd(acc, continuity_term<T>(r2, vx, nb.v.w, P));   // v.w = m_j/rho_j
     };
     int cnt;
-    if (exact || E.cell0[i] == kInvalidCell) {   // exact list from k_mask / k_fix_build
+    if (EXACT || E.cell0[i] == kInvalidCell) {   // exact list from k_mask / k_fix_build
         cnt = E.acount[i];
         if (cnt < 0) { flag_overflow(E, i); return; }
         sweep_list<T>(E, i, cnt, loadf, pair);
@@ -1602,10 +1609,14 @@ static void sub_continuity(SphEngine* e, T full, cudaStream_t s)
 {
     Eng<T> E = eng_of<T>(e);
     const int crp = e->cur_rp;
-    if (e->nf > 0)
-        note_launch(), k_cont_du<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full,
-            split_filter(e) ? 1 : 0);
+    if (e->nf > 0 && split_filter(e))
+        note_launch(), k_cont_du<T, D, true><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0,
+                                              s>>>(
+            E, make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full);
+    else if (e->nf > 0)
+        note_launch(), k_cont_du<T, D, false><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0,
+                                               s>>>(
+            E, make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full);
     else if (e->n > 0)   // no fluid: the other rp buffer must still carry walls
         cudaMemcpyAsync(E.rp[crp ^ 1], E.rp[crp], sizeof(vec2<T>) * (size_t)e->n,
                         cudaMemcpyDeviceToDevice, s);
