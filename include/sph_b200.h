@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 6
+#define SPH_ABI_VERSION 7
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -249,6 +249,10 @@ typedef struct {
      * cell change re-bases it; disp itself always measures the path since
      * the step's list build, which bounds every neighbour's motion) */
     void* disp0;
+    /* host hint: 1 when the previous step refreshed few lists, so the
+     * sub-step's list check and refreshes run as one queue-free pass */
+    int32_t few_refreshes;
+    int32_t reserved0;
 } SphEngine;
 
 size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64);

@@ -101,10 +101,11 @@ class SphEngine(C.Structure):
         ("cur_v", c_i32), ("cur_rp", c_i32), ("cur_pos", c_i32), ("drifted", c_i32), ("f64", c_i32), ("lists_ready", c_i32),
         ("period", c_f64 * 3),
         ("disp0", P),
+        ("few_refreshes", c_i32), ("reserved0", c_i32),
     ]
 
 
-ABI_VERSION = 6   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 7   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)

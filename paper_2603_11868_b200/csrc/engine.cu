@@ -43,6 +43,9 @@
 #define SPH_CONT_EXACT_MINB (D == 3 ? 10 : 12)
 #endif
 #endif
+#ifndef SPH_MARK_FUSED        // sub-step list check + refresh in one queue-free kernel
+#define SPH_MARK_FUSED 1
+#endif
 #ifndef SPH_MOM_MINB          // the momentum sweep holds more live state
 #define SPH_MOM_MINB (D == 2 ? 9 : 8)   // (2D 9: -1%; 3D 9/10: no gain, spills)
 #endif
@@ -976,6 +979,66 @@ k_mark(Eng<T> E, T s_eff)
 // (its 0 < r2 < c^2 subset, same order).  A particle whose skin candidates
 // exceed the capacity gets the exact list only and stays queued.
 template <class T, int D>
+__device__ __forceinline__ void refresh_one(const EngAcc<T>& acc, const GridP<T>& g,
+                                            const Eng<T>& E, T cs2, int64_t i, WarpBuf& sb,
+                                            uint32_t* srt, unsigned lane, unsigned lt)
+{
+    const int64_t slot = slot_of(E, i);
+    const bool fluid = i < E.nf;
+    T xi[3];
+    acc.position(i, xi);
+    CollectCounts cc = warp_collect<T, D, true>(acc, g, i, xi, cs2, fluid ? 3u : 1u, sb);
+    if (cc.stored <= kCap) {
+        warp_emit_sorted(sb, cc.stored, lane, [&](int pos, uint32_t j) {
+            E.lists[ell_index(slot, pos)] = (int32_t)j;
+            srt[pos] = j;
+        });
+        // the exact subset in list order
+        int ex = 0;
+        for (int b = 0; b < cc.stored; b += 32) {
+            const int k = b + (int)lane;
+            bool ok = false;
+            uint32_t j = 0;
+            if (k < cc.stored) {
+                j = srt[k];
+                T xj[3];
+                acc.position(j, xj);
+                const T r2 = accept_r2<T, D>(xi, xj);
+                ok = (r2 < g.c2) && (r2 > T(0));
+            }
+            const unsigned bl = __ballot_sync(0xffffffffu, ok);
+            if (ok) E.elist[ell_index(slot, ex + __popc(bl & lt))] = (int32_t)j;
+            ex += __popc(bl);
+        }
+        // walls: wall-wall neighbours count toward the capacity (nww)
+        const int total = ex + (fluid ? 0 : cc.accepted);
+        if (lane == 0) {
+            int cxyz[3];
+            E.acount[slot] = total > kCap ? -1 : ex;
+            E.cell0[i] = cell_key_of<T, D>(xi, g, cxyz);
+            E.lcount[slot] = cc.stored;
+            E.nww[slot] = cc.accepted;
+            E.disp0[i] = E.disp[i];
+        }
+    } else {   // skin list over capacity: this sub-step's exact list only
+        __syncwarp();
+        CollectCounts ce = warp_collect<T, D, false>(acc, g, i, xi, T(0), fluid ? 3u : 1u,
+                                                     sb);
+        if (ce.accepted > kCap) {
+            if (lane == 0) E.acount[slot] = -1;
+        } else {
+            warp_emit_sorted(sb, ce.stored, lane, [&](int pos, uint32_t j) {
+                E.elist[ell_index(slot, pos)] = (int32_t)j;
+            });
+            if (lane == 0) E.acount[slot] = ce.stored;
+        }
+        if (lane == 0) E.cell0[i] = kInvalidCell;
+    }
+    if (lane == 0) atomicAdd(&E.stats->nfix, 1u);
+    __syncwarp();
+}
+
+template <class T, int D>
 __global__ void __launch_bounds__(kNlThreads, 4)
 k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E, T cs2)
 {
@@ -984,63 +1047,42 @@ k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E, T cs2)
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
     const uint32_t qn = *(volatile uint32_t*)E.qcount;
-    WarpBuf& sb = bufs[warp];
-    uint32_t* srt = sorted[warp];
-    for (uint32_t q = blockIdx.x * kNlWarps + warp; q < qn; q += gridDim.x * kNlWarps) {
-        const int64_t i = E.queue[q];
-        const int64_t slot = slot_of(E, i);
-        const bool fluid = i < E.nf;
-        T xi[3];
-        acc.position(i, xi);
-        CollectCounts cc = warp_collect<T, D, true>(acc, g, i, xi, cs2, fluid ? 3u : 1u, sb);
-        if (cc.stored <= kCap) {
-            warp_emit_sorted(sb, cc.stored, lane, [&](int pos, uint32_t j) {
-                E.lists[ell_index(slot, pos)] = (int32_t)j;
-                srt[pos] = j;
-            });
-            // the exact subset in list order
-            int ex = 0;
-            for (int b = 0; b < cc.stored; b += 32) {
-                const int k = b + (int)lane;
-                bool ok = false;
-                uint32_t j = 0;
-                if (k < cc.stored) {
-                    j = srt[k];
-                    T xj[3];
-                    acc.position(j, xj);
-                    const T r2 = accept_r2<T, D>(xi, xj);
-                    ok = (r2 < g.c2) && (r2 > T(0));
-                }
-                const unsigned bl = __ballot_sync(0xffffffffu, ok);
-                if (ok) E.elist[ell_index(slot, ex + __popc(bl & lt))] = (int32_t)j;
-                ex += __popc(bl);
+    for (uint32_t q = blockIdx.x * kNlWarps + warp; q < qn; q += gridDim.x * kNlWarps)
+        refresh_one<T, D>(acc, g, E, cs2, (int64_t)E.queue[q], bufs[warp], sorted[warp], lane,
+                          lt);
+}
+
+// The sub-step's list check and refresh in one pass (no queue): each warp
+// tests 32 consecutive particles (k_mark's criterion) and refreshes the
+// ones it finds invalid itself, so scattered refreshes spread over all warps.
+template <class T, int D>
+__global__ void __launch_bounds__(kNlThreads, 4)
+k_mark_refresh(const EngAcc<T> acc, const GridP<T> g, Eng<T> E, T cs2, T s_eff)
+{
+    __shared__ WarpBuf bufs[kNlWarps];
+    __shared__ uint32_t sorted[kNlWarps][kCap];
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const unsigned lt = lanemask_lt();
+    const T dmax = T(__longlong_as_double((long long)E.stats->dmax_bits));
+    for (int64_t base = ((int64_t)blockIdx.x * kNlWarps + warp) * 32; base < E.n;
+         base += (int64_t)gridDim.x * kNlWarps * 32) {
+        const int64_t i = base + lane;
+        bool need = false;
+        if (i < E.n) {
+            if (E.cell0[i] == kInvalidCell) {
+                need = true;
+            } else if (RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax) > s_eff) {
+                E.cell0[i] = kInvalidCell;
+                need = true;
+                atomicAdd(&E.stats->ndisp, 1u);
             }
-            // walls: wall-wall neighbours count toward the capacity (nww)
-            const int total = ex + (fluid ? 0 : cc.accepted);
-            if (lane == 0) {
-                int cxyz[3];
-                E.acount[slot] = total > kCap ? -1 : ex;
-                E.cell0[i] = cell_key_of<T, D>(xi, g, cxyz);
-                E.lcount[slot] = cc.stored;
-                E.nww[slot] = cc.accepted;
-                E.disp0[i] = E.disp[i];
-            }
-        } else {   // skin list over capacity: this sub-step's exact list only
-            __syncwarp();
-            CollectCounts ce = warp_collect<T, D, false>(acc, g, i, xi, T(0), fluid ? 3u : 1u,
-                                                         sb);
-            if (ce.accepted > kCap) {
-                if (lane == 0) E.acount[slot] = -1;
-            } else {
-                warp_emit_sorted(sb, ce.stored, lane, [&](int pos, uint32_t j) {
-                    E.elist[ell_index(slot, pos)] = (int32_t)j;
-                });
-                if (lane == 0) E.acount[slot] = ce.stored;
-            }
-            if (lane == 0) E.cell0[i] = kInvalidCell;
         }
-        if (lane == 0) atomicAdd(&E.stats->nfix, 1u);
-        __syncwarp();
+        unsigned m = __ballot_sync(0xffffffffu, need);
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            refresh_one<T, D>(acc, g, E, cs2, base + l, bufs[warp], sorted[warp], lane, lt);
+        }
     }
 }
 
@@ -1470,8 +1512,19 @@ template <class T, int D>
 static void mark_and_fix(const SphEngine* e, cudaStream_t s)
 {
     Eng<T> E = eng_of<T>(e);
-    cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
     if (e->n <= 0) return;
+    // few refreshes expected (host hint from the previous step): check +
+    // refresh in one pass; otherwise the queue spreads the (spatially
+    // clustered) refreshes over more warps (measured with the one-pass
+    // kernel: 2D at rest -3 us per sub-step, at step 40 +27 us)
+    if (SPH_MARK_FUSED && e->few_refreshes) {
+        const int64_t want = (e->n + kNlThreads - 1) / kNlThreads;
+        const int blocks = (int)(want < 148 * 4 ? want : 148 * 4);
+        note_launch(), k_mark_refresh<T, D><<<blocks, kNlThreads, 0, s>>>(
+            acc_of_engine<T>(e), grid_of_engine<T>(e), E, skin_cs2<T>(e), skin_eff<T>(e));
+        return;
+    }
+    cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
     note_launch(), k_mark<T><<<grid_for(e->n, 256), 256, 0, s>>>(E, skin_eff<T>(e));
     launch_fix<T, D>(e, s);
 }

@@ -766,6 +766,8 @@ class Simulation:
         self._host_stale = True
         self.last_nsub = nsub
         self.last_nfix = int(stats.nfix)
+        # list refreshes were rare: the next step checks and refreshes in one pass
+        d["E"].few_refreshes = int(stats.nfix < 2e-4 * max(1, self.registry.particle_count) * nsub)
         self._adapt_skin(stats.ndisp, nsub)
         self.out_of_bounds += stats.oob + self._oob_walls
         self._finish_counts(stats, check=True)
