@@ -1231,6 +1231,88 @@ k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor,
     add_interactions(E.stats, visits_sum);
 }
 
+// WALL_PRESSURE with G lanes per wall: lane q evaluates list entries
+// q, q + G, ... (gather, exact test, Shepard weight and p_j * w -- the
+// expensive part), then every lane of the group adds the G terms in list
+// order (shuffles), so the binary64 sums follow the reference's order bit
+// for bit.  A thread per wall leaves most SMs idle (a few tens of thousands
+// of walls, each a serial chain of dependent gathers).
+#ifndef SPH_WALL_LANES   // 2D: 8 (wall pressure 14 -> 12 us per sub-step); 3D: most
+#define SPH_WALL_LANES (D == 2 ? 8 : 1)   // walls have no fluid neighbour (G=8: 3x slower)
+#endif
+template <class T, int D, int G>
+__global__ void __launch_bounds__(kSweepThreads)
+k_wall_g(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor, int filter,
+         int cvn)
+{
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const unsigned lane = lane_id(), q = lane & (G - 1);
+    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane & ~(G - 1));
+    unsigned long long visits_sum = 0;
+    if (gid < E.nw) {   // uniform across the group
+        const int64_t i = E.nf + gid;
+        const int64_t slot = E.nf_pad + gid;
+        vec2<T>* __restrict__ rp = E.rp[b];
+        T xi[3];
+        to3<T>(E.pos[i], xi);
+        const T rho_i = rp[i].x;
+        double num = double(RN<T>::sub(rho_i, rho_i));
+        double den = num;
+        const bool exact = !filter || E.cell0[i] == kInvalidCell;
+        const int nl = exact ? E.acount[slot] : E.lcount[slot];
+        const int32_t* __restrict__ lp = (exact ? E.elist : E.lists) + ell_base(slot);
+        int acnt = exact ? nl : 0;
+        for (int base = 0; base < nl; base += G) {
+            const int e = base + (int)q;
+            bool ok = false;
+            double tn = 0.0, tw = 0.0;
+            if (e < nl) {
+                const int j = lp[ell_off(e)];
+                const vec4<T> pj = E.pos[j];
+                T xj[3];
+                to3<T>(pj, xj);
+                const T r2 = pair_r2<T, D>(xi, xj);
+                ok = exact || ((r2 < g.c2) && (r2 > T(0)));
+                if (ok) {
+                    tw = wall_weight<T>(r2, P);
+                    tn = dmul(double(rp[j].y), tw);
+                }
+            }
+            const unsigned okm = __ballot_sync(gmask, ok) >> (lane & ~(G - 1));
+#pragma unroll
+            for (int k = 0; k < G; k++) {
+                const double an = __shfl_sync(gmask, tn, k, G);
+                const double aw = __shfl_sync(gmask, tw, k, G);
+                if ((okm >> k) & 1u) {
+                    num = dadd(num, an);
+                    den = dadd(den, aw);
+                }
+            }
+            if (!exact) acnt += __popc(okm);
+        }
+        if (!exact && acnt + E.nww[slot] > kCap) acnt = -1;
+        if (q == 0) {
+            if (!exact) E.acount[slot] = acnt;
+            if (acnt < 0) {
+                flag_overflow(E, i);
+            } else {
+                vec2<T> out;
+                out.y = den > 0.0 ? RN<T>::from_d(ddiv(num, den)) : T(0);
+                out.x = RN<T>::add(P.rho0, RN<T>::div(out.y, P.c0c0));
+                rp[i] = out;
+                E.rq[i] = rq_of<T>(out);
+                if (cvn >= 0)
+                    reinterpret_cast<T*>(&E.vel[cvn][i])[3] = RN<T>::div(E.pos[i].w, out.x);
+                E.nnb[i] = (uint32_t)acnt;
+                if (zero_drho) E.drho[i] = T(0);
+                if (is_owned(E, i))
+                    visits_sum = (unsigned long long)acnt * (unsigned long long)count_factor;
+            }
+        }
+    }
+    add_interactions(E.stats, visits_sum);
+}
+
 // physics.py:122-158 MOMENTUM (+ :546-547 KICK(half) into the other velocity
 // buffer when kick != 0), fluid only; rho/p from buffer brp.
 //
@@ -1548,8 +1630,13 @@ static void launch_wall(const SphEngine* e, int b, int zero_drho, int count_fact
     const GridP<T> g = grid_of_engine<T>(e);
     // a thread per wall: a warp per wall with an ordered shuffle chain for
     // the sums measured 1.4x (2D) to 7x (3D) slower
-    note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
-        E, P, g, b, zero_drho, count_factor, filter, cvn);
+    if (SPH_WALL_LANES > 1)
+        note_launch(), k_wall_g<T, D, (SPH_WALL_LANES > 1 ? SPH_WALL_LANES : 2)>
+            <<<grid_for(nw * SPH_WALL_LANES, kSweepThreads), kSweepThreads, 0, s>>>(
+                E, P, g, b, zero_drho, count_factor, filter, cvn);
+    else
+        note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
+            E, P, g, b, zero_drho, count_factor, filter, cvn);
 }
 
 // physics.py:460-467 initialize, in its two halo-exchange phases: exact
