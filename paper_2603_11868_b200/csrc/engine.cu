@@ -1064,24 +1064,51 @@ k_mark_refresh(const EngAcc<T> acc, const GridP<T> g, Eng<T> E, T cs2, T s_eff)
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
     const T dmax = T(__longlong_as_double((long long)E.stats->dmax_bits));
-    for (int64_t base = ((int64_t)blockIdx.x * kNlWarps + warp) * 32; base < E.n;
-         base += (int64_t)gridDim.x * kNlWarps * 32) {
-        const int64_t i = base + lane;
-        bool need = false;
-        if (i < E.n) {
-            if (E.cell0[i] == kInvalidCell) {
-                need = true;
-            } else if (RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax) > s_eff) {
+    // 4 consecutive particles per lane (vector loads), 128 per warp trip
+    for (int64_t base = ((int64_t)blockIdx.x * kNlWarps + warp) * 128; base < E.n;
+         base += (int64_t)gridDim.x * kNlWarps * 128) {
+        const int64_t i0 = base + 4 * lane;
+        uint32_t c4[4] = {0, 0, 0, 0};
+        T d4[4] = {0, 0, 0, 0}, e4[4] = {0, 0, 0, 0};
+        if (sizeof(T) == 4 && i0 + 3 < E.n) {
+            const uint4 c = *reinterpret_cast<const uint4*>(E.cell0 + i0);
+            const float4 d = *reinterpret_cast<const float4*>(E.disp + i0);
+            const float4 z = *reinterpret_cast<const float4*>(E.disp0 + i0);
+            c4[0] = c.x; c4[1] = c.y; c4[2] = c.z; c4[3] = c.w;
+            d4[0] = d.x; d4[1] = d.y; d4[2] = d.z; d4[3] = d.w;
+            e4[0] = z.x; e4[1] = z.y; e4[2] = z.z; e4[3] = z.w;
+        } else {
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (i0 + r < E.n) {
+                    c4[r] = E.cell0[i0 + r];
+                    d4[r] = E.disp[i0 + r];
+                    e4[r] = E.disp0[i0 + r];
+                }
+        }
+        unsigned bits = 0;
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const int64_t i = i0 + r;
+            if (i >= E.n) continue;
+            if (c4[r] == kInvalidCell) {
+                bits |= 1u << r;
+            } else if (RN<T>::add_ru(RN<T>::sub_ru(d4[r], e4[r]), dmax) > s_eff) {
                 E.cell0[i] = kInvalidCell;
-                need = true;
+                bits |= 1u << r;
                 atomicAdd(&E.stats->ndisp, 1u);
             }
         }
-        unsigned m = __ballot_sync(0xffffffffu, need);
+        unsigned m = __ballot_sync(0xffffffffu, bits != 0);
         while (m) {
             const int l = __ffs(m) - 1;
             m &= m - 1;
-            refresh_one<T, D>(acc, g, E, cs2, base + l, bufs[warp], sorted[warp], lane, lt);
+            const unsigned bl = __shfl_sync(0xffffffffu, bits, l);
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if ((bl >> r) & 1u)
+                    refresh_one<T, D>(acc, g, E, cs2, base + 4 * l + r, bufs[warp],
+                                      sorted[warp], lane, lt);
         }
     }
 }
@@ -1600,7 +1627,7 @@ static void mark_and_fix(const SphEngine* e, cudaStream_t s)
     // clustered) refreshes over more warps (measured with the one-pass
     // kernel: 2D at rest -3 us per sub-step, at step 40 +27 us)
     if (SPH_MARK_FUSED && e->few_refreshes) {
-        const int64_t want = (e->n + kNlThreads - 1) / kNlThreads;
+        const int64_t want = (e->n + 4 * kNlThreads - 1) / (4 * kNlThreads);
         const int blocks = (int)(want < 148 * 4 ? want : 148 * 4);
         note_launch(), k_mark_refresh<T, D><<<blocks, kNlThreads, 0, s>>>(
             acc_of_engine<T>(e), grid_of_engine<T>(e), E, skin_cs2<T>(e), skin_eff<T>(e));
