@@ -65,7 +65,12 @@ def build_library(force=False, verbose=False, extra_flags=(), out=None):
     """Build the library (to `out`, default the in-tree path; the default
     build also produces the periodic-box variant)."""
     if out is None and not extra_flags:
-        _build_one(force, verbose, PERIODIC_FLAGS, LIB_PERIODIC)
+        # both libraries at once: their engine.cu compiles are the long poles
+        with cf.ThreadPoolExecutor(max_workers=2) as ex:
+            per = ex.submit(_build_one, force, verbose, PERIODIC_FLAGS, LIB_PERIODIC)
+            lib = ex.submit(_build_one, force, verbose, extra_flags, out)
+            per.result()
+            return lib.result()
     return _build_one(force, verbose, extra_flags, out)
 
 
