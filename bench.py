@@ -139,24 +139,41 @@ class ClockSampler:
         self.index = index
         self.rows = []
         self.proc = None
+        self.t0 = self.t1 = None
 
     def start(self):
+        """Spawn the sampler (20 ms period) and wait for its first row, so the
+        timed region that follows is covered from its start."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        deadline = time.perf_counter() + 5.0
+        while not self.rows and time.perf_counter() < deadline:
+            time.sleep(0.005)
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.perf_counter(), [c.strip() for c in line.split(",")]))
 
     def stop(self):
+        # samples read within the timed region (one period of slack after it)
+        if self.t0 is not None:
+            t1 = (self.t1 or time.perf_counter()) + 0.025
+            self.rows = [r for r in self.rows if self.t0 <= r[0] <= t1]
+        self.rows = [r[1] if isinstance(r, tuple) else r for r in self.rows]
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -263,11 +280,12 @@ def gpu_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     sampler = ClockSampler(local_rank)
+    sampler.start()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     launches0 = lib.sph_kernel_launches()
-    sampler.start()
+    sampler.mark_start()
     times, nsubs = [], []
     for _ in range(args.steps):
         flush.zero_()
@@ -280,6 +298,7 @@ def gpu_arm(args, rank, world, local_rank):
         times.append(ev0.elapsed_time(ev1) / 1e3)
         nsubs.append(sim.last_nsub)
     torch.cuda.synchronize()
+    sampler.mark_end()
     clocks = sampler.stop()
     launches = lib.sph_kernel_launches() - launches0 - 0
     total = sum(times)
@@ -408,10 +427,11 @@ def slab_arm(args, rank, world, local_rank):
     torch.cuda.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     sampler = ClockSampler(local_rank)
+    sampler.start()
     torch.distributed.barrier()
     torch.cuda.synchronize()
     launches0 = lib.sph_kernel_launches()
-    sampler.start()
+    sampler.mark_start()
     times, nsubs = [], []
     for _ in range(args.steps):
         flush.zero_()
@@ -424,6 +444,7 @@ def slab_arm(args, rank, world, local_rank):
         times.append(ev0.elapsed_time(ev1) / 1e3)
         nsubs.append(sim.last_nsub)
     torch.cuda.synchronize()
+    sampler.mark_end()
     clocks = sampler.stop()
     launches = lib.sph_kernel_launches() - launches0
     total = float(comm.allreduce([sum(times)], "max")[0])
@@ -528,7 +549,7 @@ def e2e_run(sim, reg, steps, world, dev):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="2d1m")

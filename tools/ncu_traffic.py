@@ -13,7 +13,7 @@ import sys
 
 # csrc kernel -> bench.py sub-step name (physics.SUBSTEP_KERNELS)
 NAMES = {"k_kick_drift": "kick_drift", "k_cont_du": "continuity_du",
-         "k_wall": "wall_pressure", "k_mom": "momentum_kick",
+         "k_wall": "wall_pressure", "k_wall_g": "wall_pressure", "k_mark_refresh": "list_filter", "k_mom": "momentum_kick",
          "k_skin_tile": "skin_build", "k_skin_warp": "skin_build", "k_mark": "list_filter",
          "k_mask": "list_filter"}
 

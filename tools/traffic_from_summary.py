@@ -7,7 +7,7 @@ import re
 import sys
 
 NAMES = {"k_kick_drift": "kick_drift", "k_cont_du": "continuity_du",
-         "k_wall": "wall_pressure", "k_mom": "momentum_kick", "k_mark": "list_filter",
+         "k_wall": "wall_pressure", "k_wall_g": "wall_pressure", "k_mark_refresh": "list_filter", "k_mom": "momentum_kick", "k_mark": "list_filter",
          "k_mask": "list_filter", "k_skin_tile": "skin_build", "k_skin_warp": "skin_build"}
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
