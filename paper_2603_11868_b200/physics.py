@@ -518,6 +518,7 @@ class Simulation:
         self.kernel_times = None    # dict name -> [ms per launch] when profiling
         self._skin_factor = 3.0
         self.last_nfix = 0
+        self.list_refresh = "auto"  # sub-step list upkeep: auto | pass | queue
         registry.attach_engine(self)
 
     def _lib(self):
@@ -766,8 +767,13 @@ class Simulation:
         self._host_stale = True
         self.last_nsub = nsub
         self.last_nfix = int(stats.nfix)
-        # list refreshes were rare: the next step checks and refreshes in one pass
-        d["E"].few_refreshes = int(stats.nfix < 2e-4 * max(1, self.registry.particle_count) * nsub)
+        # list refreshes were rare: the next step checks and refreshes in one
+        # pass (list_refresh "auto"); "pass" / "queue" force one of the paths
+        if self.list_refresh == "auto":
+            few = stats.nfix < 2e-4 * max(1, self.registry.particle_count) * nsub
+        else:
+            few = self.list_refresh == "pass"
+        d["E"].few_refreshes = int(few)
         self._adapt_skin(stats.ndisp, nsub)
         self.out_of_bounds += stats.oob + self._oob_walls
         self._finish_counts(stats, check=True)
