@@ -169,11 +169,6 @@ class ClockSampler:
             self.rows.append((time.perf_counter(), [c.strip() for c in line.split(",")]))
 
     def stop(self):
-        # samples read within the timed region (one period of slack after it)
-        if self.t0 is not None:
-            t1 = (self.t1 or time.perf_counter()) + 0.025
-            self.rows = [r for r in self.rows if self.t0 <= r[0] <= t1]
-        self.rows = [r[1] if isinstance(r, tuple) else r for r in self.rows]
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -182,6 +177,12 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.thread.join(timeout=5)
+        # samples read within the timed region (one period of slack after it)
+        rows = list(self.rows)
+        if self.t0 is not None:
+            t1 = (self.t1 or time.perf_counter()) + 0.025
+            rows = [r for r in rows if self.t0 <= r[0] <= t1]
+        self.rows = [r[1] for r in rows]
         sm, mx, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
                  "sw_power_cap")

@@ -953,22 +953,42 @@ template <class T>
 __global__ void __launch_bounds__(256)
 k_mark(Eng<T> E, T s_eff)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool need = false;
-    if (i < E.n) {
-        const uint32_t c0 = E.cell0[i];
-        if (c0 == kInvalidCell) {
-            need = true;
-        } else {
-            const T dmax = T(__longlong_as_double((long long)E.stats->dmax_bits));
-            if (RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax) > s_eff) {
+    // 4 consecutive particles per thread (vector loads)
+    const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    const T dmax = T(__longlong_as_double((long long)E.stats->dmax_bits));
+    uint32_t c4[4] = {0, 0, 0, 0};
+    T d4[4] = {0, 0, 0, 0}, e4[4] = {0, 0, 0, 0};
+    if (sizeof(T) == 4 && i0 + 3 < E.n) {
+        const uint4 c = *reinterpret_cast<const uint4*>(E.cell0 + i0);
+        const float4 d = *reinterpret_cast<const float4*>(E.disp + i0);
+        const float4 z = *reinterpret_cast<const float4*>(E.disp0 + i0);
+        c4[0] = c.x; c4[1] = c.y; c4[2] = c.z; c4[3] = c.w;
+        d4[0] = d.x; d4[1] = d.y; d4[2] = d.z; d4[3] = d.w;
+        e4[0] = z.x; e4[1] = z.y; e4[2] = z.z; e4[3] = z.w;
+    } else {
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+            if (i0 + r < E.n) {
+                c4[r] = E.cell0[i0 + r];
+                d4[r] = E.disp[i0 + r];
+                e4[r] = E.disp0[i0 + r];
+            }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const int64_t i = i0 + r;
+        bool need = false;
+        if (i < E.n) {
+            if (c4[r] == kInvalidCell) {
+                need = true;
+            } else if (RN<T>::add_ru(RN<T>::sub_ru(d4[r], e4[r]), dmax) > s_eff) {
                 E.cell0[i] = kInvalidCell;
                 need = true;
                 atomicAdd(&E.stats->ndisp, 1u);
             }
         }
+        enqueue(E.queue, E.qcount, need, (uint32_t)i);
     }
-    enqueue(E.queue, E.qcount, need, (uint32_t)i);
 }
 
 // List refresh of the queued particles (cell changed, or own displacement
@@ -1634,7 +1654,7 @@ static void mark_and_fix(const SphEngine* e, cudaStream_t s)
         return;
     }
     cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
-    note_launch(), k_mark<T><<<grid_for(e->n, 256), 256, 0, s>>>(E, skin_eff<T>(e));
+    note_launch(), k_mark<T><<<grid_for((e->n + 3) / 4, 256), 256, 0, s>>>(E, skin_eff<T>(e));
     launch_fix<T, D>(e, s);
 }
 
