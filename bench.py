@@ -71,17 +71,21 @@ def tg_side(name, world=1):
     return int(round(CONFIGS[name][1]["n"] * world ** (1.0 / 3.0)))
 
 
-def build_case(name, world=1):
+def case_config(name, world=1):
     from paper_2603_11868_b200 import cases
     spec = CONFIGS[name][1]
     if spec["kind"] == "tg":
-        return cases.build_case(cases.taylor_green_config(3, tg_side(name, world),
-                                                          precision="f32"))
+        return cases.taylor_green_config(3, tg_side(name, world), precision="f32")
     if spec["kind"] == "2d":
-        cfg = cases.CaseConfig(case="dambreak2d", dp=spec["dp"], precision="f32")
-    else:
-        cfg = cases.kleefsman_config(dp=spec["dp"], precision="f32")
-    return cases.build_case(cfg)
+        return cases.CaseConfig(case="dambreak2d", dp=spec["dp"], precision="f32")
+    return cases.kleefsman_config(dp=spec["dp"], precision="f32")
+
+
+def build_case(name, world=1):
+    """Host placement (the reference's numpy lattice restated): the CPU arms
+    and the slab path start from it."""
+    from paper_2603_11868_b200 import cases
+    return cases.build_case(case_config(name, world))
 
 
 def data_label(name):
@@ -268,13 +272,27 @@ def gpu_arm(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     from paper_2603_11868_b200.physics import grid_is_periodic
-    reg, grid = build_case(args.config)
+    from paper_2603_11868_b200 import cases
+    cfg = case_config(args.config)
+    t_setup = time.perf_counter()
+    if CONFIGS[args.config][1]["kind"] == "tg":   # analytic field: host numpy
+        reg, grid = cases.build_case(cfg)
+        state, setup = None, "host placement (cases.build_case)"
+    else:                                         # lattice placement on the device
+        reg, grid, state = cases.build_case_device(cfg, dev)
+        setup = "device placement (cases.build_case_device, csrc/cases.cu)"
     lib = _native.lib(periodic=grid_is_periodic(grid))
     n = reg.particle_count
     d = reg.dim
-    nw = int((reg.raw_view("wall") != 0).sum())
+    nw = int((reg.raw_view("wall") != 0).sum()) if state is None else \
+        int((state["wall"] != 0).sum().item())
     nf = n - nw
     sim = Simulation(reg, grid, ExecutionPolicy.cuda(local_rank))
+    if state is not None:
+        sim.load_device_state(state)
+        del state
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
     sim.initialize()
     for _ in range(args.warmup):
         sim.advance()
@@ -366,6 +384,7 @@ def gpu_arm(args, rank, world, local_rank):
                    "particles": n, "fluid": nf, "wall": nw, "grid_cells": ncells,
                    "nsub_per_step": nsubs, "l2": "flushed between steps (256 MB write)",
                    "parallelism": "single GPU",
+                   "setup": f"{setup}, {setup_s:.2f} s (untimed)",
                    "sub_step_updates_per_s": world * n * sum(nsubs) / total},
         "gpu_launches": int(launches),
         "clocks": clocks,
