@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import struct
 import time
 
@@ -471,6 +472,13 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
     return E, T
 
 
+# Verlet skin = factor x (vmax dt + amax dt^2) + 0.02 cutoff, the factor
+# adapted per step from the displacement-triggered refreshes (experiment
+# overrides through the environment)
+SKIN_FACTOR_START = float(os.environ.get("SPH_SKIN_START", "2.0"))
+SKIN_FACTOR_FLOOR = float(os.environ.get("SPH_SKIN_FLOOR", "0.5"))
+
+
 def grid_is_periodic(grid):
     per = getattr(grid, "period", None)
     return per is not None and any(float(p) > 0.0 for p in per)
@@ -516,7 +524,7 @@ class Simulation:
         self._norms = None          # (vmax, amax) valid for the device state
         self._oob_walls = 0
         self.kernel_times = None    # dict name -> [ms per launch] when profiling
-        self._skin_factor = 3.0
+        self._skin_factor = SKIN_FACTOR_START
         self.last_nfix = 0
         self.list_refresh = "auto"  # sub-step list upkeep: auto | pass | queue
         registry.attach_engine(self)
@@ -703,7 +711,7 @@ class Simulation:
         if frac > 2e-3:
             self._skin_factor = min(self._skin_factor * 1.5, 16.0)
         elif frac < 5e-4:
-            self._skin_factor = max(2.0, self._skin_factor * 0.95)
+            self._skin_factor = max(SKIN_FACTOR_FLOOR, self._skin_factor * 0.95)
 
     def advance(self, end_time=None):
         """One advective step (physics.py:489-552); returns the dt taken."""
