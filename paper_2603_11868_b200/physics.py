@@ -477,6 +477,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
 # overrides through the environment)
 SKIN_FACTOR_START = float(os.environ.get("SPH_SKIN_START", "2.0"))
 SKIN_FACTOR_FLOOR = float(os.environ.get("SPH_SKIN_FLOOR", "0.5"))
+SKIN_MARGIN = float(os.environ.get("SPH_SKIN_MARGIN", "0.02"))
 
 
 def grid_is_periodic(grid):
@@ -700,7 +701,7 @@ class Simulation:
         cutoff = float(self._dev["E"].cutoff)
         est = vmax * dt + amax * dt * dt
         cap = (0.45 if self.registry.dim == 3 else 1.0) * cutoff
-        return min(self._skin_factor * est + 0.02 * cutoff, cap)
+        return min(self._skin_factor * est + SKIN_MARGIN * cutoff, cap)
 
     def _adapt_skin(self, ndisp, nsub):
         """Grow the skin when displacement-triggered refreshes are frequent,
