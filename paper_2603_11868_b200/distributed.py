@@ -279,16 +279,16 @@ class DistributedSimulation:
         """Rows of every field to each neighbour in ONE message: the fields
         are viewed as int32 columns of one (n, width) matrix."""
         torch = self.comm.torch
-        n = int(fields["id"].shape[0])
         widths = [int(np.prod(fields[f].shape[1:], dtype=np.int64)) *
                   fields[f].element_size() // 4 for f in FIELDS]
-        if n:
-            packed = torch.cat([fields[f].reshape(n, -1).contiguous().view(torch.int32)
-                                for f in FIELDS], dim=1)
-        else:
-            packed = torch.empty((0, sum(widths)), dtype=torch.int32, device=self.comm.device)
-        got = self.comm.exchange({q: packed[r] for q, r in send_rows.items()}, recv_counts,
-                                 (sum(widths),), torch.int32)
+
+        def pack(rows):   # only the rows sent: the halo, not the whole rank
+            k = int(rows.numel())
+            return torch.cat([fields[f].index_select(0, rows).reshape(k, -1).view(torch.int32)
+                              for f in FIELDS], dim=1)
+
+        got = self.comm.exchange({q: pack(r) for q, r in send_rows.items() if r.numel()},
+                                 recv_counts, (sum(widths),), torch.int32)
         out = {f: {} for f in FIELDS}
         for q, m in got.items():
             c0 = 0
@@ -305,7 +305,9 @@ class DistributedSimulation:
         me = self.comm.rank
         dest = self.layout.owner(self._planes(self.owned["x"]))
         keep = dest == me
-        cnt = torch.bincount(dest, minlength=self.comm.size).cpu().tolist()
+        # per-rank counts as W reductions (a CUDA bincount into W bins
+        # serialises on a few global atomics)
+        cnt = torch.stack([(dest == q).sum() for q in range(self.comm.size)]).cpu().tolist()
         send_rows = {q: torch.nonzero(dest == q).flatten()
                      for q in range(self.comm.size) if q != me and cnt[q]}
         self.migrated += sum(cnt[q] for q in send_rows)
@@ -314,7 +316,8 @@ class DistributedSimulation:
         # any local order gives the same bits (sums run in id order); kept
         # particles first, then arrivals by source rank
         if send_rows or any(got[f] for f in ("id",)):
-            self.owned = {f: torch.cat([self.owned[f][keep]] +
+            kept = torch.nonzero(keep).flatten()
+            self.owned = {f: torch.cat([self.owned[f].index_select(0, kept)] +
                                        [got[f][q] for q in sorted(got[f])]) for f in FIELDS}
 
     def _build_local(self):
@@ -334,7 +337,7 @@ class DistributedSimulation:
         got = self._exchange_fields(self.owned, send_rows, recv_counts)
         n_own = int(self.owned["id"].shape[0])
         local = {f: torch.cat([self.owned[f]] + [got[f][q] for q in sorted(got[f])])
-                 for f in FIELDS}
+                 if got[f] else self.owned[f] for f in FIELDS}
         ghost_rows, off = {}, n_own
         for q in sorted(recv_counts):
             ghost_rows[q] = torch.arange(off, off + recv_counts[q], device=self.comm.device)
@@ -650,11 +653,11 @@ class EngineBackend:
         wall = local["wall"]
         nf = int((wall == 0).sum())
         self._ensure(n, nf, n - nf)
-        gid = local["id"].to(torch.int64)
-        order = torch.argsort(gid)
+        # local id = rank of the global id (ids < 2^31: a 32-bit key sort)
+        gid_sorted, order = torch.sort(local["id"])
         lid = torch.empty(n, dtype=torch.int32, device=self.device)
         lid[order] = torch.arange(n, dtype=torch.int32, device=self.device)
-        self.gid_of_lid = local["id"][order]
+        self.gid_of_lid = gid_sorted
         self.n, self.n_own = n, n_owned
         owned = self.T["owned_id"]
         owned[:n].zero_()
