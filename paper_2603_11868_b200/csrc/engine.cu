@@ -28,6 +28,7 @@
 //   k_mom         MOMENTUM + KICK (fluid), + the next sub-step's KICK + DRIFT
 //
 // Tuning knobs below were chosen by measurement.
+#include <type_traits>
 #include "engine.cuh"
 
 #ifndef SPH_SWEEP_MINB
@@ -51,6 +52,9 @@
 #endif
 #ifndef SPH_MASK_MINB
 #define SPH_MASK_MINB 12     // k_mask (split filtering): quad prefetch + staged stores
+#endif
+#ifndef SPH_SKIN_FLUID_PASS
+#define SPH_SKIN_FLUID_PASS 1   // k_skin_tile: fluid-pair passes without wall tests
 #endif
 #ifndef SPH_SKIN_THREADS_PER_SM
 #define SPH_SKIN_THREADS_PER_SM 1024   // skin-list build occupancy (register cap)
@@ -464,44 +468,54 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
             int32_t* __restrict__ lpA = E.lists + ell_base(slA);
             int32_t* __restrict__ lpB = E.lists + ell_base(slB);
             int cntA = 0, cntB = 0, naA = 0, naB = 0;
-            for (int base = 0; base < Mp; base += 32) {
-                const int k = base + (int)lane;
-                const uint32_t j = sj[k];
-                T xj[3];
-                to3<T>(spos[k], xj);
+            // FO: both particles fluid (warp-uniform; most passes) -- every
+            // candidate is eligible and no wall-wall count is kept
+            auto scan = [&](auto fo) {
+                constexpr bool FO = decltype(fo)::value;
+                for (int base = 0; base < Mp; base += 32) {
+                    const int k = base + (int)lane;
+                    const uint32_t j = sj[k];
+                    T xj[3];
+                    to3<T>(spos[k], xj);
 #if SPH_PERIODIC
-                const T r2a = tile_r2<T, D>(xa, xj);
+                    const T r2a = tile_r2<T, D>(xa, xj);
+                    const T r2b = tile_r2<T, D>(xb, xj);
 #else
-                const T r2a = accept_r2<T, D>(xa, xj);
+                    const T r2a = accept_r2<T, D>(xa, xj);
+                    const T r2b = accept_r2<T, D>(xb, xj);
 #endif
-#if SPH_PERIODIC
-                const T r2b = tile_r2<T, D>(xb, xj);
-#else
-                const T r2b = accept_r2<T, D>(xb, xj);
-#endif
-                const bool jf = (int64_t)j < nf;
-                const bool stA = (flA || jf) && r2a < cs2 && j != (uint32_t)iA;
-                const bool stB = hasB && (flB || jf) && r2b < cs2 && j != (uint32_t)iB;
-                const unsigned bA = __ballot_sync(0xffffffffu, stA);
-                const unsigned bB = __ballot_sync(0xffffffffu, stB);
-                if (stA) {
-                    const int p = cntA + __popc(bA & lt);
-                    if (p < kCap) lpA[ell_off(p)] = (int32_t)j;
-                }
-                if (stB) {
-                    const int p = cntB + __popc(bB & lt);
-                    if (p < kCap) lpB[ell_off(p)] = (int32_t)j;
-                }
-                cntA += __popc(bA);
-                cntB += __popc(bB);
-                if (!flA || !flB) {   // walls: static exact wall-wall count
-                    const bool ctA = !flA && !jf && r2a < g.c2 && r2a > T(0) && j != (uint32_t)iA;
-                    const bool ctB = hasB && !flB && !jf && r2b < g.c2 && r2b > T(0) &&
+                    const bool jf = FO || (int64_t)j < nf;
+                    const bool stA = (FO || flA || jf) && r2a < cs2 && j != (uint32_t)iA;
+                    const bool stB = (FO || hasB) && (FO || flB || jf) && r2b < cs2 &&
                                      j != (uint32_t)iB;
-                    naA += __popc(__ballot_sync(0xffffffffu, ctA));
-                    naB += __popc(__ballot_sync(0xffffffffu, ctB));
+                    const unsigned bA = __ballot_sync(0xffffffffu, stA);
+                    const unsigned bB = __ballot_sync(0xffffffffu, stB);
+                    if (stA) {
+                        const int p = cntA + __popc(bA & lt);
+                        if (p < kCap) lpA[ell_off(p)] = (int32_t)j;
+                    }
+                    if (stB) {
+                        const int p = cntB + __popc(bB & lt);
+                        if (p < kCap) lpB[ell_off(p)] = (int32_t)j;
+                    }
+                    cntA += __popc(bA);
+                    cntB += __popc(bB);
+                    if (!FO && (!flA || !flB)) {   // walls: static exact wall-wall count
+                        const bool ctA = !flA && !jf && r2a < g.c2 && r2a > T(0) &&
+                                         j != (uint32_t)iA;
+                        const bool ctB = hasB && !flB && !jf && r2b < g.c2 && r2b > T(0) &&
+                                         j != (uint32_t)iB;
+                        naA += __popc(__ballot_sync(0xffffffffu, ctA));
+                        naB += __popc(__ballot_sync(0xffffffffu, ctB));
+                    }
                 }
-            }
+            };
+#if SPH_SKIN_FLUID_PASS
+            if (flB) scan(std::true_type{});   // flB implies flA and hasB
+            else scan(std::false_type{});
+#else
+            scan(std::false_type{});
+#endif
             if (lane < 2 && (lane == 0 || hasB)) {
                 const int64_t i = lane ? iB : iA;
                 const int64_t slot = lane ? slB : slA;
