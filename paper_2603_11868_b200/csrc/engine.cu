@@ -53,6 +53,9 @@
 #ifndef SPH_MASK_MINB
 #define SPH_MASK_MINB 12     // k_mask (split filtering): quad prefetch + staged stores
 #endif
+#ifndef SPH_SKIN_SORT_CT
+#define SPH_SKIN_SORT_CT 1     // block bitonic: straight-line chunk merge stages
+#endif
 #ifndef SPH_SKIN_FLUID_PASS
 #define SPH_SKIN_FLUID_PASS 1   // k_skin_tile: fluid-pair passes without wall tests
 #endif
@@ -307,6 +310,30 @@ __device__ __forceinline__ void chunk_bitonic(K (&v)[2], int base, int k, int jt
     }
 }
 
+// chunk_bitonic with a compile-time top partner distance (straight-line
+// stages; the runtime-k merge stages otherwise dispatch through a jump table)
+template <int J, class K>
+__device__ __forceinline__ void chunk_bitonic_ct(K (&v)[2], int base, int k, unsigned lane)
+{
+    if constexpr (J >= 2) {
+#pragma unroll
+        for (int r = 0; r < 2; r++) {
+            const K o = __shfl_xor_sync(0xffffffffu, v[r], J >> 1);
+            const int e = base + 2 * (int)lane + r;
+            const bool up = (e & k) == 0, lower = (e & J) == 0;
+            v[r] = ((o < v[r]) == (lower == up)) ? o : v[r];
+        }
+        chunk_bitonic_ct<J / 2>(v, base, k, lane);
+    } else {
+        const int e = base + 2 * (int)lane;
+        const bool up = (e & k) == 0;
+        const K x0 = v[0], x1 = v[1];
+        const bool sw = (x0 > x1) == up;
+        v[0] = sw ? x1 : x0;
+        v[1] = sw ? x0 : x1;
+    }
+}
+
 template <int NT, class K>
 __device__ __forceinline__ void block_bitonic(K* key, int P)
 {
@@ -332,7 +359,11 @@ __device__ __forceinline__ void block_bitonic(K* key, int P)
         for (int c = warp; c < (P >> 6); c += NW) {
             const int base = c << 6;
             K v[2] = {key[base + 2 * lane], key[base + 2 * lane + 1]};
+#if SPH_SKIN_SORT_CT
+            chunk_bitonic_ct<32>(v, base, k, lane);
+#else
             chunk_bitonic(v, base, k, 32, lane);
+#endif
             key[base + 2 * lane] = v[0];
             key[base + 2 * lane + 1] = v[1];
         }
