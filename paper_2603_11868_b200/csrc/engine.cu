@@ -458,10 +458,10 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         }
         int P = 64;
         while (P < M) P <<= 1;
+        int r = 0;   // k only grows: each thread's run search resumes where it stopped
         for (int k = tid; k < P; k += NT) {
             uint32_t key = 0xffffffffu;
             if (k < M) {
-                int r = 0;
                 while (r + 1 < nruns && run_pre[r + 1] <= (uint32_t)k) r++;
                 key = E.id[run_start[r] + ((uint32_t)k - run_pre[r])];
             }
