@@ -766,38 +766,46 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
             int32_t* __restrict__ lpA = E.lists + ell_base(slA);
             int32_t* __restrict__ lpB = E.lists + ell_base(slB);
             int cntA = 0, cntB = 0, naA = 0, naB = 0;
-            for (int base = 0; base < Mp; base += 32) {
-                const int k = base + (int)lane;
-                const uint32_t j = sj[k];
-                T xj[3];
-                to3<T>(spos[k], xj);
+            auto scan = [&](auto fo) {   // FO: both fluid (as in k_skin_tile)
+                constexpr bool FO = decltype(fo)::value;
+                for (int base = 0; base < Mp; base += 32) {
+                    const int k = base + (int)lane;
+                    const uint32_t j = sj[k];
+                    T xj[3];
+                    to3<T>(spos[k], xj);
 #if SPH_PERIODIC
-                const T r2a = tile_r2<T, D>(xa, xj);
+                    const T r2a = tile_r2<T, D>(xa, xj);
+                    const T r2b = tile_r2<T, D>(xb, xj);
 #else
-                const T r2a = accept_r2<T, D>(xa, xj);
+                    const T r2a = accept_r2<T, D>(xa, xj);
+                    const T r2b = accept_r2<T, D>(xb, xj);
 #endif
-#if SPH_PERIODIC
-                const T r2b = tile_r2<T, D>(xb, xj);
-#else
-                const T r2b = accept_r2<T, D>(xb, xj);
-#endif
-                const bool jf = (int64_t)j < nf;
-                const bool stA = (flA || jf) && r2a < cs2 && j != (uint32_t)iA;
-                const bool stB = hasB && (flB || jf) && r2b < cs2 && j != (uint32_t)iB;
-                const unsigned bA = __ballot_sync(0xffffffffu, stA);
-                const unsigned bB = __ballot_sync(0xffffffffu, stB);
-                if (stA) lpA[ell_off(cntA + __popc(bA & lt))] = (int32_t)j;   // M <= 128 < kCap
-                if (stB) lpB[ell_off(cntB + __popc(bB & lt))] = (int32_t)j;
-                cntA += __popc(bA);
-                cntB += __popc(bB);
-                if (!flA || !flB) {
-                    const bool ctA = !flA && !jf && r2a < g.c2 && r2a > T(0) && j != (uint32_t)iA;
-                    const bool ctB = hasB && !flB && !jf && r2b < g.c2 && r2b > T(0) &&
+                    const bool jf = FO || (int64_t)j < nf;
+                    const bool stA = (FO || flA || jf) && r2a < cs2 && j != (uint32_t)iA;
+                    const bool stB = (FO || hasB) && (FO || flB || jf) && r2b < cs2 &&
                                      j != (uint32_t)iB;
-                    naA += __popc(__ballot_sync(0xffffffffu, ctA));
-                    naB += __popc(__ballot_sync(0xffffffffu, ctB));
+                    const unsigned bA = __ballot_sync(0xffffffffu, stA);
+                    const unsigned bB = __ballot_sync(0xffffffffu, stB);
+                    if (stA) lpA[ell_off(cntA + __popc(bA & lt))] = (int32_t)j;   // M <= 128 < kCap
+                    if (stB) lpB[ell_off(cntB + __popc(bB & lt))] = (int32_t)j;
+                    cntA += __popc(bA);
+                    cntB += __popc(bB);
+                    if (!FO && (!flA || !flB)) {
+                        const bool ctA = !flA && !jf && r2a < g.c2 && r2a > T(0) &&
+                                         j != (uint32_t)iA;
+                        const bool ctB = hasB && !flB && !jf && r2b < g.c2 && r2b > T(0) &&
+                                         j != (uint32_t)iB;
+                        naA += __popc(__ballot_sync(0xffffffffu, ctA));
+                        naB += __popc(__ballot_sync(0xffffffffu, ctB));
+                    }
                 }
-            }
+            };
+#if SPH_SKIN_FLUID_PASS
+            if (flB) scan(std::true_type{});
+            else scan(std::false_type{});
+#else
+            scan(std::false_type{});
+#endif
             if (lane < 2 && (lane == 0 || hasB)) {
                 const int64_t i = lane ? iB : iA;
                 const int64_t slot = lane ? slB : slA;
