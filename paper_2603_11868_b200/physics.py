@@ -489,6 +489,17 @@ def engine_set_counts(E, n, nf):
     E.n, E.nf = int(n), int(nf)
 
 
+def _upload_async(arr, device):
+    """Host registry field -> device tensor, queued on the current stream
+    (asynchronous from pinned memory; a pageable source is staged by the
+    driver before the call returns)."""
+    torch = torch_mod()
+    a = np.ascontiguousarray(arr)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    return torch.from_numpy(a).to(device, non_blocking=True)
+
+
 class Simulation:
     """Advective-step driver (physics.py:416-564) with the state in HBM.
 
@@ -557,10 +568,11 @@ class Simulation:
             ctypes.byref(d["E"]), *[ptr(outs[f]) for f in _ENGINE_FIELDS],
             d["stream"])
         _native.check(rc, "engine_pull")
-        for f in _ENGINE_FIELDS:
+        for f in _ENGINE_FIELDS:   # queued back to back, one synchronise
             host = reg.raw_view(f)
             hv = host.view(np.int32) if host.dtype == np.uint32 else host
-            torch.from_numpy(hv).copy_(outs[f])
+            torch.from_numpy(hv).copy_(outs[f], non_blocking=True)
+        torch.cuda.current_stream(d["device"]).synchronize()
         # the caller may now modify the host arrays in place
         self._host_dirty = True
         self._norms = None
@@ -598,7 +610,10 @@ class Simulation:
         d = self._dev
         st = Staging(d["device"])
         if devs is None:
-            devs = [st.to_dev(reg.raw_view(f)) for f in _ENGINE_FIELDS]
+            # every field's upload is queued on the engine's stream before the
+            # push kernels (pinned registries copy asynchronously; the
+            # stats read below synchronises before the host may touch them)
+            devs = [_upload_async(reg.raw_view(f), d["device"]) for f in _ENGINE_FIELDS]
         # the id-permutation check and the fluid count run on the device
         for attempt in range(2):
             rc = self._lib().sph_engine_push(ctypes.byref(d["E"]),
