@@ -293,6 +293,53 @@ __device__ __forceinline__ unsigned long long dkey(double f)
 // reports it as gpu_launches); defined in sort.cu
 void note_launch();
 
+// Programmatic dependent launch (sm_90+): the sub-step kernels are launched
+// with programmaticStreamSerialization, so a kernel's blocks may be
+// scheduled while the previous kernel's last wave still runs.  Every kernel
+// launched that way calls pdl_begin() first: griddepcontrol.wait blocks
+// until the previous grid has completed and its writes are visible (so the
+// stream order is unchanged), then launch_dependents lets the next grid
+// launch once all of this grid's blocks are resident.  Without PDL both are
+// no-ops.  Measured (bench, alternating A/B runs): 2D 1M +0.7% (short
+// sub-step kernels, ~10-120 us), 3D 4M -1.1% (ms-long sweeps): the engine
+// enables it for 2D only (pdl_for).
+#ifndef SPH_PDL
+#define SPH_PDL 1
+#endif
+__device__ __forceinline__ void pdl_begin()
+{
+#if SPH_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+template <class... KArgs, class... Args>
+inline void launch_pdl(bool pdl, void (*kernel)(KArgs...), int grid, int block, cudaStream_t s,
+                       Args&&... args)
+{
+    note_launch();
+#if SPH_PDL
+    if (!pdl) {
+        kernel<<<grid, block, 0, s>>>(static_cast<Args&&>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+#else
+    kernel<<<grid, block, 0, s>>>(static_cast<Args&&>(args)...);
+#endif
+}
+
 inline int grid_for(int64_t n, int threads, int cap = 1 << 30)
 {
     int64_t g = (n + threads - 1) / threads;

@@ -927,6 +927,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(256)
 k_kick_drift(Eng<T> E, int cv, int crp, GridP<T> g, T half, T full)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     T dnew = T(0);
     if (i >= E.n) {
@@ -958,6 +959,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(kSweepThreads, SPH_MASK_MINB)
 k_mask(Eng<T> E, GridP<T> g, T s_eff)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool need = false;
     if (i < E.n) {
@@ -1006,6 +1008,7 @@ template <class T>
 __global__ void __launch_bounds__(256)
 k_mark(Eng<T> E, T s_eff)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     // 4 consecutive particles per thread (vector loads)
     const int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
     const T dmax = T(__longlong_as_double((long long)E.stats->dmax_bits));
@@ -1115,6 +1118,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(kNlThreads, 4)
 k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E, T cs2)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     __shared__ WarpBuf bufs[kNlWarps];
     __shared__ uint32_t sorted[kNlWarps][kCap];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -1132,6 +1136,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(kNlThreads, 4)
 k_mark_refresh(const EngAcc<T> acc, const GridP<T> g, Eng<T> E, T cs2, T s_eff)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     __shared__ WarpBuf bufs[kNlWarps];
     __shared__ uint32_t sorted[kNlWarps][kCap];
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -1206,6 +1211,7 @@ template <class T, int D, bool EXACT>
 __global__ void __launch_bounds__(kSweepThreads, EXACT ? SPH_CONT_EXACT_MINB : SPH_CONT_MINB)
 k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= E.nf) return;
     const vec4<T>* __restrict__ pos = E.pos;
@@ -1281,6 +1287,7 @@ __global__ void __launch_bounds__(kSweepThreads, SPH_SWEEP_MINB)
 k_wall(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor, int filter,
        int cvn)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long visits_sum = 0;
     if (t < E.nw) {
@@ -1345,6 +1352,7 @@ __global__ void __launch_bounds__(kSweepThreads)
 k_wall_g(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_factor, int filter,
          int cvn)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
     const unsigned lane = lane_id(), q = lane & (G - 1);
     const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (lane & ~(G - 1));
@@ -1425,6 +1433,7 @@ __global__ void __launch_bounds__(kSweepThreads, SPH_MOM_MINB)
 k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor, GridP<T> g,
       int fuse, T full)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long csum = 0;
     T dnew = T(0);
@@ -1643,6 +1652,9 @@ extern "C" int sph_engine_build_lists(SphEngine* e, double skin, cudaStream_t s)
     return SPH_DISPATCH(e, build_lists_impl, e, skin, s);
 }
 
+// programmatic dependent launch for the sub-step kernels (common.cuh): 2D only
+static inline bool pdl_for(const SphEngine* e) { return e->dim == 2; }
+
 template <class T, int D>
 static void launch_fix(const SphEngine* e, cudaStream_t s)
 {
@@ -1651,7 +1663,7 @@ static void launch_fix(const SphEngine* e, cudaStream_t s)
     EngAcc<T> acc = acc_of_engine<T>(e);
     const int64_t want = (e->n + kNlWarps - 1) / kNlWarps;
     const int blocks = (int)(want < 148 * 8 ? want : 148 * 8);
-    note_launch(), k_fix_build<T, D><<<blocks, kNlThreads, 0, s>>>(acc, g, E, skin_cs2<T>(e));
+    launch_pdl(pdl_for(e), k_fix_build<T, D>, blocks, kNlThreads, s, acc, g, E, skin_cs2<T>(e));
 }
 
 // exact lists for every particle: filtered skin lists (k_mask), exact
@@ -1663,8 +1675,8 @@ static void prepare_lists(const SphEngine* e, cudaStream_t s)
     Eng<T> E = eng_of<T>(e);
     cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
     if (e->n <= 0) return;
-    note_launch(), k_mask<T, D><<<grid_for(e->n, kSweepThreads), kSweepThreads, 0, s>>>(
-        E, g, skin_eff<T>(e));
+    launch_pdl(pdl_for(e), k_mask<T, D>, grid_for(e->n, kSweepThreads), kSweepThreads, s, E, g,
+               skin_eff<T>(e));
     launch_fix<T, D>(e, s);
 }
 
@@ -1702,12 +1714,12 @@ static void mark_and_fix(const SphEngine* e, cudaStream_t s)
     if (SPH_MARK_FUSED && e->few_refreshes) {
         const int64_t want = (e->n + 4 * kNlThreads - 1) / (4 * kNlThreads);
         const int blocks = (int)(want < 148 * 4 ? want : 148 * 4);
-        note_launch(), k_mark_refresh<T, D><<<blocks, kNlThreads, 0, s>>>(
-            acc_of_engine<T>(e), grid_of_engine<T>(e), E, skin_cs2<T>(e), skin_eff<T>(e));
+        launch_pdl(pdl_for(e), k_mark_refresh<T, D>, blocks, kNlThreads, s, acc_of_engine<T>(e),
+                   grid_of_engine<T>(e), E, skin_cs2<T>(e), skin_eff<T>(e));
         return;
     }
     cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
-    note_launch(), k_mark<T><<<grid_for((e->n + 3) / 4, 256), 256, 0, s>>>(E, skin_eff<T>(e));
+    launch_pdl(pdl_for(e), k_mark<T>, grid_for((e->n + 3) / 4, 256), 256, s, E, skin_eff<T>(e));
     launch_fix<T, D>(e, s);
 }
 
@@ -1731,12 +1743,12 @@ static void launch_wall(const SphEngine* e, int b, int zero_drho, int count_fact
     // a thread per wall: a warp per wall with an ordered shuffle chain for
     // the sums measured 1.4x (2D) to 7x (3D) slower
     if (SPH_WALL_LANES > 1)
-        note_launch(), k_wall_g<T, D, (SPH_WALL_LANES > 1 ? SPH_WALL_LANES : 2)>
-            <<<grid_for(nw * SPH_WALL_LANES, kSweepThreads), kSweepThreads, 0, s>>>(
-                E, P, g, b, zero_drho, count_factor, filter, cvn);
+        launch_pdl(pdl_for(e), k_wall_g<T, D, (SPH_WALL_LANES > 1 ? SPH_WALL_LANES : 2)>,
+                   grid_for(nw * SPH_WALL_LANES, kSweepThreads), kSweepThreads, s, E, P, g, b,
+                   zero_drho, count_factor, filter, cvn);
     else
-        note_launch(), k_wall<T, D><<<grid_for(nw, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, P, g, b, zero_drho, count_factor, filter, cvn);
+        launch_pdl(pdl_for(e), k_wall<T, D>, grid_for(nw, kSweepThreads), kSweepThreads, s, E, P, g, b,
+                   zero_drho, count_factor, filter, cvn);
 }
 
 // physics.py:460-467 initialize, in its two halo-exchange phases: exact
@@ -1808,8 +1820,8 @@ template <class T, int D>
 static void sub_kick_drift(SphEngine* e, T half, T full, cudaStream_t s)
 {
     if (e->n > 0)
-        note_launch(), k_kick_drift<T, D><<<grid_for(e->n, 256), 256, 0, s>>>(
-            eng_of<T>(e), e->cur_v, e->cur_rp, grid_of_engine<T>(e), half, full);
+        launch_pdl(pdl_for(e), k_kick_drift<T, D>, grid_for(e->n, 256), 256, s, eng_of<T>(e), e->cur_v,
+                   e->cur_rp, grid_of_engine<T>(e), half, full);
 }
 
 // list upkeep of a sub-step: exact lists for all (split) or for the
@@ -1830,6 +1842,7 @@ static void sub_lists(SphEngine* e, cudaStream_t s)
 template <class T>
 __global__ void __launch_bounds__(256) k_wall_operands(Eng<T> E, int cv, int crp)
 {
+    pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     const int64_t i = E.nf + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < E.n)
         reinterpret_cast<T*>(&E.vel[cv][i])[3] = RN<T>::div(E.pos[i].w, E.rp[crp][i].x);
@@ -1840,8 +1853,8 @@ static void sub_wall_operands(SphEngine* e, cudaStream_t s)
 {
     const int64_t nw = e->n - e->nf;
     if (nw > 0)
-        note_launch(), k_wall_operands<T><<<grid_for(nw, 256), 256, 0, s>>>(eng_of<T>(e),
-                                                                          e->cur_v, e->cur_rp);
+        launch_pdl(pdl_for(e), k_wall_operands<T>, grid_for(nw, 256), 256, s, eng_of<T>(e), e->cur_v,
+                   e->cur_rp);
 }
 
 template <class T, int D>
@@ -1850,13 +1863,11 @@ static void sub_continuity(SphEngine* e, T full, cudaStream_t s)
     Eng<T> E = eng_of<T>(e);
     const int crp = e->cur_rp;
     if (e->nf > 0 && split_filter(e))
-        note_launch(), k_cont_du<T, D, true><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0,
-                                              s>>>(
-            E, make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full);
+        launch_pdl(pdl_for(e), k_cont_du<T, D, true>, grid_for(e->nf, kSweepThreads), kSweepThreads, s, E,
+                   make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full);
     else if (e->nf > 0)
-        note_launch(), k_cont_du<T, D, false><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0,
-                                               s>>>(
-            E, make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full);
+        launch_pdl(pdl_for(e), k_cont_du<T, D, false>, grid_for(e->nf, kSweepThreads), kSweepThreads, s, E,
+                   make_phys<T>(phys_of_engine(e)), grid_of_engine<T>(e), e->cur_v, crp, full);
     else if (e->n > 0)   // no fluid: the other rp buffer must still carry walls
         cudaMemcpyAsync(E.rp[crp ^ 1], E.rp[crp], sizeof(vec2<T>) * (size_t)e->n,
                         cudaMemcpyDeviceToDevice, s);
@@ -1884,9 +1895,9 @@ static void sub_momentum(SphEngine* e, T half, T next_full, bool fuse, bool zero
         cudaMemsetAsync((char*)e->dvdt + sizeof(vec4<T>) * (size_t)e->nf, 0,
                         sizeof(vec4<T>) * (size_t)(e->n - e->nf), s);
     if (e->nf > 0)
-        note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
-            E, make_phys<T>(phys_of_engine(e)), cv, e->cur_rp ^ 1, 1, half, 2,
-            grid_of_engine<T>(e), fuse ? 1 : 0, next_full);
+        launch_pdl(pdl_for(e), k_mom<T, D>, grid_for(e->nf, kSweepThreads), kSweepThreads, s, E,
+                   make_phys<T>(phys_of_engine(e)), cv, e->cur_rp ^ 1, 1, half, 2,
+                   grid_of_engine<T>(e), fuse ? 1 : 0, next_full);
     else if (e->n > 0)
         cudaMemcpyAsync(E.vel[cv ^ 1], E.vel[cv], sizeof(vec4<T>) * (size_t)e->n,
                         cudaMemcpyDeviceToDevice, s);
