@@ -1652,8 +1652,9 @@ extern "C" int sph_engine_build_lists(SphEngine* e, double skin, cudaStream_t s)
     return SPH_DISPATCH(e, build_lists_impl, e, skin, s);
 }
 
-// programmatic dependent launch for the sub-step kernels (common.cuh): 2D only
-static inline bool pdl_for(const SphEngine* e) { return e->dim == 2; }
+// programmatic dependent launch for the sub-step kernels (common.cuh): 2D
+// only, and not on slab ranks, whose sub-steps interleave NCCL kernels
+static inline bool pdl_for(const SphEngine* e) { return e->dim == 2 && !e->owned_id; }
 
 template <class T, int D>
 static void launch_fix(const SphEngine* e, cudaStream_t s)
