@@ -157,3 +157,51 @@ def test_cell_plane_matches_kernel_binning():
     keys, _ = O.compute_keys(x, origin, np.float32(0.065), shape)
     assert np.array_equal(cell_plane(x[:, 0], origin[0], np.float32(0.065), 40),
                           keys // 30)
+
+
+class _RecordingComm:
+    """Comm stand-in: records what each peer is sent and hands it back as
+    that peer's message (a loopback), so packing and unpacking meet."""
+
+    def __init__(self):
+        import torch
+        self.torch = torch
+        self.device = torch.device("cpu")
+        self.sent = {}
+
+    def exchange(self, sends, recv_counts, row_shape, dtype):
+        self.sent = {q: t.clone() for q, t in sends.items()}
+        for q, t in sends.items():
+            assert t.dtype == dtype and tuple(t.shape[1:]) == tuple(row_shape)
+            assert t.shape[0] == recv_counts[q]
+        return {q: t.clone() for q, t in sends.items()}
+
+
+def test_exchange_fields_packs_only_the_sent_rows():
+    """distributed.DistributedSimulation._exchange_fields: one int32 message
+    per peer holding exactly the selected rows of every field, unpacked to
+    the original dtypes and values; peers with no rows get no message."""
+    import torch
+    from paper_2603_11868_b200.distributed import DistributedSimulation
+    rng = np.random.default_rng(5)
+    n, d = 50, 3
+    fields = {}
+    for f in FIELDS:
+        if f in ("x", "v", "dvdt"):
+            fields[f] = torch.from_numpy(rng.standard_normal((n, d)).astype(np.float32))
+        elif f in ("id", "wall", "nnb", "oflow"):
+            fields[f] = torch.from_numpy(rng.integers(0, 1 << 30, n).astype(np.int32))
+        else:
+            fields[f] = torch.from_numpy(rng.standard_normal(n).astype(np.float32))
+    sim = DistributedSimulation.__new__(DistributedSimulation)
+    sim.comm = _RecordingComm()
+    rows = {1: torch.tensor([3, 7, 7, 49]), 2: torch.tensor([0]),
+            3: torch.zeros(0, dtype=torch.int64)}
+    got = sim._exchange_fields(fields, rows, {1: 4, 2: 1, 3: 0})
+    assert sorted(sim.comm.sent) == [1, 2]          # no empty message
+    width = sum(3 if f in ("x", "v", "dvdt") else 1 for f in FIELDS)
+    assert sim.comm.sent[1].shape == (4, width)
+    for q in (1, 2):
+        for f in FIELDS:
+            assert got[f][q].dtype == fields[f].dtype
+            assert torch.equal(got[f][q], fields[f][rows[q]])
