@@ -53,6 +53,9 @@
 #ifndef SPH_MASK_MINB
 #define SPH_MASK_MINB 12     // k_mask (split filtering): quad prefetch + staged stores
 #endif
+#ifndef SPH_FIX_MINB
+#define SPH_FIX_MINB 4          // k_fix_build blocks per SM (register cap)
+#endif
 #ifndef SPH_SKIN_SORT_CT
 #define SPH_SKIN_SORT_CT 1     // block bitonic: straight-line chunk merge stages
 #endif
@@ -1115,7 +1118,7 @@ __device__ __forceinline__ void refresh_one(const EngAcc<T>& acc, const GridP<T>
 }
 
 template <class T, int D>
-__global__ void __launch_bounds__(kNlThreads, 4)
+__global__ void __launch_bounds__(kNlThreads, SPH_FIX_MINB)
 k_fix_build(const EngAcc<T> acc, const GridP<T> g, Eng<T> E, T cs2)
 {
     pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
