@@ -1965,30 +1965,34 @@ extern "C" int sph_engine_substep_timed(SphEngine* e, double half_dt, double ful
     return rc ? rc : check_launch("engine_substep_timed");
 }
 
-// physics.py:522-548 for the nsub sub-steps of one advective step
+// physics.py:522-548 for the nsub sub-steps of one advective step.  ms
+// (optional): per-part CUDA-event times summed over the sub-steps; the
+// events are only recorded between the launches (no host synchronisation
+// until the last sub-step), so the timed step runs as the untimed one does
 template <class T, int D>
 static int substeps_impl(SphEngine* e, double half_d, double full_d, int nsub, float* ms,
                          cudaStream_t s)
 {
     const T half = T(half_d), full = T(full_d);
-    cudaEvent_t ev[6];
+    cudaEvent_t* ev = nullptr;
     if (ms) {
-        for (int k = 0; k < 6; k++) cudaEventCreate(&ev[k]);
+        ev = new cudaEvent_t[6 * (size_t)(nsub > 0 ? nsub : 1)];
+        for (int k = 0; k < 6 * nsub; k++) cudaEventCreate(&ev[k]);
         for (int k = 0; k < 5; k++) ms[k] = 0.0f;
     }
-    for (int k = 0; k < nsub; k++) {
-        substep_parts<T, D>(e, half, full, k + 1 < nsub, ms ? ev : nullptr, s);
-        if (ms) {
-            cudaEventSynchronize(ev[5]);
+    for (int k = 0; k < nsub; k++)
+        substep_parts<T, D>(e, half, full, k + 1 < nsub, ms ? ev + 6 * k : nullptr, s);
+    if (ms) {
+        if (nsub > 0) cudaEventSynchronize(ev[6 * nsub - 1]);
+        for (int k = 0; k < nsub; k++)
             for (int q = 0; q < 5; q++) {
                 float t = 0.0f;
-                cudaEventElapsedTime(&t, ev[q], ev[q + 1]);
+                cudaEventElapsedTime(&t, ev[6 * k + q], ev[6 * k + q + 1]);
                 ms[q] += t;
             }
-        }
+        for (int k = 0; k < 6 * nsub; k++) cudaEventDestroy(ev[k]);
+        delete[] ev;
     }
-    if (ms)
-        for (int k = 0; k < 6; k++) cudaEventDestroy(ev[k]);
     return check_launch("engine_substeps");
 }
 

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native
 from . import variables as var
-from ._device import (Staging, device_of, is_tensor, ptr, stream_ptr,
+from ._device import (C_void, Staging, device_of, is_tensor, ptr, stream_ptr,
                       torch_mod, workspace)
 from .execution import (ExecutionPolicy, ParticleKernel, ReduceSpec,
                         particle_for, particle_reduce)
@@ -536,6 +536,7 @@ class Simulation:
         self._norms = None          # (vmax, amax) valid for the device state
         self._oob_walls = 0
         self.kernel_times = None    # dict name -> [ms per launch] when profiling
+        self._pending_events = []
         self._skin_factor = SKIN_FACTOR_START
         self.last_nfix = 0
         self.list_refresh = "auto"  # sub-step list upkeep: auto | pass | queue
@@ -560,19 +561,20 @@ class Simulation:
         torch = torch_mod()
         reg = self.registry
         outs = {}
-        for f in _ENGINE_FIELDS:
-            host = reg.raw_view(f)
-            tdt = torch.int32 if host.dtype == np.uint32 else d["tdtype"]
-            outs[f] = torch.empty(host.shape, dtype=tdt, device=d["device"])
-        rc = self._lib().sph_engine_pull(
-            ctypes.byref(d["E"]), *[ptr(outs[f]) for f in _ENGINE_FIELDS],
-            d["stream"])
-        _native.check(rc, "engine_pull")
-        for f in _ENGINE_FIELDS:   # queued back to back, one synchronise
-            host = reg.raw_view(f)
-            hv = host.view(np.int32) if host.dtype == np.uint32 else host
-            torch.from_numpy(hv).copy_(outs[f], non_blocking=True)
-        torch.cuda.current_stream(d["device"]).synchronize()
+        with torch.cuda.stream(d["tstream"]):
+            for f in _ENGINE_FIELDS:
+                host = reg.raw_view(f)
+                tdt = torch.int32 if host.dtype == np.uint32 else d["tdtype"]
+                outs[f] = torch.empty(host.shape, dtype=tdt, device=d["device"])
+            rc = self._lib().sph_engine_pull(
+                ctypes.byref(d["E"]), *[ptr(outs[f]) for f in _ENGINE_FIELDS],
+                d["stream"])
+            _native.check(rc, "engine_pull")
+            for f in _ENGINE_FIELDS:   # queued back to back, one synchronise
+                host = reg.raw_view(f)
+                hv = host.view(np.int32) if host.dtype == np.uint32 else host
+                torch.from_numpy(hv).copy_(outs[f], non_blocking=True)
+        d["tstream"].synchronize()
         # the caller may now modify the host arrays in place
         self._host_dirty = True
         self._norms = None
@@ -597,8 +599,11 @@ class Simulation:
                             force_scalars(reg, self.grid), reg.singular("g"))
         engine_set_counts(E, n, nf)
         torch = torch_mod()
+        # the engine's stream: every engine call and every copy to or from
+        # its buffers is queued on it, whatever stream is current later
+        tstream = torch.cuda.current_stream(T["pos0"].device)
         self._dev = {"device": T["pos0"].device, "E": E, "T": T, "tdtype": T["pos0"].dtype,
-                     "stream": stream_ptr(T["pos0"].device),
+                     "tstream": tstream, "stream": C_void(tstream.cuda_stream),
                      "stats_host": torch.empty(T["stats"].shape, dtype=torch.uint8,
                                                pin_memory=True)}
 
@@ -613,7 +618,10 @@ class Simulation:
             # every field's upload is queued on the engine's stream before the
             # push kernels (pinned registries copy asynchronously; the
             # stats read below synchronises before the host may touch them)
-            devs = [_upload_async(reg.raw_view(f), d["device"]) for f in _ENGINE_FIELDS]
+            with torch_mod().cuda.stream(d["tstream"]):
+                devs = [_upload_async(reg.raw_view(f), d["device"]) for f in _ENGINE_FIELDS]
+        else:   # caller-provided device tensors: ordered before the push
+            d["tstream"].wait_stream(torch_mod().cuda.current_stream(d["device"]))
         # the id-permutation check and the fluid count run on the device
         for attempt in range(2):
             rc = self._lib().sph_engine_push(ctypes.byref(d["E"]),
@@ -663,8 +671,9 @@ class Simulation:
 
     def _read_stats(self):
         d = self._dev
-        d["stats_host"].copy_(d["T"]["stats"], non_blocking=True)
-        torch_mod().cuda.current_stream(d["device"]).synchronize()
+        with torch_mod().cuda.stream(d["tstream"]):
+            d["stats_host"].copy_(d["T"]["stats"], non_blocking=True)
+        d["tstream"].synchronize()
         return _native.SphStepStats.from_buffer_copy(d["stats_host"].numpy().tobytes())
 
     def _finish_counts(self, stats, check):
@@ -679,8 +688,38 @@ class Simulation:
     def _rebuild_cll(self):
         """physics.py:446-449 on the engine layout."""
         t0 = time.perf_counter()
-        self._call("sph_engine_rebuild_cll")
+        with self._kernel_event("cll_rebuild"):
+            self._call("sph_engine_rebuild_cll")
         self.phase_seconds["cll"] += time.perf_counter() - t0
+
+    def _kernel_event(self, name):
+        """CUDA events on the engine stream around a per-step part when
+        kernel_times is set (read, without an extra synchronisation, after
+        the step's stats read)."""
+        sim = self
+
+        class _Ev:
+            def __enter__(self_):
+                if sim.kernel_times is None:
+                    return self_
+                torch = torch_mod()
+                self_.e = (torch.cuda.Event(enable_timing=True),
+                           torch.cuda.Event(enable_timing=True))
+                self_.e[0].record(sim._dev["tstream"])
+                return self_
+
+            def __exit__(self_, *exc):
+                if sim.kernel_times is not None and hasattr(self_, "e"):
+                    self_.e[1].record(sim._dev["tstream"])
+                    sim._pending_events.append((name, self_.e))
+                return False
+        return _Ev()
+
+    def _collect_events(self):
+        for name, (e0, e1) in self._pending_events:
+            e1.synchronize()
+            self.kernel_times.setdefault(name, []).append(e0.elapsed_time(e1))
+        self._pending_events = []
 
     def initialize(self):
         """physics.py:460-467: CLL, wall pressure, momentum, counts."""
@@ -762,7 +801,8 @@ class Simulation:
         if end_time is not None:
             dt = min(dt, end_time - self.time)
         t0 = time.perf_counter()
-        self._build_lists(self._choose_skin(vmax, amax, dt))
+        with self._kernel_event("skin_build"):
+            self._build_lists(self._choose_skin(vmax, amax, dt))
         self.phase_seconds["cll"] += time.perf_counter() - t0
         if self.shepard_every and self.step_count > 0 \
                 and self.step_count % self.shepard_every == 0:
@@ -788,6 +828,8 @@ class Simulation:
         self._call("sph_engine_stats", ctypes.c_int32(_native.STATS_NORMS))
         stats = self._read_stats()
         self.phase_seconds["interactions"] += time.perf_counter() - t0
+        if self.kernel_times is not None:
+            self._collect_events()
         self._host_stale = True
         self.last_nsub = nsub
         self.last_nfix = int(stats.nfix)
