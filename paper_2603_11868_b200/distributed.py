@@ -450,6 +450,24 @@ class DistributedSimulation:
             raise SimulationUnstableError(f"runaway velocity at step {self.step_count}")
         return dt
 
+    def checkpoint(self):
+        """The rank's state between steps (owned particles, layout, counters):
+        restore() repeats the following steps bit for bit."""
+        be = self.backend
+        return ({f: t.clone() for f, t in self.owned.items()}, self.layout,
+                {k: getattr(self, k) for k in ("step_count", "time", "interaction_count",
+                                               "out_of_bounds", "migrated")},
+                getattr(be, "_skin_factor", None))
+
+    def restore(self, ck):
+        owned, layout, attrs, skin = ck
+        self.owned = {f: t.clone() for f, t in owned.items()}
+        self.layout = layout
+        for k, v in attrs.items():
+            setattr(self, k, v)
+        if skin is not None:
+            self.backend._skin_factor = skin
+
     def gather(self):
         """All owned particles of all ranks as numpy, ordered by id (every rank)."""
         out = {}

@@ -434,6 +434,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
     T["offs_w"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
     T["lists"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
     T["elist"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
+    T["amask"] = torch.empty((tiles, NEIGHBOR_CAPACITY // 32, 32), dtype=i32, device=dev)
     for k in ("lcount", "acount", "nww"):
         T[k] = torch.empty((tiles * 32,), dtype=i32, device=dev)
     T["qcount"] = torch.zeros((4,), dtype=i32, device=dev)
@@ -450,7 +451,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
     E.rq = T["rq"].data_ptr()
     for k in ("dvdt", "drho", "id", "nnb", "refpos", "rho_scratch_id",
               "oflow_id", "wall_id", "vol_id", "offs_f", "offs_w", "lists",
-              "lcount", "acount", "nww", "elist", "cell0", "disp", "disp0", "queue",
+              "lcount", "acount", "nww", "elist", "amask", "cell0", "disp", "disp0", "queue",
               "qcount", "ws", "stats"):
         setattr(E, k, T[k].data_ptr())
     E.owned_id = None      # every particle owned (multi-rank runs set it)
@@ -861,6 +862,20 @@ class Simulation:
             raise SimulationUnstableError(
                 f"runaway velocity {vmax_f:.3g} at step {self.step_count}")
         return dt
+
+    def skin_entries(self):
+        """(fluid, wall) totals of the current skin-list entry counts (the
+        list bytes the sweeps stream; diagnostic)."""
+        d = self._dev
+        if d is None:
+            return 0, 0
+        E = d["E"]
+        lc = d["T"]["lcount"]
+        nf, nw = int(E.nf), int(E.n - E.nf)
+        nf_pad = (nf + 31) // 32 * 32
+        f = int(lc[:nf].sum().item()) if nf else 0
+        w = int(lc[nf_pad:nf_pad + nw].sum().item()) if nw else 0
+        return f, w
 
     def probe_candidates(self, location, reach, cap=1 << 16):
         """Fluid particles within (a conservatively widened) reach of a point,

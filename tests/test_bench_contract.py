@@ -33,6 +33,39 @@ def test_reference_arm_prints_one_contract_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
 
 
+def test_reference_arm_under_gpus_2_respawns_one_rank_line():
+    """`bench.py --gpus 2` without a launcher re-executes under
+    torch.distributed.run; only rank 0 runs the reference arm and prints."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--config", "2dref", "--steps", "1", "--warmup", "3",
+                          "--cpu-budget", "10"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    assert d["config"] == bench.config_of("2dref", 2, 5153, 3200, 1953, 7656)
+
+
+def test_world_size_must_match_gpus():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "WORLD_SIZE" in out.stderr
+
+
+def test_roofline_bytes_follow_survey_8d():
+    # momentum: nf (20d + 20); 2D 1M: 963,966 x 60 = 57.8 MB (VERDICT r1 recompute)
+    assert bench.kernel_bytes("momentum_kick", 2, 997518, 963966, 33552) == 963966 * 60
+    assert bench.kernel_bytes("continuity_du", 3, 10, 7, 3) == 7 * 48
+    assert bench.kernel_bytes("wall_pressure", 3, 10, 7, 3) == 3 * 28
+    # neighbour-list bytes are reported separately, never as algorithmic
+    assert bench.list_bytes("momentum_kick", 100, 0, 0, 0) == 400
+
+
 def test_step_byte_model_matches_survey_table():
     # SURVEY.md 8(d): config 1 B_sub = 109.1, B_step = 103.9 (d = 2, w = 0.379)
     n, nw = 5153, 1953
