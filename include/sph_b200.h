@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 7
+#define SPH_ABI_VERSION 8
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -252,7 +252,16 @@ typedef struct {
     /* host hint: 1 when the previous step refreshed few lists, so the
      * sub-step's list check and refreshes run as one queue-free pass */
     int32_t few_refreshes;
-    int32_t reserved0;
+    /* library state: the walls' static wall-wall neighbour counts (nww) are
+     * valid (computed by the first list build after a push; walls never
+     * move), so later builds skip wall-only candidate blocks */
+    int32_t nww_ready;
+    /* this sub-step's accept mask over the skin lists (dev): bit t of word
+     * t/32 of a slot is set when skin entry t passed the exact test
+     * (0 < r2 < c^2); tile layout [slots/32][256/32][32] uint32.  Written by
+     * the fused continuity filter, walked by the momentum sweep (the exact
+     * list elist is then not materialised) */
+    uint32_t* amask;
 } SphEngine;
 
 size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64);
@@ -303,6 +312,10 @@ int sph_engine_substep_timed(SphEngine* e, double half_dt, double full_dt, float
  * flags & 2: recompute the exact vmax/amax (physics.py:390-391) and the
  * stability inputs (physics.py:554-564) into e->stats */
 int sph_engine_stats(SphEngine* e, int flags, cudaStream_t s);
+/* binary snapshot (report.py:187-205 fields, by original id): out (dev) is
+ * an (n, 2*dim + 2) run-precision row-major array, row = particle id,
+ * columns x[dim], v[dim], rho, p of the current state */
+int sph_engine_snapshot(const SphEngine* e, void* out, cudaStream_t s);
 /* physics.py:589-606 sample_pressure, device half: records (registry
  * position, x, y, z, m, rho, p) as binary64 of the fluid particles with
  * |x - loc| < radius (binary64), at most cap of them (*count = all found;

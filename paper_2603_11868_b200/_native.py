@@ -101,11 +101,12 @@ class SphEngine(C.Structure):
         ("cur_v", c_i32), ("cur_rp", c_i32), ("cur_pos", c_i32), ("drifted", c_i32), ("f64", c_i32), ("lists_ready", c_i32),
         ("period", c_f64 * 3),
         ("disp0", P),
-        ("few_refreshes", c_i32), ("reserved0", c_i32),
+        ("few_refreshes", c_i32), ("nww_ready", c_i32),
+        ("amask", P),
     ]
 
 
-ABI_VERSION = 7   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 8   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)
@@ -142,6 +143,7 @@ _PROTOS = {
     "sph_engine_substeps_timed": (c_i32, [_P, c_f64, c_f64, c_i32, _P, _P]),
     "sph_engine_phase": (c_i32, [_P, c_i32, c_f64, c_f64, _P]),
     "sph_engine_probe": (c_i32, [_P, _P, c_f64, _P, c_i32, _P, _P]),
+    "sph_engine_snapshot": (c_i32, [_P, _P, _P]),
     "sph_engine_halo_width": (c_i32, [c_i32]),
     "sph_engine_pack": (c_i32, [_P, c_i32, _P, c_i64, _P, _P]),
     "sph_halo_pack": (c_i32, [_P, _P, c_i32, c_i32, _P]),

@@ -62,6 +62,9 @@
 #ifndef SPH_SKIN_FLUID_PASS
 #define SPH_SKIN_FLUID_PASS 1   // k_skin_tile: fluid-pair passes without wall tests
 #endif
+#ifndef SPH_SKIN_WALL_SKIP
+#define SPH_SKIN_WALL_SKIP 1    // skip wall-only blocks once the wall-wall counts are known
+#endif
 #ifndef SPH_SKIN_THREADS_PER_SM
 #define SPH_SKIN_THREADS_PER_SM 1024   // skin-list build occupancy (register cap)
 #endif
@@ -71,11 +74,36 @@
 #ifndef SPH_CONT_FILTER_QUADS      // continuity: visit accepted entries per list quad
 #define SPH_CONT_FILTER_QUADS (D == 3)   // (measured: 3D -4.5%, 2D +23%)
 #endif
+#ifndef SPH_MASK_LISTS      // fused filter writes an accept mask, momentum walks it
+#define SPH_MASK_LISTS 0     // (measured: continuity -9%, momentum +22%: off)
+#endif
+#ifndef SPH_LIST_CS          // list streams (skin / exact lists, ~1 GB each per
+#define SPH_LIST_CS 0        // 3D 4M sub-step) with evict-first hints (measured: 3D -1%, 2D +11%: off)
+#endif
 #ifndef SPH_MOM_ILP
 #define SPH_MOM_ILP 1        // momentum: two pairs per basic block (1: in 2D, 2: always)
 #endif
 
 namespace sph {
+
+// neighbour-list quads: streamed once per sweep and larger than L2, so they
+// are loaded / stored evict-first (the gathered particle data keeps L2)
+__device__ __forceinline__ int4 ld_list(const int4* p)
+{
+#if SPH_LIST_CS
+    return __ldcs(p);
+#else
+    return *p;
+#endif
+}
+__device__ __forceinline__ void st_list(int4* p, int4 v)
+{
+#if SPH_LIST_CS
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
 
 // Software-pipelined walk over the exact list of slot (ascending original
 // id): the list entry two pairs ahead and the neighbour data one pair ahead
@@ -88,10 +116,10 @@ __device__ __forceinline__ void sweep_list(const Eng<T>& E, int64_t slot, int cn
     // quad-ELL: 4 entries per int4; the next quad is requested before the
     // current one is processed, so the list stream never stalls a pair
     const int4* __restrict__ q4 = reinterpret_cast<const int4*>(E.elist + ell_base(slot));
-    int4 qn = q4[0];
+    int4 qn = ld_list(q4);
     for (int t0 = 0; t0 < cnt; t0 += 4) {
         const int4 q = qn;
-        if (t0 + 4 < cnt) qn = q4[((t0 >> 2) + 1) * 32];
+        if (t0 + 4 < cnt) qn = ld_list(q4 + ((t0 >> 2) + 1) * 32);
         body(t0, load(q.x));
         if (t0 + 1 < cnt) body(t0 + 1, load(q.y));
         if (t0 + 2 < cnt) body(t0 + 2, load(q.z));
@@ -132,7 +160,8 @@ template <class T> struct NbrPR { vec4<T> p; vec2<T> rp; };
 #endif
 template <class T, int D, class Load, class Body>
 __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const T (&xi)[3],
-                                            T c2, int nl, Load load, Body body)
+                                            T c2, int nl, Load load, Body body,
+                                            uint32_t* __restrict__ mp = nullptr)
 {
     constexpr int CH = SPH_WALK_CHUNK, NM = CH / 32;
     const int32_t* __restrict__ lp = E.lists + ell_base(slot);
@@ -143,7 +172,7 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
 #pragma unroll
         for (int h = 0; h < NM; h++) m[h] = 0;
         for (int u0 = 0; u0 < ne; u0 += 4) {
-            const int4 q = q4[((w0 + u0) >> 2) * 32];
+            const int4 q = ld_list(q4 + ((w0 + u0) >> 2) * 32);
             int jj[4] = {q.x, u0 + 1 < ne ? q.y : -1, u0 + 2 < ne ? q.z : -1,
                          u0 + 3 < ne ? q.w : -1};
             vec4<T> pj[4];
@@ -167,6 +196,7 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
 #pragma unroll
         for (int h = 0; h < NM; h++) {
             uint32_t mh = m[h];
+            if (mp && w0 + 32 * h < nl) mp[((w0 >> 5) + h) * 32] = mh;   // accept mask
             while (mh) {
                 const int u = __ffs(mh) - 1;
                 mh &= mh - 1;
@@ -181,16 +211,18 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
 // are gathered together, tested (0 < r2 < c^2, binary32), and each accepted
 // neighbour is visited right away with the position already in registers
 // (body(j, pos_j)); visits stay in list (= ascending id) order.
+// mp != nullptr: the accept bits are also stored as the slot's mask words
 template <class T, int D, class Body>
 __device__ __forceinline__ void filter_quads(const Eng<T>& E, int64_t slot, const T (&xi)[3], T c2,
-                                             int nl, Body body)
+                                             int nl, Body body, uint32_t* __restrict__ mp = nullptr)
 {
     if (nl <= 0) return;
     const int4* __restrict__ q4 = reinterpret_cast<const int4*>(E.lists + ell_base(slot));
-    int4 qn = q4[0];
+    int4 qn = ld_list(q4);
+    uint32_t mw = 0;
     for (int u0 = 0; u0 < nl; u0 += 4) {
         const int4 q = qn;
-        if (u0 + 4 < nl) qn = q4[((u0 >> 2) + 1) * 32];
+        if (u0 + 4 < nl) qn = ld_list(q4 + ((u0 >> 2) + 1) * 32);
         const int jj[4] = {q.x, u0 + 1 < nl ? q.y : -1, u0 + 2 < nl ? q.z : -1,
                            u0 + 3 < nl ? q.w : -1};
         vec4<T> pj[4];
@@ -201,10 +233,53 @@ __device__ __forceinline__ void filter_quads(const Eng<T>& E, int64_t slot, cons
             T xj[3];
             to3<T>(pj[k], xj);
             const T r2 = accept_r2<T, D>(xi, xj);
-            if (jj[k] >= 0 && (r2 < c2) && (r2 > T(0))) body(jj[k], pj[k]);
+            if (jj[k] >= 0 && (r2 < c2) && (r2 > T(0))) {
+                if (mp) mw |= 1u << ((u0 + k) & 31);
+                body(jj[k], pj[k]);
+            }
+        }
+        if (mp && (((u0 + 4) & 31) == 0 || u0 + 4 >= nl)) {
+            mp[(u0 >> 5) * 32] = mw;
+            mw = 0;
         }
     }
 }
+
+// The accepted entries of a slot's skin list in list (= ascending id)
+// order, from the accept mask: each lane advances through its own set
+// bits, so a warp runs max(accepted) steps as over an exact list; the
+// skin-list quad holding the next entry is loaded once per quad.
+template <class T>
+struct MaskCursor {
+    const int4* __restrict__ q4;
+    const uint32_t* __restrict__ mp;
+    uint32_t m;
+    int wbase, qidx;
+    int4 q;
+    __device__ __forceinline__ void init(const Eng<T>& E, int64_t slot)
+    {
+        q4 = reinterpret_cast<const int4*>(E.lists + ell_base(slot));
+        mp = E.amask + mask_base(slot);
+        m = mp[0];
+        wbase = 0;
+        qidx = -1;
+    }
+    __device__ __forceinline__ int next()
+    {
+        while (!m) {
+            wbase += 32;
+            m = mp[wbase];   // word wbase / 32 sits at 32 * (wbase / 32)
+        }
+        const int e = wbase + __ffs(m) - 1;
+        m &= m - 1;
+        if ((e >> 2) != qidx) {
+            qidx = e >> 2;
+            q = ld_list(q4 + qidx * 32);
+        }
+        const int r = e & 3;
+        return r == 0 ? q.x : (r == 1 ? q.y : (r == 2 ? q.z : q.w));
+    }
+};
 
 __device__ __forceinline__ void enqueue(uint32_t* queue, uint32_t* qcount, bool need,
                                         uint32_t value)
@@ -378,7 +453,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(SkinTile<T, D>::kThreads, SPH_SKIN_THREADS_PER_SM / SkinTile<T, D>::kThreads)
 k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
             const uint32_t* __restrict__ cells, const uint32_t* __restrict__ ncells_p,
-            const uint32_t* __restrict__ phys_of_id)
+            const uint32_t* __restrict__ phys_of_id, int wall_pairs)
 {
     constexpr int NT = SkinTile<T, D>::kThreads, NW = NT / 32, kC = SkinTile<T, D>::kCands;
     constexpr int kP = kC <= 64 ? 64 : (kC <= 128 ? 128 : (kC <= 256 ? 256 : (kC <= 512 ? 512
@@ -454,6 +529,24 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         }
         __syncthreads();
         const int M = (int)run_pre[nruns];
+        if (!wall_pairs && run_pre[rps] == 0) {
+            // wall-only block (no fluid candidate, so no fluid particle in the
+            // cell): walls' lists hold fluid neighbours only -- all empty; the
+            // static wall-wall counts (nww) were set by the first build
+            for (int t = (int)tid; t < nt; t += NT) {
+                const int64_t i = nf + w0 + t;
+                T xi[3];
+                to3<T>(E.pos[i], xi);
+                int cxyz[3];
+                E.cell0[i] = cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c ? (uint32_t)c
+                                                                          : kInvalidCell;
+                E.lcount[E.nf_pad + (i - nf)] = 0;
+                E.disp[i] = T(0);
+                E.disp0[i] = T(0);
+            }
+            __syncthreads();
+            continue;
+        }
         if (M > kC) {   // oversized block: per-particle path (k_skin_big)
             if (tid == 0) E.queue[atomicAdd(E.qcount, 1u)] = (uint32_t)c;
             __syncthreads();
@@ -534,7 +627,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                     }
                     cntA += __popc(bA);
                     cntB += __popc(bB);
-                    if (!FO && (!flA || !flB)) {   // walls: static exact wall-wall count
+                    if (!FO && wall_pairs && (!flA || !flB)) {   // walls: static wall-wall count
                         const bool ctA = !flA && !jf && r2a < g.c2 && r2a > T(0) &&
                                          j != (uint32_t)iA;
                         const bool ctB = hasB && !flB && !jf && r2b < g.c2 && r2b > T(0) &&
@@ -562,7 +655,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                 const bool ok = cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c && cnt <= kCap;
                 E.cell0[i] = ok ? (uint32_t)c : kInvalidCell;
                 E.lcount[slot] = ok ? cnt : 0;
-                E.nww[slot] = lane ? naB : naA;
+                if (wall_pairs) E.nww[slot] = lane ? naB : naA;
                 E.disp[i] = T(0);
                 E.disp0[i] = T(0);
             }
@@ -984,7 +1077,7 @@ k_mask(Eng<T> E, GridP<T> g, T s_eff)
             int32_t* ep = E.elist + ell_base(slot);
             // one quad of list entries + 4 positions in flight per trip
             for (int u0 = 0; u0 < nl; u0 += 4) {
-                const int4 q = q4[(u0 >> 2) * 32];
+                const int4 q = ld_list(q4 + (u0 >> 2) * 32);
                 const int jj[4] = {q.x, u0 + 1 < nl ? q.y : -1, u0 + 2 < nl ? q.z : -1,
                                    u0 + 3 < nl ? q.w : -1};
                 vec4<T> pj[4];
@@ -1238,6 +1331,23 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
         cnt = E.acount[i];
         if (cnt < 0) { flag_overflow(E, i); return; }
         sweep_list<T>(E, i, cnt, loadf, pair);
+    } else if (SPH_MASK_LISTS) {
+        // the accept bits go to the mask the momentum sweep walks
+        uint32_t* __restrict__ mp = E.amask + mask_base(i);
+        cnt = 0;
+        if (SPH_CONT_FILTER_QUADS) {
+            filter_quads<T, D>(E, i, xi, g.c2, E.lcount[i], [&](int j, const vec4<T>& pj) {
+                cnt++;
+                pair(cnt, NbrPV<T>{pj, vel[j]});
+            }, mp);
+        } else {
+            filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf,
+                              [&](int, const NbrPV<T>& nb) {
+                cnt++;
+                pair(cnt, nb);
+            }, mp);
+        }
+        E.acount[i] = cnt;   // <= lcount <= kCap
     } else {
         // the exact list, also stored a full int4 quad at a time
         int4* __restrict__ eq = reinterpret_cast<int4*>(E.elist + ell_base(i));
@@ -1248,7 +1358,7 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
             if (r == 0) e0 = j;
             else if (r == 1) e1 = j;
             else if (r == 2) e2 = j;
-            else if (cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, j);
+            else if (cnt < kCap) st_list(eq + (cnt >> 2) * 32, make_int4(e0, e1, e2, j));
             cnt++;
         };
         if (SPH_CONT_FILTER_QUADS) {
@@ -1263,7 +1373,7 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
                 pair(cnt, nb);
             });
         }
-        if ((cnt & 3) && cnt < kCap) eq[(cnt >> 2) * 32] = make_int4(e0, e1, e2, 0);
+        if ((cnt & 3) && cnt < kCap) st_list(eq + (cnt >> 2) * 32, make_int4(e0, e1, e2, 0));
         if (cnt > kCap) {
             E.acount[i] = -1;
             flag_overflow(E, i);
@@ -1434,7 +1544,7 @@ k_wall_g(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_facto
 template <class T, int D>
 __global__ void __launch_bounds__(kSweepThreads, SPH_MOM_MINB)
 k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor, GridP<T> g,
-      int fuse, T full)
+      int fuse, T full, int mask_ok)
 {
     pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1457,8 +1567,46 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
             const T pi_rr = RQI.y;
             T a[3] = {P.g[0], P.g[1], P.g[2]};
             auto loadf = [&](int j) { return NbrPVR<T>{pos[j], vel[j], rq[j]}; };
-#if SPH_MOM_ILP
-            if (SPH_MOM_ILP > 1 || D == 2) {
+            // the accepted entries come from the continuity sweep's accept
+            // mask over the skin list (valid lists), else from the exact list
+            const bool use_mask = SPH_MASK_LISTS && mask_ok && E.cell0[i] != kInvalidCell;
+            constexpr bool kIlp = SPH_MOM_ILP && (SPH_MOM_ILP > 1 || D == 2);
+            if (kIlp && use_mask) {
+            auto terms = [&](const NbrPVR<T>& nb, double (&t)[3]) {
+                T xj[3], vj[3], dx[3], r2, vx;
+                to3<T>(nb.p, xj);
+                to3<T>(nb.v, vj);
+                pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
+                momentum_terms<T, D>(r2, vx, dx, rho_i, pi_rr, nb.rp.x, nb.rp.y, nb.p.w, P, t);
+            };
+            MaskCursor<T> mc;
+            mc.init(E, i);
+            for (int t0 = 0; t0 < acnt; t0 += 2) {
+                const bool hb = t0 + 1 < acnt;
+                const int ja = mc.next();
+                const int jb = hb ? mc.next() : ja;
+                const NbrPVR<T> na = loadf(ja), nb = loadf(jb);
+                double ta[3], tb[3];
+                terms(na, ta);
+                terms(nb, tb);
+                momentum_accumulate<T, D>(ta, a);
+                if (hb) momentum_accumulate<T, D>(tb, a);
+            }
+            } else if (use_mask) {
+                MaskCursor<T> mc;
+                mc.init(E, i);
+                int jn = acnt > 0 ? mc.next() : 0;
+                for (int t = 0; t < acnt; t++) {
+                    const int j = jn;
+                    if (t + 1 < acnt) jn = mc.next();
+                    const NbrPVR<T> nb = loadf(j);
+                    T xj[3], vj[3], dx[3], r2, vx;
+                    to3<T>(nb.p, xj);
+                    to3<T>(nb.v, vj);
+                    pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
+                    momentum_pair<T, D>(r2, vx, dx, rho_i, pi_rr, nb.rp.x, nb.rp.y, nb.p.w, P, a);
+                }
+            } else if (kIlp) {
             // two pairs per basic block: their terms are independent chains the
             // scheduler interleaves; accumulation stays in list order
             auto terms = [&](const NbrPVR<T>& nb, double (&t)[3]) {
@@ -1470,10 +1618,10 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
             };
             if (acnt > 0) {
                 const int4* __restrict__ q4 = reinterpret_cast<const int4*>(E.elist + ell_base(i));
-                int4 qn = q4[0];
+                int4 qn = ld_list(q4);
                 for (int t0 = 0; t0 < acnt; t0 += 4) {
                     const int4 q = qn;
-                    if (t0 + 4 < acnt) qn = q4[((t0 >> 2) + 1) * 32];
+                    if (t0 + 4 < acnt) qn = ld_list(q4 + ((t0 >> 2) + 1) * 32);
                     {
                         const bool hb = t0 + 1 < acnt;
                         const NbrPVR<T> na = loadf(q.x), nb = loadf(hb ? q.y : q.x);
@@ -1494,9 +1642,7 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
                     }
                 }
             }
-            } else
-#endif
-            {
+            } else {
             sweep_list<T>(E, i, acnt, loadf, [&](int, const NbrPVR<T>& nb) {
                 T xj[3], vj[3], dx[3], r2, vx;
                 to3<T>(nb.p, xj);
@@ -1615,6 +1761,8 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
     EngAcc<T> acc = acc_of_engine<T>(e);
     Eng<T> E = eng_of<T>(e);
     const T cs2 = skin_cs2<T>(e);
+    // walls' static wall-wall counts: computed by the first build after a push
+    const int wall_pairs = (SPH_SKIN_WALL_SKIP && e->nww_ready) ? 0 : 1;
     if (e->n > 0) {
         constexpr int NT = SkinTile<T, D>::kThreads;
         const int64_t want = e->ncells < e->n ? e->ncells : e->n;
@@ -1637,14 +1785,15 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
                                                s>>>(g, cs2, E, cells, counts, phys_of_id, big,
                                                     counts + 1);
             note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, big,
-                                                                  counts + 1, phys_of_id);
+                                                                  counts + 1, phys_of_id, 1);
         } else {        // 3D blocks hold ~450: a thread block per cell
             note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, cells, counts,
-                                                                  phys_of_id);
+                                                                  phys_of_id, wall_pairs);
         }
         note_launch(), k_skin_big<T, D><<<148 * 2, kNlThreads, 0, s>>>(acc, g, cs2, E);
     }
     e->lists_ready = 1;
+    e->nww_ready = 1;
     return check_launch("engine_build_lists");
 }
 
@@ -1775,7 +1924,7 @@ static void init_momentum(SphEngine* e, cudaStream_t s)
         note_launch(), k_rq_fill<T><<<grid_for(e->nf, 256), 256, 0, s>>>(E, e->cur_rp, e->nf);
         note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
             E, make_phys<T>(phys_of_engine(e)), e->cur_v, e->cur_rp, 0, T(0), 1,
-            grid_of_engine<T>(e), 0, T(0));
+            grid_of_engine<T>(e), 0, T(0), 0);   // exact lists (prepare_lists)
     }
     // momentum writes dvdt = 0 for walls (physics.py:128-131)
     if (nw > 0)
@@ -1901,7 +2050,7 @@ static void sub_momentum(SphEngine* e, T half, T next_full, bool fuse, bool zero
     if (e->nf > 0)
         launch_pdl(pdl_for(e), k_mom<T, D>, grid_for(e->nf, kSweepThreads), kSweepThreads, s, E,
                    make_phys<T>(phys_of_engine(e)), cv, e->cur_rp ^ 1, 1, half, 2,
-                   grid_of_engine<T>(e), fuse ? 1 : 0, next_full);
+                   grid_of_engine<T>(e), fuse ? 1 : 0, next_full, split_filter(e) ? 0 : 1);
     else if (e->n > 0)
         cudaMemcpyAsync(E.vel[cv ^ 1], E.vel[cv], sizeof(vec4<T>) * (size_t)e->n,
                         cudaMemcpyDeviceToDevice, s);

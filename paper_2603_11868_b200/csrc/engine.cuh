@@ -40,6 +40,7 @@ struct Eng {
     const uint8_t* owned_id;
     uint32_t* offs_f; uint32_t* offs_w;
     int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; int32_t* elist;
+    uint32_t* amask;
     uint32_t* cell0; T* disp; T* disp0; uint32_t* queue; uint32_t* qcount;
     SphStepStats* stats;
 };
@@ -61,7 +62,7 @@ inline Eng<T> eng_of(const SphEngine* e)
     g.owned_id = e->owned_id;
     g.offs_f = e->offs_f; g.offs_w = e->offs_w;
     g.lists = e->lists; g.lcount = e->lcount; g.acount = e->acount; g.nww = e->nww;
-    g.elist = e->elist; g.cell0 = e->cell0; g.disp = (T*)e->disp; g.disp0 = (T*)e->disp0;
+    g.elist = e->elist; g.amask = e->amask; g.cell0 = e->cell0; g.disp = (T*)e->disp; g.disp0 = (T*)e->disp0;
     g.queue = e->queue;
     g.qcount = e->qcount; g.stats = e->stats;
     return g;
@@ -110,6 +111,13 @@ template <class T>
 __device__ __forceinline__ int64_t slot_of(const Eng<T>& E, int64_t i)
 {
     return i < E.nf ? i : E.nf_pad + (i - E.nf);
+}
+
+// accept-mask words of a slot: word w at mask_base(slot) + 32 w (a warp's
+// 32 lanes store / load one contiguous 128-byte row per word)
+__device__ __forceinline__ size_t mask_base(int64_t slot)
+{
+    return (size_t)(slot >> 5) * (kCap / 32 * 32) + (size_t)(slot & 31);
 }
 
 template <class T>

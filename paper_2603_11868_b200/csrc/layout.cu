@@ -292,9 +292,42 @@ __global__ void k_probe(Eng<T> E, int crp, double lx, double ly, double lz, doub
     o[4] = double(P4.w); o[5] = double(RP.x); o[6] = double(RP.y);
 }
 
+// report.py:187-205 snapshot fields by original id: row id of out holds
+// x[D], v[D], rho, p (run precision)
+template <class T, int D>
+__global__ void k_snapshot(Eng<T> E, int cv, int crp, T* __restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= E.n) return;
+    const vec4<T> P4 = E.pos[i], V4 = E.vel[cv][i];
+    const vec2<T> RP = E.rp[crp][i];
+    T* o = out + (size_t)E.id[i] * (2 * D + 2);
+    o[0] = P4.x; o[1] = P4.y;
+    if (D == 3) o[2] = P4.z;
+    o[D] = V4.x; o[D + 1] = V4.y;
+    if (D == 3) o[D + 2] = V4.z;
+    o[2 * D] = RP.x; o[2 * D + 1] = RP.y;
+}
+
 }  // namespace sph
 
 using namespace sph;
+
+template <class T, int D>
+static int snapshot_impl(const SphEngine* e, void* out, cudaStream_t s)
+{
+    if (e->n > 0)
+        note_launch(), k_snapshot<T, D><<<grid_for(e->n, 256), 256, 0, s>>>(
+            eng_of<T>(e), e->cur_v, e->cur_rp, (T*)out);
+    return check_launch("engine_snapshot");
+}
+
+extern "C" int sph_engine_snapshot(const SphEngine* e, void* out, cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc) return rc;
+    return SPH_DISPATCH(e, snapshot_impl, e, out, s);
+}
 
 template <class T, int D>
 static int probe_impl(const SphEngine* e, const double* loc, double radius, double* out,
@@ -401,6 +434,7 @@ static int push_impl(SphEngine* e, const void* x, const void* v, const void* rho
     e->cur_pos = 0;
     e->drifted = 0;
     e->lists_ready = 0;
+    e->nww_ready = 0;
     return check_launch("engine_push");
 }
 

@@ -863,6 +863,36 @@ class Simulation:
                 f"runaway velocity {vmax_f:.3g} at step {self.step_count}")
         return dt
 
+    def snapshot_rows(self):
+        """The snapshot fields (report.py:187-205) by original id as one
+        (n, 2 dim + 2) run-dtype array: x[dim], v[dim], rho, p; row = id.
+        Device-resident state: one gather kernel (sph_engine_snapshot) and
+        one D2H copy into a reused pinned buffer; otherwise from the
+        registry."""
+        reg = self.registry
+        n, d = reg.particle_count, reg.dim
+        if self._dev is None or not self._host_stale:
+            ids = reg.view("id").astype(np.int64)
+            out = np.empty((n, 2 * d + 2), reg.dtype)
+            out[ids, :d] = reg.view("x")
+            out[ids, d:2 * d] = reg.view("v")
+            out[ids, 2 * d] = reg.view("rho")
+            out[ids, 2 * d + 1] = reg.view("p")
+            return out
+        torch = torch_mod()
+        dv = self._dev
+        shape = (n, 2 * d + 2)
+        if dv.get("snap") is None or tuple(dv["snap"].shape) != shape:
+            dv["snap"] = torch.empty(shape, dtype=dv["tdtype"], device=dv["device"])
+            dv["snap_host"] = torch.empty(shape, dtype=dv["tdtype"], pin_memory=True)
+        with torch.cuda.stream(dv["tstream"]):
+            rc = self._lib().sph_engine_snapshot(ctypes.byref(dv["E"]), ptr(dv["snap"]),
+                                                 dv["stream"])
+            _native.check(rc, "engine_snapshot")
+            dv["snap_host"].copy_(dv["snap"], non_blocking=True)
+        dv["tstream"].synchronize()
+        return dv["snap_host"].numpy()
+
     def skin_entries(self):
         """(fluid, wall) totals of the current skin-list entry counts (the
         list bytes the sweeps stream; diagnostic)."""

@@ -54,3 +54,28 @@ def test_cli_runs_a_case(tmp_path, capsys):
     line = capsys.readouterr().out.strip().splitlines()[-1].split(",")
     assert line[0] == "hydrostatic" and line[1] == "cuda"
     assert (tmp_path / "report.txt").exists() and (tmp_path / "snapshot_0000.csv").exists()
+
+
+@pytest.mark.parametrize("name", sorted(RUNS))
+def test_binary_snapshots_equal_the_csv_snapshots(name, tmp_path):
+    """snapshot_format="npy" (device gather by id, one D2H copy) holds the
+    bits the reference-format CSV snapshots print: rows by id, x*, v*, rho, p."""
+    import numpy as np
+    csv_dir, npy_dir = tmp_path / "csv", tmp_path / "npy"
+    report.run_simulation(_config(name, csv_dir))
+    cfg = _config(name, npy_dir)
+    cfg.snapshot_format = "npy"
+    report.run_simulation(cfg)
+    snaps = sorted(f for f in os.listdir(csv_dir) if f.startswith("snapshot_"))
+    assert snaps
+    assert sorted(f for f in os.listdir(npy_dir) if f.startswith("snapshot_")) == \
+        [f[:-4] + ".npy" for f in snaps]
+    for f in snaps:
+        rows = np.load(npy_dir / (f[:-4] + ".npy"))
+        with open(csv_dir / f) as fh:
+            head = fh.readline().strip().split(",")
+            txt = np.loadtxt(fh, delimiter=",", dtype=np.float64, ndmin=2)
+        assert head[0] == "id" and rows.shape == (txt.shape[0], len(head) - 1)
+        assert np.array_equal(txt[:, 0], np.arange(rows.shape[0]))
+        # %.17g round-trips binary64 exactly; the run dtype widens exactly
+        assert np.array_equal(rows.astype(np.float64), txt[:, 1:])

@@ -73,3 +73,23 @@ def test_report_row_schema(tmp_path):
             assert rows[0][k] == v, k
     assert float(rows[0]["particle_updates_per_s"]) == 3028 * 30 / 2.0
     assert (tmp_path / "report.txt").read_text().startswith("case:            hydrostatic")
+
+
+def test_binary_snapshot_holds_the_csv_values_by_id(tmp_path):
+    """write_snapshot_npy (host-authoritative path) writes row = id,
+    x*, v*, rho, p: the values the reference-format CSV prints."""
+    from paper_2603_11868_b200.neighborhood import UniformGrid
+    from paper_2603_11868_b200.physics import Simulation
+    from paper_2603_11868_b200 import ExecutionPolicy
+    gold = os.path.join(HERE, "run_kleefsman", "snapshot_0000.csv")
+    reg = _snapshot_registry(gold)
+    sim = Simulation(reg, UniformGrid.from_bounds((0, 0, 0), (1, 1, 1), 0.1),
+                     ExecutionPolicy.sequenced())
+    out = tmp_path / "s.npy"
+    report.write_snapshot_npy(sim, str(out))
+    rows = np.load(out)
+    with open(gold) as fh:
+        fh.readline()
+        txt = np.loadtxt(fh, delimiter=",", dtype=np.float64, ndmin=2)
+    assert rows.dtype == np.float32 and rows.shape == (txt.shape[0], txt.shape[1] - 1)
+    assert np.array_equal(rows.astype(np.float64), txt[np.argsort(txt[:, 0]), 1:])
