@@ -119,6 +119,12 @@ int sph_copy(void* dst, const void* src, int64_t nbytes, cudaStream_t s);
  * reciprocal-based division differs from IEEE __fdiv_rn / __ddiv_rn, over n
  * pseudo-random a (binary32 h = (float)h and binary64 h) */
 int sph_selftest_div(double h, int64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t s);
+/* test support: the f32 sweeps' straight-line pair factor (physics.cuh
+ * pair_fac_spec) against the per-operation IEEE sequence for every binary32
+ * r2 bit pattern in [lo_bits, hi_bits); *bad += mismatches, *first_bad =
+ * min mismatching pattern (initialise to 0xffffffff) */
+int sph_selftest_pair_fac(double h, double alpha_d, uint32_t lo_bits, uint32_t hi_bits,
+                          unsigned long long* bad, unsigned int* first_bad, cudaStream_t s);
 
 /* physics.py:296-310 VMAX_SPEC through particle_reduce (execution.py:191-209):
  * *out (dev double) = max_i sqrt(sum_k f64(v_ik*v_ik)), identity 0.0 */

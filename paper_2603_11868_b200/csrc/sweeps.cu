@@ -435,3 +435,36 @@ extern "C" int sph_selftest_div(double h, int64_t n, uint64_t seed, unsigned lon
     note_launch(), k_selftest_div<<<148 * 8, 256, 0, s>>>((float)h, h, n, seed, bad);
     return check_launch("selftest_div");
 }
+
+// pair_fac_spec (physics.cuh, the straight-line f32 pair factor) against the
+// per-operation reference sequence for EVERY binary32 bit pattern in
+// [lo_bits, hi_bits) (positive r2; the sweeps see 0 < r2 < c^2).
+__global__ void k_selftest_pair_fac(PhysT<float> P, uint32_t lo, uint32_t hi,
+                                    unsigned long long* bad, unsigned int* first)
+{
+    unsigned long long nb = 0;
+    for (uint64_t u = (uint64_t)lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+         u < (uint64_t)hi; u += (uint64_t)gridDim.x * blockDim.x) {
+        const float r2 = __uint_as_float((uint32_t)u);
+        const double a = pair_fac_spec(r2, P), b = pair_fac_ref<float>(r2, P);
+        if (__double_as_longlong(a) != __double_as_longlong(b)) {
+            nb++;
+            atomicMin(first, (unsigned int)u);
+        }
+    }
+    nb = warp_sum(nb);
+    if (lane_id() == 0 && nb) atomicAdd(bad, nb);
+}
+
+extern "C" int sph_selftest_pair_fac(double h, double alpha_d, uint32_t lo_bits,
+                                     uint32_t hi_bits, unsigned long long* bad,
+                                     unsigned int* first_bad, cudaStream_t s)
+{
+    PhysP p{};
+    p.h = (double)(float)h;
+    p.alpha_d = (double)(float)alpha_d;
+    note_launch(), k_selftest_pair_fac<<<148 * 16, 256, 0, s>>>(make_phys<float>(p), lo_bits,
+                                                                hi_bits, bad, first_bad);
+    return check_launch("selftest_pair_fac");
+}
+
