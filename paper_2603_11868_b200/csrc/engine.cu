@@ -62,6 +62,16 @@
 #ifndef SPH_SKIN_FLUID_PASS
 #define SPH_SKIN_FLUID_PASS 1   // k_skin_tile: fluid-pair passes without wall tests
 #endif
+#ifndef SPH_SKIN_PRUNE          // drop block candidates beyond the cell box's skin reach
+#if SPH_PERIODIC                // (3D 4M skin build -4%; Taylor-Green +2%: bounded only)
+#define SPH_SKIN_PRUNE 0
+#else
+#define SPH_SKIN_PRUNE 1
+#endif
+#endif
+#ifndef SPH_SKIN_FMA
+#define SPH_SKIN_FMA 1          // skin test r2 with FMAs (not rounded like the reference)
+#endif
 #ifndef SPH_SKIN_WALL_SKIP
 #define SPH_SKIN_WALL_SKIP 1    // skip wall-only blocks once the wall-wall counts are known
 #endif
@@ -76,6 +86,9 @@
 #endif
 #ifndef SPH_MASK_LISTS      // fused filter writes an accept mask, momentum walks it
 #define SPH_MASK_LISTS 0     // (measured: continuity -9%, momentum +22%: off)
+#endif
+#ifndef SPH_ELIST_SCALAR     // continuity's exact-list stores: 4-byte stores per entry
+#define SPH_ELIST_SCALAR (D == 3)   // (1) or int4 quads assembled in registers (0); 3D -4% cont, 2D -3% PU/s
 #endif
 #ifndef SPH_LIST_CS          // list streams (skin / exact lists, ~1 GB each per
 #define SPH_LIST_CS 0        // 3D 4M sub-step) with evict-first hints (measured: 3D -1%, 2D +11%: off)
@@ -339,6 +352,57 @@ __device__ __forceinline__ T tile_r2(const T (&xi)[3], const T (&xj)[3])
     return r2;
 }
 
+// The skin test's r2 with fused multiply-adds: the skin lists only need to
+// be a superset of the pairs within cutoff + skin - margin (skin_eff keeps a
+// margin of 1e-4 relative, far above the ulp-level difference from the
+// exact r2), so this test need not round like the reference's
+template <class T, int D>
+__device__ __forceinline__ T skin_r2(const T (&xi)[3], const T (&xj)[3])
+{
+    const T dx = xi[0] - xj[0], dy = xi[1] - xj[1];
+    T r2 = fma_rn(dy, dy, dx * dx);
+    if (D == 3) {
+        const T dz = xi[2] - xj[2];
+        r2 = fma_rn(dz, dz, r2);
+    }
+    return r2;
+}
+
+// Box of cell cc widened for rounding and opened at bounded grid faces
+// (clamped particles live beyond them): a candidate farther than the skin
+// reach from it is in no skin list of the cell's particles (SPH_SKIN_PRUNE)
+template <class T, int D>
+struct CellReach {
+    T lo[3], hi[3], r2;
+    __device__ __forceinline__ CellReach(const int (&cc)[3], const GridP<T>& g, T cs2)
+    {
+        const T w = T(1e-4) * g.cs, inf = T(INFINITY);
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            const T a = g.o[k] + T(cc[k]) * g.cs;
+#if SPH_PERIODIC
+            lo[k] = a - w;
+            hi[k] = a + g.cs + w;
+#else
+            lo[k] = cc[k] > 0 ? a - w : -inf;
+            hi[k] = cc[k] < g.s[k] - 1 ? a + g.cs + w : inf;
+#endif
+        }
+        r2 = cs2 * T(1.0002);
+    }
+    __device__ __forceinline__ bool reaches(const vec4<T>& p) const
+    {
+        const T x[3] = {p.x, p.y, p.z};
+        T d2 = T(0);
+#pragma unroll
+        for (int k = 0; k < D; k++) {
+            const T d = fmax(fmax(lo[k] - x[k], x[k] - hi[k]), T(0));
+            d2 = fma_rn(d, d, d2);
+        }
+        return d2 <= r2;
+    }
+};
+
 template <class T, int D> struct SkinTile;
 #ifndef SPH_SKIN2_THREADS
 #define SPH_SKIN2_THREADS 128
@@ -461,6 +525,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
     __shared__ uint32_t sj[kP];        // candidate ids, sorted; then their indices j
     __shared__ vec4<T> spos[kC];       // positions in sorted order
     __shared__ uint32_t run_start[2 * 9], run_pre[2 * 9 + 1];
+    __shared__ int s_kept;
     const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const unsigned lt = lanemask_lt();
     const int64_t nf = E.nf;
@@ -555,20 +620,37 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         int P = 64;
         while (P < M) P <<= 1;
         int r = 0;   // k only grows: each thread's run search resumes where it stopped
+        int kept = 0;
+        const CellReach<T, D> reach(cc, g, cs2);
         for (int k = tid; k < P; k += NT) {
-            uint32_t key = 0xffffffffu;
+            uint32_t key = 0xffffffffu;   // pruned / padding: sorts to the end
             if (k < M) {
                 while (r + 1 < nruns && run_pre[r + 1] <= (uint32_t)k) r++;
-                key = E.id[run_start[r] + ((uint32_t)k - run_pre[r])];
+                const uint32_t ph = run_start[r] + ((uint32_t)k - run_pre[r]);
+                bool keep = true;
+                if (SPH_SKIN_PRUNE) {
+                    vec4<T> p = E.pos[ph];
+                    tile_image<T, D>(p, cc, g);
+                    keep = reach.reaches(p);
+                }
+                if (keep) {
+                    key = E.id[ph];
+                    kept++;
+                }
             }
             sj[k] = key;
         }
+        if (tid == 0) s_kept = 0;
         __syncthreads();
+        kept = warp_sum(kept);
+        if (lane == 0 && kept) atomicAdd(&s_kept, kept);
+        __syncthreads();
+        const int Mk = s_kept;   // candidates kept, first after the sort
         block_bitonic<NT>(sj, P);   // ids are unique: a total order
-        const int Mp = (M + 31) & ~31;
+        const int Mp = (Mk + 31) & ~31;
         for (int k = tid; k < Mp; k += NT) {
             vec4<T> p;
-            if (k < M) {
+            if (k < Mk) {
                 const uint32_t j = phys_of_id[sj[k]];
                 sj[k] = j;
                 p = E.pos[j];
@@ -608,8 +690,8 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                     const T r2a = tile_r2<T, D>(xa, xj);
                     const T r2b = tile_r2<T, D>(xb, xj);
 #else
-                    const T r2a = accept_r2<T, D>(xa, xj);
-                    const T r2b = accept_r2<T, D>(xb, xj);
+                    const T r2a = SPH_SKIN_FMA ? skin_r2<T, D>(xa, xj) : accept_r2<T, D>(xa, xj);
+                    const T r2b = SPH_SKIN_FMA ? skin_r2<T, D>(xb, xj) : accept_r2<T, D>(xb, xj);
 #endif
                     const bool jf = FO || (int64_t)j < nf;
                     const bool stA = (FO || flA || jf) && r2a < cs2 && j != (uint32_t)iA;
@@ -628,9 +710,11 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                     cntA += __popc(bA);
                     cntB += __popc(bB);
                     if (!FO && wall_pairs && (!flA || !flB)) {   // walls: static wall-wall count
-                        const bool ctA = !flA && !jf && r2a < g.c2 && r2a > T(0) &&
+                        // (the reference's exact acceptance test)
+                        const T e2a = accept_r2<T, D>(xa, xj), e2b = accept_r2<T, D>(xb, xj);
+                        const bool ctA = !flA && !jf && e2a < g.c2 && e2a > T(0) &&
                                          j != (uint32_t)iA;
-                        const bool ctB = hasB && !flB && !jf && r2b < g.c2 && r2b > T(0) &&
+                        const bool ctB = hasB && !flB && !jf && e2b < g.c2 && e2b > T(0) &&
                                          j != (uint32_t)iB;
                         naA += __popc(__ballot_sync(0xffffffffu, ctA));
                         naB += __popc(__ballot_sync(0xffffffffu, ctB));
@@ -1353,12 +1437,17 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
         int4* __restrict__ eq = reinterpret_cast<int4*>(E.elist + ell_base(i));
         int e0 = 0, e1 = 0, e2 = 0;
         cnt = 0;
+        int32_t* __restrict__ ep = E.elist + ell_base(i);
         auto store = [&](int j) {
-            const int r = cnt & 3;
-            if (r == 0) e0 = j;
-            else if (r == 1) e1 = j;
-            else if (r == 2) e2 = j;
-            else if (cnt < kCap) st_list(eq + (cnt >> 2) * 32, make_int4(e0, e1, e2, j));
+            if (SPH_ELIST_SCALAR) {   // one 4-byte store per entry
+                if (cnt < kCap) ep[ell_off(cnt)] = j;
+            } else {
+                const int r = cnt & 3;
+                if (r == 0) e0 = j;
+                else if (r == 1) e1 = j;
+                else if (r == 2) e2 = j;
+                else if (cnt < kCap) st_list(eq + (cnt >> 2) * 32, make_int4(e0, e1, e2, j));
+            }
             cnt++;
         };
         if (SPH_CONT_FILTER_QUADS) {
@@ -1373,7 +1462,7 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
                 pair(cnt, nb);
             });
         }
-        if ((cnt & 3) && cnt < kCap) st_list(eq + (cnt >> 2) * 32, make_int4(e0, e1, e2, 0));
+        if (!SPH_ELIST_SCALAR && (cnt & 3) && cnt < kCap) st_list(eq + (cnt >> 2) * 32, make_int4(e0, e1, e2, 0));
         if (cnt > kCap) {
             E.acount[i] = -1;
             flag_overflow(E, i);
