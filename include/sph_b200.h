@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 8
+#define SPH_ABI_VERSION 9
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -268,9 +268,16 @@ typedef struct {
      * the fused continuity filter, walked by the momentum sweep (the exact
      * list elist is then not materialised) */
     uint32_t* amask;
+    /* id space: 0 = ids are a permutation of 0..n-1 (checked at push);
+     * > 0 = ids are distinct values below id_range (multi-rank slabs use
+     * GLOBAL ids, so the by-id arrays -- rho_scratch_id, oflow_id, wall_id,
+     * vol_id, owned_id -- hold id_range entries; only the range is checked) */
+    int64_t id_range;
 } SphEngine;
 
 size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64);
+/* the same for an engine with SphEngine.id_range > 0 */
+size_t sph_engine_workspace_bytes_ids(int64_t n, int64_t ncells, int32_t f64, int64_t id_range);
 /* Registry-order (n,d)/(n,) device arrays <-> engine SoA.  push lays the
  * particles out (fluid/wall split, cell order) and records refpos. */
 int sph_engine_push(SphEngine* e, const void* x, const void* v, const void* rho, const void* p,

@@ -103,10 +103,11 @@ class SphEngine(C.Structure):
         ("disp0", P),
         ("few_refreshes", c_i32), ("nww_ready", c_i32),
         ("amask", P),
+        ("id_range", c_i64),
     ]
 
 
-ABI_VERSION = 8   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 9   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)
@@ -125,6 +126,7 @@ _PROTOS = {
     "sph_cll_workspace_bytes": (c_size, [c_i64, c_i64]),
     "sph_sort_workspace_bytes": (c_size, [c_i64]),
     "sph_engine_workspace_bytes": (c_size, [c_i64, c_i64, c_i32]),
+    "sph_engine_workspace_bytes_ids": (c_size, [c_i64, c_i64, c_i32, c_i64]),
     "sph_radix_sort_perm": (c_i32, [_P, c_i64, _P, _P, c_size, _P]),
     "sph_gather": (c_i32, [_P, _P, _P, c_i64, c_i32, _P]),
     "sph_copy": (c_i32, [_P, _P, c_i64, _P]),

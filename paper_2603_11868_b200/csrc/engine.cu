@@ -1859,7 +1859,7 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
         cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
         // physical index of every id (workspace scratch, free between rebuilds)
         Bump bump(e->ws, e->ws_bytes);
-        uint32_t* phys_of_id = bump.take<uint32_t>(e->n);
+        uint32_t* phys_of_id = bump.take<uint32_t>(e->id_range > e->n ? e->id_range : e->n);
         uint32_t* cells = bump.take<uint32_t>(e->n);   // nonempty cells <= n
         uint32_t* big = bump.take<uint32_t>(e->n);     // cells with > 128 candidates
         uint32_t* counts = bump.take<uint32_t>(2);

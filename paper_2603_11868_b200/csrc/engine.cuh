@@ -32,6 +32,7 @@ constexpr uint32_t kInvalidCell = 0xffffffffu;   // list is not a valid skin lis
 template <class T>
 struct Eng {
     int64_t n, nf, nw, nf_pad;
+    int64_t idr;         // ids are below idr (the by-id arrays' length)
     vec4<T>* pos;        // the current position buffer
     vec4<T>* pos_next;   // the other one (fused kick+drift writes it)
     vec4<T>* vel[2]; vec2<T>* rp[2]; vec2<T>* rq; vec4<T>* dvdt; T* drho;
@@ -50,6 +51,7 @@ inline Eng<T> eng_of(const SphEngine* e)
 {
     Eng<T> g;
     g.n = e->n; g.nf = e->nf; g.nw = e->n - e->nf; g.nf_pad = (e->nf + 31) / 32 * 32;
+    g.idr = e->id_range > 0 ? e->id_range : e->n;
     g.pos = (vec4<T>*)e->pos[e->cur_pos];
     g.pos_next = (vec4<T>*)e->pos[e->cur_pos ^ 1];
     g.vel[0] = (vec4<T>*)e->vel[0]; g.vel[1] = (vec4<T>*)e->vel[1];

@@ -30,6 +30,20 @@ __global__ void k_id_count(const uint32_t* __restrict__ id, const uint32_t* __re
     if (lane_id() == 0 && b) atomicAdd(&st->fluid_seen, (unsigned)__popc(b));
 }
 
+// id_range mode: ids only range-checked (distinct by the caller's contract)
+__global__ void k_id_range(const uint32_t* __restrict__ id, const uint32_t* __restrict__ wall,
+                           int64_t n, int64_t id_range, SphStepStats* st)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool fluid = false;
+    if (r < n) {
+        if (id[r] >= (uint64_t)id_range) st->push_error = 1;
+        fluid = wall[r] == 0;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, fluid);
+    if (lane_id() == 0 && b) atomicAdd(&st->fluid_seen, (unsigned)__popc(b));
+}
+
 __global__ void k_id_check(const uint32_t* __restrict__ cnt, int64_t n, SphStepStats* st)
 {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -83,7 +97,7 @@ __global__ void k_push_gather(Eng<T> E, const uint32_t* __restrict__ perm, const
     E.id[i] = pid;
     E.nnb[i] = nnb[r];
     E.refpos[i] = r;
-    if (pid >= (uint64_t)E.n) return;   // reported by k_id_count (push_error)
+    if (pid >= (uint64_t)E.idr) return;   // reported by k_id_count (push_error)
     E.rho_scratch_id[pid] = rho_scratch[r];
     E.oflow_id[pid] = oflow[r];
     E.wall_id[pid] = wall[r];
@@ -355,6 +369,15 @@ static size_t engine_sort_bytes(int64_t n)
     return 4 * align_up(sizeof(uint32_t) * m) + radix_hist_bytes(n);
 }
 
+extern "C" size_t sph_engine_workspace_bytes_ids(int64_t n, int64_t ncells, int32_t f64,
+                                                 int64_t id_range)
+{
+    // the skin build's phys_of_id map is indexed by id
+    const size_t base = sph_engine_workspace_bytes(n, ncells, f64);
+    const int64_t extra = id_range > n ? id_range - n : 0;
+    return base + align_up(sizeof(uint32_t) * (size_t)extra);
+}
+
 extern "C" size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64)
 {
     (void)ncells;
@@ -382,7 +405,7 @@ static int validate_ws(const SphEngine* e)
 {
     int rc = engine_validate(e);
     if (rc) return rc;
-    if (e->ws_bytes < sph_engine_workspace_bytes(e->n, e->ncells, e->f64)) {
+    if (e->ws_bytes < sph_engine_workspace_bytes_ids(e->n, e->ncells, e->f64, e->id_range)) {
         set_error("engine: workspace too small");
         return SPH_ERR_WORKSPACE;
     }
@@ -403,11 +426,16 @@ static int push_impl(SphEngine* e, const void* x, const void* v, const void* rho
     const int64_t n = e->n;
     cudaMemsetAsync(e->stats, 0, sizeof(SphStepStats), s);
     if (n > 0) {
-        uint32_t* cnt = bump.take<uint32_t>(n);
-        if (!cnt) return SPH_ERR_WORKSPACE;
-        cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)n, s);
-        note_launch(), k_id_count<<<grid_for(n, 256), 256, 0, s>>>(id, wall, n, cnt, e->stats);
-        note_launch(), k_id_check<<<grid_for(n, 256), 256, 0, s>>>(cnt, n, e->stats);
+        if (e->id_range > 0) {
+            note_launch(), k_id_range<<<grid_for(n, 256), 256, 0, s>>>(id, wall, n, e->id_range,
+                                                                       e->stats);
+        } else {
+            uint32_t* cnt = bump.take<uint32_t>(n);
+            if (!cnt) return SPH_ERR_WORKSPACE;
+            cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)n, s);
+            note_launch(), k_id_count<<<grid_for(n, 256), 256, 0, s>>>(id, wall, n, cnt, e->stats);
+            note_launch(), k_id_check<<<grid_for(n, 256), 256, 0, s>>>(cnt, n, e->stats);
+        }
         note_launch(), k_push_keys<T, D><<<grid_for(n, 256), 256, 0, s>>>(
             (const T*)x, wall, n, g, e->key_bits, sb.k0, &e->stats->oob_walls);
         int which = 0;

@@ -256,6 +256,8 @@ class DistributedSimulation:
         self.ghost_fluid = 0   # fluid ghosts received at the last step
         if hasattr(backend, "attach"):
             backend.attach(comm)
+        if hasattr(backend, "set_id_range"):   # global ids are 0 .. N-1
+            backend.set_id_range(int(comm.allreduce_i64([int(self.owned["id"].shape[0])])[0]))
 
     # -- decomposition ----------------------------------------------------------
 
@@ -507,6 +509,7 @@ class EngineBackend:
         self.E = None
         self.T = None
         self._caps = (0, 0, 0)
+        self.id_range = 0         # > 0: the engine runs on GLOBAL ids (set_id_range)
         self._skin_factor = 3.0
         self.comm_handle = None     # NCCL communicator of the library (NCCL runs)
         self.native_loop = False
@@ -526,6 +529,11 @@ class EngineBackend:
         torch.cuda.current_stream(self.device).synchronize()
         return self._native.SphStepStats.from_buffer_copy(host.numpy().tobytes())
 
+    def set_id_range(self, n_total):
+        """Ids are the global registry ids 0 .. n_total-1: the engine's by-id
+        arrays span them, so no per-step local relabelling is needed."""
+        self.id_range = int(n_total)
+
     def _ensure(self, n, nf, nw):
         from .physics import engine_alloc, engine_set_counts
         cn, cf, cw = self._caps
@@ -533,7 +541,8 @@ class EngineBackend:
             grow = lambda a, c: max(a, int(c * 1.15) + 64)   # noqa: E731
             caps = (grow(n, cn), grow(nf, cf), grow(nw, cw))
             self.E, self.T = engine_alloc(self.device, caps[0], caps[1], caps[2], self.dim,
-                                          self.f64, self.grid, self.scalars, self.sing["g"])
+                                          self.f64, self.grid, self.scalars, self.sing["g"],
+                                          id_range=self.id_range)
             self._caps = caps
         engine_set_counts(self.E, n, nf)
         self.E.owned_id = self.T["owned_id"].data_ptr()
@@ -671,15 +680,19 @@ class EngineBackend:
         wall = local["wall"]
         nf = int((wall == 0).sum())
         self._ensure(n, nf, n - nf)
-        # local id = rank of the global id (ids < 2^31: a 32-bit key sort)
-        gid_sorted, order = torch.sort(local["id"])
-        lid = torch.empty(n, dtype=torch.int32, device=self.device)
-        lid[order] = torch.arange(n, dtype=torch.int32, device=self.device)
-        self.gid_of_lid = gid_sorted
+        if self.id_range:   # global ids; ownership flags by id
+            lid = local["id"]
+            self.gid_of_lid = None
+        else:               # local id = rank of the global id (a 32-bit key sort)
+            gid_sorted, order = torch.sort(local["id"])
+            lid = torch.empty(n, dtype=torch.int32, device=self.device)
+            lid[order] = torch.arange(n, dtype=torch.int32, device=self.device)
+            self.gid_of_lid = gid_sorted
         self.n, self.n_own = n, n_owned
         owned = self.T["owned_id"]
-        owned[:n].zero_()
-        owned[lid[:n_owned].to(torch.int64)] = 1
+        li = lid.to(torch.int64)
+        owned[li[n_owned:]] = 0
+        owned[li[:n_owned]] = 1
         if n:
             args = [local[f].contiguous() for f in ("x", "v", "rho", "p", "m", "Vol",
                                                     "drho", "dvdt", "rho_scratch")]
@@ -810,5 +823,6 @@ class EngineBackend:
                      "id", "wall", "nnb", "oflow")
             self._call("sph_engine_pull", *[ctypes.c_void_p(out[f].data_ptr()) for f in order])
         own = {f: out[f][: self.n_own] for f in FIELDS}
-        own["id"] = self.gid_of_lid[own["id"].to(torch.int64)]
+        if self.gid_of_lid is not None:
+            own["id"] = self.gid_of_lid[own["id"].to(torch.int64)]
         return own

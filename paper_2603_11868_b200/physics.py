@@ -408,7 +408,7 @@ def _bits_to_double(b):
     return struct.unpack("<d", struct.pack("<Q", b))[0]
 
 
-def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
+def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=0):
     """Device storage of one engine (include/sph_b200.h SphEngine) for up to
     n_cap particles of which at most nf_cap fluid and nw_cap wall (the list
     tiles of the two segments are sized separately).  Returns the struct and
@@ -419,17 +419,22 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
     ncells = grid.cell_count
     lib = _native.lib()
     n = max(int(n_cap), 1)
+    nid = max(n, int(id_range))     # by-id arrays (global ids on slab ranks)
     tiles = max((nf_cap + 31) // 32 + (nw_cap + 31) // 32, 1)
     T = {}
     for k in ("pos0", "pos1", "vel0", "vel1", "dvdt"):
         T[k] = torch.empty((n, 4), dtype=tdt, device=dev)
     for k in ("rp0", "rp1", "rq"):
         T[k] = torch.empty((n, 2), dtype=tdt, device=dev)
-    for k in ("drho", "rho_scratch_id", "vol_id", "disp", "disp0"):
+    for k in ("drho", "disp", "disp0"):
         T[k] = torch.empty((n,), dtype=tdt, device=dev)
-    for k in ("id", "nnb", "refpos", "oflow_id", "wall_id", "cell0", "queue"):
+    for k in ("rho_scratch_id", "vol_id"):
+        T[k] = torch.empty((nid,), dtype=tdt, device=dev)
+    for k in ("id", "nnb", "refpos", "cell0", "queue"):
         T[k] = torch.empty((n,), dtype=i32, device=dev)
-    T["owned_id"] = torch.ones((n,), dtype=torch.uint8, device=dev)
+    for k in ("oflow_id", "wall_id"):
+        T[k] = torch.empty((nid,), dtype=i32, device=dev)
+    T["owned_id"] = torch.ones((nid,), dtype=torch.uint8, device=dev)
     T["offs_f"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
     T["offs_w"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
     T["lists"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
@@ -438,7 +443,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
     for k in ("lcount", "acount", "nww"):
         T[k] = torch.empty((tiles * 32,), dtype=i32, device=dev)
     T["qcount"] = torch.zeros((4,), dtype=i32, device=dev)
-    ws_bytes = lib.sph_engine_workspace_bytes(n, ncells, int(f64))
+    ws_bytes = lib.sph_engine_workspace_bytes_ids(n, ncells, int(f64), int(id_range))
     T["ws"] = torch.empty((ws_bytes,), dtype=torch.uint8, device=dev)
     T["stats"] = torch.zeros((ctypes.sizeof(_native.SphStepStats),), dtype=torch.uint8,
                              device=dev)
@@ -455,6 +460,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g):
               "qcount", "ws", "stats"):
         setattr(E, k, T[k].data_ptr())
     E.owned_id = None      # every particle owned (multi-rank runs set it)
+    E.id_range = int(id_range)
     E.ws_bytes = ws_bytes
     (cs, cutoff, h, alpha_d, c0, rho0, avisc, eps_h2) = scalars
     g = np.asarray(g)
