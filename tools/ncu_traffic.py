@@ -25,8 +25,11 @@ def _val(r, hdr, units, key):
 
 
 def traffic(path):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"],
-                         capture_output=True, text=True, check=True).stdout
+    r = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"],
+                       capture_output=True, text=True)
+    if r.returncode != 0:   # a capture that failed to import: no entry
+        return {}
+    raw = r.stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     acc = {}
