@@ -385,6 +385,7 @@ def timed_window(sim, steps, flush, stream, sampler=None):
     between steps; returns (seconds, nsubs)."""
     import torch
     times, nsubs = [], []
+    sim.list_modes = []
     if sampler is not None:
         sampler.mark_start()
     for _ in range(steps):
@@ -398,6 +399,7 @@ def timed_window(sim, steps, flush, stream, sampler=None):
         ev1.synchronize()
         times.append(ev0.elapsed_time(ev1) / 1e3)
         nsubs.append(sim.last_nsub)
+        sim.list_modes.append(getattr(sim, "last_list_mode", None))
     torch.cuda.synchronize()
     if sampler is not None:
         sampler.mark_end()
@@ -452,6 +454,7 @@ def gpu_arm(args, rank, world, local_rank):
     launches = lib.sph_kernel_launches() - launches0
     value = n * args.steps / total
     interactions_end = sim.interaction_count
+    list_modes = list(sim.list_modes)
     digest = state_digest({f: reg.view(f) for f in _ENGINE_FIELDS}) if args.digest else None
 
     # 2. roofline: the same window with per-kernel CUDA events
@@ -542,6 +545,10 @@ def gpu_arm(args, rank, world, local_rank):
         "nsub_per_step": nsubs,
         "interactions_total": int(interactions_end),
         "state_sha256": digest,
+        "skin_lists": {"built": list_modes.count("build"),
+                       "carried": list_modes.count("maintain"),
+                       "note": "steps whose skin lists were rebuilt / carried over from "
+                               "the previous step (sph_engine_maintain_lists)"},
         "sub_step_updates_per_s": n * sum(nsubs) / total,
         "setup": f"{setup}, {setup_s:.2f} s (untimed)",
         "gpu_launches": int(launches),

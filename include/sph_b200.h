@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 9
+#define SPH_ABI_VERSION 10
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -273,6 +273,18 @@ typedef struct {
      * GLOBAL ids, so the by-id arrays -- rho_scratch_id, oflow_id, wall_id,
      * vol_id, owned_id -- hold id_range entries; only the range is checked) */
     int64_t id_range;
+    /* skin lists kept across advective steps (sph_engine_maintain_lists):
+     * per particle in physical order (dev) the cell key of the current CLL
+     * (key_sorted; walls: their static cell), the key of the PREVIOUS CLL
+     * (key_prev, fluid), the last re-sort's permutation (new i <- old
+     * perm[i]) and its inverse; the second list / count buffers the
+     * maintenance writes (swapped with lists / lcount).  NULL: lists are
+     * rebuilt every step.  lists_stale: the lists were valid before the last
+     * CLL rebuild (library state). */
+    uint32_t* key_sorted; uint32_t* key_prev; uint32_t* perm; uint32_t* inv;
+    int32_t* lists_alt; int32_t* lcount_alt;
+    int32_t lists_stale;
+    int32_t reserved1;
 } SphEngine;
 
 size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64);
@@ -299,6 +311,15 @@ int sph_engine_ref_sort(SphEngine* e, cudaStream_t s);
  * back to an exact rebuild for a particle whose cell changed or whose
  * displacement bound exceeds the skin, so results are the reference's. */
 int sph_engine_build_lists(SphEngine* e, double skin, cudaStream_t s);
+/* carry the skin lists of the previous advective step across this step's
+ * CLL rebuild instead of rebuilding them (same skin; needs the persistent
+ * arrays above): entries are renumbered through the re-sort, entries whose
+ * current CLL cell left the particle's 3^d block are dropped, particles
+ * that moved INTO the block since the previous CLL are merged in id order
+ * when within cutoff + skin; particles whose list is no longer valid (cell
+ * change, displacement since the list build + the largest displacement
+ * since the full build > skin) get a fresh list of their current block */
+int sph_engine_maintain_lists(SphEngine* e, cudaStream_t s);
 /* physics.py:460-467 initialize: wall pressure + momentum + counts */
 int sph_engine_initialize(SphEngine* e, cudaStream_t s);
 /* physics.py:469-487 _shepard_filter (SHEPARD, COPY_SCALAR, DENSITY_UPDATE) */
@@ -407,6 +428,47 @@ int sph_halo_exchange(SphEngine* e, void* comm, const SphHaloPlan* plan, int32_t
  * CONTINUITY, RP_NEXT of wall ghosts after WALL), one host call per step */
 int sph_engine_substeps_slab(SphEngine* e, void* comm, const SphHaloPlan* plan, double half_dt,
                              double full_dt, int32_t nsub, cudaStream_t s);
+
+/* ---- slab bookkeeping (distributed.py) ---------------------
+ * A rank's particles in registry layout (distributed.FIELDS order): x[d],
+ * v[d], rho, p, m, Vol, drho, dvdt[d], rho_scratch (run precision), id,
+ * wall, nnb, oflow (uint32); device pointers, row-major. */
+typedef struct {
+    void* f[13];
+} SphRows;
+#define SPH_MAX_RANKS 64
+/* slab layout seen by one rank: rank r owns axis-0 cell planes
+ * [cuts[r], cuts[r+1]); halo = planes within `halo` outside a slab (ring
+ * distance when periodic); peers = the ranks exchanged with */
+typedef struct {
+    int64_t nplanes;                  /* == shape[0] */
+    double origin[3], cell_size;      /* grid (run-precision values) */
+    int64_t shape[3];
+    int32_t nranks, rank, periodic, halo;
+    int64_t cuts[SPH_MAX_RANKS + 1];
+    int32_t npeers;
+    int32_t peer[SPH_MAX_PEERS];
+} SphSlabGeom;
+/* int32 words of one packed row record */
+int32_t sph_slab_record_words(int32_t dim, int32_t f64);
+/* classify rows [0, n) by the axis-0 cell plane of x (neighborhood.py:76-84
+ * binning): lists (dev, (3 npeers + 1) x n) get per peer k the rows moving to
+ * peer k (list 3k), the kept rows in peer k's halo, fluid (3k+1) and wall
+ * (3k+2), and all kept rows (list 3 npeers); counts (dev, 3 npeers + 3) the
+ * list lengths, then counts[3 npeers + 1] > 0 when a row's new owner is no
+ * peer and counts[3 npeers + 2] = rows whose cell key clamps on some axis
+ * (the reference's out-of-bounds count, neighborhood.py:79-84) */
+int sph_slab_classify(const SphSlabGeom* g, const void* x, const uint32_t* wall, int64_t n,
+                      int32_t dim, int32_t f64, int32_t* lists, int32_t* counts, cudaStream_t s);
+/* records (n x words int32) <- rows[k] of in (rows == NULL: rows 0..n-1) */
+int sph_slab_pack(const SphRows* in, int32_t dim, int32_t f64, const int32_t* rows, int64_t n,
+                  void* out, cudaStream_t s);
+/* rows [dst_off, dst_off + n) of out <- records */
+int sph_slab_unpack(const void* records, int64_t n, const SphRows* out, int32_t dim, int32_t f64,
+                    int64_t dst_off, cudaStream_t s);
+/* rows [dst_off, dst_off + n) of out <- rows[k] of in */
+int sph_slab_gather(const SphRows* in, const int32_t* rows, int64_t n, const SphRows* out,
+                    int32_t dim, int32_t f64, int64_t dst_off, cudaStream_t s);
 
 #ifdef __cplusplus
 }

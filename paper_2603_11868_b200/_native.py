@@ -104,10 +104,30 @@ class SphEngine(C.Structure):
         ("few_refreshes", c_i32), ("nww_ready", c_i32),
         ("amask", P),
         ("id_range", c_i64),
+        ("key_sorted", P), ("key_prev", P), ("perm", P), ("inv", P),
+        ("lists_alt", P), ("lcount_alt", P),
+        ("lists_stale", c_i32), ("reserved1", c_i32),
     ]
 
 
-ABI_VERSION = 9   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+class SphRows(C.Structure):
+    _fields_ = [("f", c_void_p * 13)]
+
+
+SPH_MAX_RANKS = 64
+
+
+class SphSlabGeom(C.Structure):
+    _fields_ = [
+        ("nplanes", c_i64), ("origin", c_f64 * 3), ("cell_size", c_f64),
+        ("shape", c_i64 * 3),
+        ("nranks", c_i32), ("rank", c_i32), ("periodic", c_i32), ("halo", c_i32),
+        ("cuts", c_i64 * (SPH_MAX_RANKS + 1)),
+        ("npeers", c_i32), ("peer", c_i32 * 8),
+    ]
+
+
+ABI_VERSION = 10   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)
@@ -147,6 +167,12 @@ _PROTOS = {
     "sph_engine_phase": (c_i32, [_P, c_i32, c_f64, c_f64, _P]),
     "sph_engine_probe": (c_i32, [_P, _P, c_f64, _P, c_i32, _P, _P]),
     "sph_engine_snapshot": (c_i32, [_P, _P, _P]),
+    "sph_engine_maintain_lists": (c_i32, [_P, _P]),
+    "sph_slab_record_words": (c_i32, [c_i32, c_i32]),
+    "sph_slab_classify": (c_i32, [_P, _P, _P, c_i64, c_i32, c_i32, _P, _P, _P]),
+    "sph_slab_pack": (c_i32, [_P, c_i32, c_i32, _P, c_i64, _P, _P]),
+    "sph_slab_unpack": (c_i32, [_P, c_i64, _P, c_i32, c_i32, c_i64, _P]),
+    "sph_slab_gather": (c_i32, [_P, _P, c_i64, _P, c_i32, c_i32, c_i64, _P]),
     "sph_engine_halo_width": (c_i32, [c_i32]),
     "sph_engine_pack": (c_i32, [_P, c_i32, _P, c_i64, _P, _P]),
     "sph_halo_pack": (c_i32, [_P, _P, c_i32, c_i32, _P]),

@@ -1051,6 +1051,179 @@ k_skin_big(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E)
 }
 
 // ---------------------------------------------------------------------------
+// skin lists carried across a CLL rebuild (sph_engine_maintain_lists)
+// ---------------------------------------------------------------------------
+// The reference's candidate set of i within step s is every j whose step-s
+// CLL cell lies in the 3^d block of i's current cell (neighborhood.py:
+// 188-213).  A list valid before the rebuild (i still in its list cell, the
+// displacement test passing) holds, in ascending id, the block members of
+// the previous CLL within cutoff + skin at build time; membership changes
+// only through particles whose CLL cell changed (movers).  So the list of
+// step s = the old entries renumbered through the re-sort, minus those
+// whose new cell left the block, plus the movers that entered the block
+// within cutoff + skin now (enough: any later pair within the cutoff, with
+// the validity test holding, is within cutoff + skin now).
+template <class T>
+__device__ __forceinline__ bool axis_periodic(int k)
+{
+#if SPH_PERIODIC
+    return BoxOf<T>::L(k) > T(0);
+#else
+    (void)k;
+    return false;
+#endif
+}
+
+template <class T, int D>
+__device__ __forceinline__ void key_coords(uint32_t key, const GridP<T>& g, int (&c)[3])
+{
+    if (D == 3) {
+        c[2] = (int)(key % (uint32_t)g.s[2]);
+        key /= (uint32_t)g.s[2];
+    } else {
+        c[2] = 0;
+    }
+    c[1] = (int)(key % (uint32_t)g.s[1]);
+    c[0] = (int)(key / (uint32_t)g.s[1]);
+}
+
+// is the cell of key within the 3^d block of cell cc (clamped or wrapped)
+template <class T, int D>
+__device__ __forceinline__ bool in_block(uint32_t key, const int (&cc)[3], const GridP<T>& g)
+{
+    int c[3];
+    key_coords<T, D>(key, g, c);
+#pragma unroll
+    for (int k = 0; k < D; k++) {
+        int d = c[k] - cc[k];
+        d = d < 0 ? -d : d;
+        if (axis_periodic<T>(k) && g.s[k] - d < d) d = g.s[k] - d;
+        if (d > 1) return false;
+    }
+    return true;
+}
+
+// movers: fluid particles whose CLL cell changed in this rebuild, counted per
+// (new) cell for a CSR of arrivals
+__global__ void __launch_bounds__(256)
+k_mover_count(const uint32_t* __restrict__ key_sorted, const uint32_t* __restrict__ key_prev,
+              int64_t nf, uint32_t* __restrict__ ccount)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nf && key_sorted[i] != key_prev[i]) atomicAdd(&ccount[key_sorted[i]], 1u);
+}
+
+__global__ void __launch_bounds__(256)
+k_mover_fill(const uint32_t* __restrict__ key_sorted, const uint32_t* __restrict__ key_prev,
+             int64_t nf, uint32_t* __restrict__ cursor, uint32_t* __restrict__ movers)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nf && key_sorted[i] != key_prev[i])
+        movers[atomicAdd(&cursor[key_sorted[i]], 1u)] = (uint32_t)i;
+}
+
+#ifndef SPH_MAINTAIN_ARRIVALS
+#define SPH_MAINTAIN_ARRIVALS 8   // arrivals merged per list (more: the list is rebuilt)
+#endif
+
+template <class T, int D>
+__global__ void __launch_bounds__(128)
+k_maintain(Eng<T> E, GridP<T> g, T cs2, T s_eff, const uint32_t* __restrict__ key_sorted,
+           const uint32_t* __restrict__ key_prev, const uint32_t* __restrict__ perm,
+           const uint32_t* __restrict__ inv, const int32_t* __restrict__ lists_old,
+           const int32_t* __restrict__ lcount_old, int32_t* __restrict__ lists_new,
+           int32_t* __restrict__ lcount_new, const uint32_t* __restrict__ moff,
+           const uint32_t* __restrict__ movers)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool need = false;
+    if (i < E.n) {
+        const int64_t nf = E.nf;
+        const bool fluid = i < nf;
+        const int64_t slot = slot_of(E, i);
+        const int64_t so = fluid ? (int64_t)perm[i] : slot;   // walls never move
+        const uint32_t c0 = E.cell0[i];
+        const T dmax = T(__longlong_as_double((long long)E.stats->dmax_bits));
+        if (c0 == kInvalidCell || c0 != key_sorted[i] ||
+            RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax) > s_eff) {
+            need = true;
+        } else {
+            int cc[3];
+            key_coords<T, D>(c0, g, cc);
+            T xi[3];
+            to3<T>(E.pos[i], xi);
+            // movers that entered the block, within cutoff + skin
+            uint32_t arr[SPH_MAINTAIN_ARRIVALS];
+            int na = 0;
+            bool ovf = false;
+            int lo[3], hi[3];
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                if (k >= D) { lo[k] = hi[k] = 0; continue; }
+                if (axis_periodic<T>(k)) { lo[k] = cc[k] - 1; hi[k] = cc[k] + 1; }
+                else { lo[k] = max(cc[k] - 1, 0); hi[k] = min(cc[k] + 1, g.s[k] - 1); }
+            }
+            for (int a = lo[0]; a <= hi[0]; a++)
+                for (int b = lo[1]; b <= hi[1]; b++)
+                    for (int z = lo[2]; z <= hi[2]; z++) {
+                        const int ax = (a + g.s[0]) % g.s[0], by = (b + g.s[1]) % g.s[1];
+                        const int cz = D == 3 ? (z + g.s[2]) % g.s[2] : 0;
+                        uint32_t key = (uint32_t)ax * g.s[1] + by;
+                        if (D == 3) key = key * g.s[2] + cz;
+                        for (uint32_t m = moff[key]; m < moff[key + 1]; m++) {
+                            const uint32_t j = movers[m];
+                            if ((int64_t)j == i || in_block<T, D>(key_prev[j], cc, g)) continue;
+                            T xj[3];
+                            to3<T>(E.pos[j], xj);
+#if SPH_PERIODIC
+                            if (!(accept_r2<T, D>(xi, xj) < cs2)) continue;   // minimum image
+#else
+                            if (!(skin_r2<T, D>(xi, xj) < cs2)) continue;
+#endif
+                            if (na < SPH_MAINTAIN_ARRIVALS) arr[na++] = j;
+                            else ovf = true;
+                        }
+                    }
+            // arrivals in ascending id (insertion sort, a handful)
+            for (int u = 1; u < na; u++) {
+                const uint32_t v = arr[u], iv = E.id[v];
+                int w = u - 1;
+                while (w >= 0 && E.id[arr[w]] > iv) { arr[w + 1] = arr[w]; w--; }
+                arr[w + 1] = v;
+            }
+            const int nl = lcount_old[so];
+            int cnt = 0, a = 0;
+            int32_t* __restrict__ lp = lists_new + ell_base(slot);
+            const int32_t* __restrict__ op = lists_old + ell_base(so);
+            for (int t = 0; t < nl && !ovf; t++) {
+                const int jo = op[ell_off(t)];
+                const uint32_t j = jo < nf ? inv[jo] : (uint32_t)jo;
+                if (!in_block<T, D>(key_sorted[j], cc, g)) continue;   // left the block
+                const uint32_t idj = E.id[j];
+                while (a < na && E.id[arr[a]] < idj) {
+                    if (cnt < kCap) lp[ell_off(cnt)] = (int32_t)arr[a];
+                    cnt++;
+                    a++;
+                }
+                if (cnt < kCap) lp[ell_off(cnt)] = (int32_t)j;
+                cnt++;
+            }
+            for (; a < na; a++) {
+                if (cnt < kCap) lp[ell_off(cnt)] = (int32_t)arr[a];
+                cnt++;
+            }
+            if (ovf || cnt > kCap) need = true;
+            else lcount_new[slot] = cnt;
+        }
+        if (need) {
+            E.cell0[i] = kInvalidCell;
+            lcount_new[slot] = 0;
+        }
+    }
+    enqueue(E.queue, E.qcount, need, (uint32_t)i);
+}
+
+// ---------------------------------------------------------------------------
 // per-sub-step list maintenance
 // ---------------------------------------------------------------------------
 // physics.py:526-529 KICK(half) then DRIFT(full) of one fluid particle
@@ -1891,6 +2064,61 @@ extern "C" int sph_engine_build_lists(SphEngine* e, double skin, cudaStream_t s)
     int rc = engine_begin(e, s);
     if (rc) return rc;
     return SPH_DISPATCH(e, build_lists_impl, e, skin, s);
+}
+
+template <class T, int D> static void launch_fix(const SphEngine* e, cudaStream_t s);
+
+template <class T, int D>
+static int maintain_impl(SphEngine* e, cudaStream_t s)
+{
+    if (!e->key_sorted || !e->key_prev || !e->perm || !e->inv || !e->lists_alt ||
+        !e->lcount_alt) {
+        set_error("engine_maintain_lists: the persistent-list arrays are not set");
+        return SPH_ERR_INVALID;
+    }
+    if (!e->lists_stale) {
+        set_error("engine_maintain_lists: no valid lists before the CLL rebuild");
+        return SPH_ERR_INVALID;
+    }
+    const int64_t nc = e->ncells + 1, nf = e->nf;
+    Bump bump(e->ws, e->ws_bytes);
+    uint32_t* ccount = bump.take<uint32_t>(nc);
+    uint32_t* moff = bump.take<uint32_t>(nc);
+    uint32_t* cursor = bump.take<uint32_t>(nc);
+    uint32_t* movers = bump.take<uint32_t>(nf > 0 ? nf : 1);
+    void* scr = bump.take<char>(scan_scratch_bytes(nc));
+    if (!scr) return SPH_ERR_WORKSPACE;
+    // arrivals by cell (CSR over the movers' new cells)
+    cudaMemsetAsync(ccount, 0, sizeof(uint32_t) * (size_t)nc, s);
+    if (nf > 0)
+        note_launch(), k_mover_count<<<grid_for(nf, 256), 256, 0, s>>>(e->key_sorted,
+                                                                       e->key_prev, nf, ccount);
+    int rc = exclusive_scan_u32(ccount, moff, nc, scr, s);
+    if (rc) return rc;
+    cudaMemcpyAsync(cursor, moff, sizeof(uint32_t) * (size_t)nc, cudaMemcpyDeviceToDevice, s);
+    if (nf > 0)
+        note_launch(), k_mover_fill<<<grid_for(nf, 256), 256, 0, s>>>(e->key_sorted,
+                                                                      e->key_prev, nf, cursor,
+                                                                      movers);
+    cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
+    if (e->n > 0)
+        note_launch(), k_maintain<T, D><<<grid_for(e->n, 128), 128, 0, s>>>(
+            eng_of<T>(e), grid_of_engine<T>(e), skin_cs2<T>(e), skin_eff<T>(e), e->key_sorted,
+            e->key_prev, e->perm, e->inv, e->lists, e->lcount, e->lists_alt, e->lcount_alt,
+            moff, movers);
+    int32_t* t = e->lists; e->lists = e->lists_alt; e->lists_alt = t;
+    t = e->lcount; e->lcount = e->lcount_alt; e->lcount_alt = t;
+    if (e->n > 0) launch_fix<T, D>(e, s);   // fresh lists for the queued particles
+    e->lists_ready = 1;
+    e->lists_stale = 0;
+    return check_launch("engine_maintain_lists");
+}
+
+extern "C" int sph_engine_maintain_lists(SphEngine* e, cudaStream_t s)
+{
+    int rc = engine_begin(e, s);
+    if (rc) return rc;
+    return SPH_DISPATCH(e, maintain_impl, e, s);
 }
 
 // programmatic dependent launch for the sub-step kernels (common.cuh): 2D

@@ -225,6 +225,45 @@ __global__ void k_fluid_gather(const uint32_t* __restrict__ perm, int64_t nf, in
     nnb_o[i] = nnb[r];
 }
 
+// persistent-list bookkeeping of a fluid re-sort (engine.cu maintain):
+// key_prev[i] = the previous CLL's key of new particle i (key_sorted still
+// holds the previous sorted keys, in the old order), inv = old -> new
+__global__ void __launch_bounds__(256)
+k_resort_keys(const uint32_t* __restrict__ perm, int64_t nf,
+              const uint32_t* __restrict__ key_sorted, uint32_t* __restrict__ key_prev,
+              uint32_t* __restrict__ inv)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nf) return;
+    const uint32_t o = perm[i];
+    key_prev[i] = key_sorted[o];
+    inv[o] = (uint32_t)i;
+}
+
+// the per-particle list state travels with its particle through the re-sort
+template <class T>
+__global__ void __launch_bounds__(256)
+k_resort_list_state(const uint32_t* __restrict__ perm, int64_t nf,
+                    const uint32_t* __restrict__ cell0, uint32_t* __restrict__ cell0_o,
+                    const T* __restrict__ disp, T* __restrict__ disp_o,
+                    const T* __restrict__ disp0, T* __restrict__ disp0_o)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nf) return;
+    const uint32_t o = perm[i];
+    cell0_o[i] = cell0[o];
+    disp_o[i] = disp[o];
+    disp0_o[i] = disp0[o];
+}
+
+// the static cells of the walls (push: sorted keys carry a wall flag bit)
+__global__ void __launch_bounds__(256)
+k_strip_keys(const uint32_t* __restrict__ sk, int64_t n, uint32_t mask, uint32_t* __restrict__ out)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = sk[i] & mask;
+}
+
 // exact max |v|, |dvdt| (physics.py:296-310 / 390-391) and the stability
 // inputs min rho, max run-precision |v|^2 (physics.py:554-564), all particles
 template <class T, int D>
@@ -373,19 +412,24 @@ extern "C" size_t sph_engine_workspace_bytes_ids(int64_t n, int64_t ncells, int3
                                                  int64_t id_range)
 {
     // the skin build's phys_of_id map is indexed by id
+    // (id_range itself, not id_range - n: the size must not shrink with n)
     const size_t base = sph_engine_workspace_bytes(n, ncells, f64);
-    const int64_t extra = id_range > n ? id_range - n : 0;
+    const int64_t extra = id_range > 0 ? id_range : 0;
     return base + align_up(sizeof(uint32_t) * (size_t)extra);
 }
 
 extern "C" size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64)
 {
-    (void)ncells;
     size_t m = (size_t)(n > 0 ? n : 1);
     size_t es = f64 ? 8 : 4;
     // sort scratch + spare buffers for the fused fluid gather
-    return engine_sort_bytes(n) + 2 * align_up(4 * es * m) + align_up(es * m) +
-           3 * align_up(sizeof(uint32_t) * m) + 4096;
+    const size_t rebuild = engine_sort_bytes(n) + 2 * align_up(4 * es * m) + align_up(es * m) +
+                           3 * align_up(sizeof(uint32_t) * m) + 4096;
+    // list maintenance: three per-cell arrays, the movers, scan scratch
+    const int64_t nc = ncells + 1;
+    const size_t maintain = 3 * align_up(sizeof(uint32_t) * (size_t)nc) +
+                            align_up(sizeof(uint32_t) * m) + scan_scratch_bytes(nc) + 4096;
+    return rebuild > maintain ? rebuild : maintain;
 }
 
 struct SortBufs { uint32_t *k0, *k1, *v0, *v1; void* hist; };
@@ -453,6 +497,9 @@ static int push_impl(SphEngine* e, const void* x, const void* v, const void* rho
             sk, e->nf, e->ncells, 0u, e->offs_f);
         note_launch(), k_seg_offsets<<<grid_for(e->ncells + 1, 256), 256, 0, s>>>(
             sk + e->nf, n - e->nf, e->ncells, 1u << e->key_bits, e->offs_w);
+        if (e->key_sorted)   // every particle's cell (walls keep theirs for good)
+            note_launch(), k_strip_keys<<<grid_for(n, 256), 256, 0, s>>>(
+                sk, n, (1u << e->key_bits) - 1u, e->key_sorted);
     } else {
         cudaMemsetAsync(e->offs_f, 0, sizeof(uint32_t) * (size_t)(e->ncells + 1), s);
         cudaMemsetAsync(e->offs_w, 0, sizeof(uint32_t) * (size_t)(e->ncells + 1), s);
@@ -462,6 +509,7 @@ static int push_impl(SphEngine* e, const void* x, const void* v, const void* rho
     e->cur_pos = 0;
     e->drifted = 0;
     e->lists_ready = 0;
+    e->lists_stale = 0;
     e->nww_ready = 0;
     return check_launch("engine_push");
 }
@@ -506,6 +554,8 @@ template <class T, int D>
 static int rebuild_impl(SphEngine* e, cudaStream_t s)
 {
     const int64_t nf = e->nf;
+    // lists valid until now can be carried across this rebuild (maintain)
+    e->lists_stale = e->lists_ready && e->key_sorted ? 1 : 0;
     e->lists_ready = 0;
     if (nf <= 0) return SPH_OK;
     Bump bump(e->ws, e->ws_bytes);
@@ -543,6 +593,22 @@ static int rebuild_impl(SphEngine* e, cudaStream_t s)
     e->cur_rp = crp ^ 1;
     note_launch(), k_seg_offsets<<<grid_for(e->ncells + 1, 256), 256, 0, s>>>(sk, nf, e->ncells,
                                                                              0u, e->offs_f);
+    if (e->key_sorted) {
+        note_launch(), k_resort_keys<<<grid_for(nf, 256), 256, 0, s>>>(perm, nf, e->key_sorted,
+                                                                       e->key_prev, e->inv);
+        cudaMemcpyAsync(e->key_sorted, sk, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, s);
+        cudaMemcpyAsync(e->perm, perm, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, s);
+        if (e->lists_stale) {   // list state by particle: reuse the gather's spare buffers
+            uint32_t* c0 = id_o;
+            T* d = reinterpret_cast<T*>(pos_o);
+            T* d0 = drho_o;
+            note_launch(), k_resort_list_state<T><<<grid_for(nf, 256), 256, 0, s>>>(
+                perm, nf, e->cell0, c0, (const T*)e->disp, d, (const T*)e->disp0, d0);
+            cudaMemcpyAsync(e->cell0, c0, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(e->disp, d, sizeof(T) * (size_t)nf, cudaMemcpyDeviceToDevice, s);
+            cudaMemcpyAsync(e->disp0, d0, sizeof(T) * (size_t)nf, cudaMemcpyDeviceToDevice, s);
+        }
+    }
     return check_launch("engine_rebuild_cll");
 }
 

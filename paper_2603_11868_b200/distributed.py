@@ -45,6 +45,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HALO_PLANES = 2
+SLAB_MAX_PEERS = 8     # include/sph_b200.h SPH_MAX_PEERS
 
 # per-particle state carried across ranks (registry field order)
 FIELDS = ("x", "v", "rho", "p", "m", "Vol", "drho", "dvdt", "rho_scratch",
@@ -200,21 +201,26 @@ class Comm:
                 req.wait()
         return {q: b.to(self.device) for q, b in recvs.items()}
 
-    def exchange_counts(self, counts):
-        """All ranks' send counts: counts[q] = rows this rank sends to q;
-        returns rows this rank receives from each q."""
+    def exchange_counts(self, counts, width=None):
+        """All ranks' send counts: counts[q] = rows this rank sends to q
+        (or a tuple of `width` counts); returns what this rank receives from
+        each q (ints, or lists of `width`)."""
         torch = self.torch
-        send = torch.tensor([counts.get(q, 0) for q in range(self.size)],
-                            dtype=torch.int64, device=self.wire)
+        w = width or 1
+        rows = [counts.get(q, 0 if width is None else (0,) * w) for q in range(self.size)]
+        send = torch.tensor(rows if width else [[c] for c in rows],
+                            dtype=torch.int64, device=self.wire).reshape(-1)
         if self.gloo:   # gloo has no all_to_all_single: gather the matrix
             mats = [torch.empty_like(send) for _ in range(self.size)]
             self.dist.all_gather(mats, send)
-            recv = torch.stack([m[self.rank] for m in mats])
+            recv = torch.stack([m.view(self.size, w)[self.rank] for m in mats])
         else:
             recv = torch.empty_like(send)
             self.dist.all_to_all_single(recv, send)
+            recv = recv.view(self.size, w)
         recv = recv.cpu().tolist()
-        return {q: int(recv[q]) for q in range(self.size) if q != self.rank}
+        return {q: (recv[q] if width else int(recv[q][0]))
+                for q in range(self.size) if q != self.rank}
 
 
 class DistributedSimulation:
@@ -253,6 +259,7 @@ class DistributedSimulation:
         self._sel = {}         # "fluid"/"wall" -> (send rows {q}, ghost rows {q})
         self._n_owned = 0
         self.migrated = 0      # particles sent to another rank (this rank)
+        self._layout_seen = None   # layout of the last device migration
         self.ghost_fluid = 0   # fluid ghosts received at the last step
         if hasattr(backend, "attach"):
             backend.attach(comm)
@@ -374,9 +381,108 @@ class DistributedSimulation:
 
     # -- reference API ------------------------------------------------------------
 
+    def _peers(self):
+        """The ranks this rank exchanges with: its axis-0 neighbours (a ring
+        when axis 0 is periodic; one peer when both neighbours coincide)."""
+        me, W = self.comm.rank, self.comm.size
+        if W == 1:
+            return []
+        if self.layout.periodic:
+            return sorted({(me - 1) % W, (me + 1) % W})
+        return [q for q in (me - 1, me + 1) if 0 <= q < W]
+
+    def _classify(self, fields, peers):
+        """Device classification of the owned rows (csrc/slab.cu): per peer
+        mover / fluid-halo / wall-halo row lists, the kept rows, and the
+        out-of-bounds count, with ONE device->host read of the counts."""
+        lists, cnt = self.backend.classify(fields, self.layout, self.comm.rank, peers)
+        P = len(peers)
+        if cnt[3 * P + 1]:
+            raise RuntimeError("a particle crossed more than one slab in one step")
+        return peers, lists, cnt
+
+    def _load_step_device(self):
+        """_migrate + _build_local on the device: classification, record
+        packing and row assembly are library kernels; the host sees two count
+        vectors per step (one per exchange round)."""
+        be = self.backend
+        torch = self.comm.torch
+        # round 1: movers (classified on the step-start positions).  A step
+        # moves a particle by less than a plane, so movers go to neighbours --
+        # except at the first step (any initial partition) and after a
+        # re-cut, when any rank may be the new owner
+        W, me = self.comm.size, self.comm.rank
+        everyone = [q for q in range(W) if q != me]
+        anywhere = (self._layout_seen is not self.layout) and len(everyone) <= SLAB_MAX_PEERS
+        self._layout_seen = self.layout
+        peers, lists, cnt = self._classify(self.owned, everyone if anywhere else self._peers())
+        P = len(peers)
+        oob = int(cnt[3 * P + 2])
+        sends = {q: be.pack_rows(self.owned, lists[3 * k], int(cnt[3 * k]))
+                 for k, q in enumerate(peers) if cnt[3 * k]}
+        got = self.comm.exchange(sends, self.comm.exchange_counts(
+            {q: int(cnt[3 * k]) for k, q in enumerate(peers)}), (be.record_words,), torch.int32)
+        self.migrated += sum(int(cnt[3 * k]) for k in range(P))
+        n_keep = int(cnt[3 * P])
+        if sends or got:
+            arr = [got[q] for q in sorted(got)]
+            owned = be.empty_rows(n_keep + sum(int(a.shape[0]) for a in arr))
+            be.gather_rows(self.owned, lists[3 * P], n_keep, owned, 0)
+            off = n_keep
+            for a in arr:
+                be.unpack_rows(a, owned, off)
+                off += int(a.shape[0])
+            self.owned = owned
+        # round 2: halos of the post-migration owned set (fluid records first)
+        peers, lists, cnt = self._classify(self.owned, self._peers())
+        n_own = int(self.owned["id"].shape[0])
+        sends, scount = {}, {}
+        for k, q in enumerate(peers):
+            nf, nw = int(cnt[3 * k + 1]), int(cnt[3 * k + 2])
+            scount[q] = (nf, nw)
+            if nf + nw:
+                rec = torch.empty((nf + nw, be.record_words), dtype=torch.int32,
+                                  device=self.comm.device)
+                be.pack_rows(self.owned, lists[3 * k + 1], nf, rec[:nf])
+                be.pack_rows(self.owned, lists[3 * k + 2], nw, rec[nf:])
+                sends[q] = rec
+        rcount = self.comm.exchange_counts(scount, width=2)
+        got = self.comm.exchange(sends, {q: sum(c) for q, c in rcount.items()},
+                                 (be.record_words,), torch.int32)
+        n_ghost = sum(sum(c) for c in rcount.values())
+        local = be.empty_rows(n_own + n_ghost)
+        be.copy_rows(self.owned, local, n_own)
+        sel_f, sel_w, off = ({}, {}), ({}, {}), n_own
+        dev = self.comm.device
+        for k, q in enumerate(peers):
+            nf, nw = scount[q]
+            if nf:
+                sel_f[0][q] = lists[3 * k + 1][:nf].to(torch.int64)
+            if nw:
+                sel_w[0][q] = lists[3 * k + 2][:nw].to(torch.int64)
+        for q in sorted(rcount):
+            gf, gw = rcount[q]
+            if gf + gw:
+                be.unpack_rows(got[q], local, off)
+            if gf:
+                sel_f[1][q] = torch.arange(off, off + gf, device=dev)
+            if gw:
+                sel_w[1][q] = torch.arange(off + gf, off + gf + gw, device=dev)
+            off += gf + gw
+        self._sel = {"fluid": sel_f, "wall": sel_w}
+        self._n_owned = n_own
+        self.ghost_fluid = sum(c[0] for c in rcount.values())
+        be.load(local, n_own, self.grid, count_oob=False)
+        if hasattr(be, "set_halo"):
+            be.set_halo(self._sel)
+        self.out_of_bounds += int(self.comm.allreduce_i64([oob])[0])
+
     def _load_step(self):
         if self.rebalance_every and self.step_count % self.rebalance_every == 0:
             self._rebalance()
+        if getattr(self.backend, "device_rows", False):
+            self._load_step_device()
+            return
         self._migrate()
         local = self._build_local()
         oob = self.backend.load(local, self._n_owned, self.grid)
@@ -540,9 +646,10 @@ class EngineBackend:
         if self.E is None or n > cn or nf > cf or nw > cw:
             grow = lambda a, c: max(a, int(c * 1.15) + 64)   # noqa: E731
             caps = (grow(n, cn), grow(nf, cf), grow(nw, cw))
+            # slab engines re-push every step: no persistent-list buffers
             self.E, self.T = engine_alloc(self.device, caps[0], caps[1], caps[2], self.dim,
                                           self.f64, self.grid, self.scalars, self.sing["g"],
-                                          id_range=self.id_range)
+                                          id_range=self.id_range, persist=False)
             self._caps = caps
         engine_set_counts(self.E, n, nf)
         self.E.owned_id = self.T["owned_id"].data_ptr()
@@ -672,9 +779,96 @@ class EngineBackend:
                                              self.stream)
         self._native.check(rc, "engine_substeps_slab")
 
+    # -- device row bookkeeping (csrc/slab.cu) -----------------------------------
+
+    device_rows = True
+
+    @property
+    def record_words(self):
+        return int(self.L.sph_slab_record_words(self.dim, int(self.f64)))
+
+    def _rows(self, fields):
+        R = self._native.SphRows()
+        for k, f in enumerate(FIELDS):
+            R.f[k] = fields[f].data_ptr()
+        return R
+
+    def empty_rows(self, n):
+        torch = _torch()
+        tdt, d = self.halo_dtype, self.dim
+        out = {}
+        for f in FIELDS:
+            if f in ("x", "v", "dvdt"):
+                out[f] = torch.empty((n, d), dtype=tdt, device=self.device)
+            elif f in INDEX_FIELDS:
+                out[f] = torch.empty((n,), dtype=torch.int32, device=self.device)
+            else:
+                out[f] = torch.empty((n,), dtype=tdt, device=self.device)
+        return out
+
+    def classify(self, fields, layout, rank, peers):
+        torch = _torch()
+        n = int(fields["id"].shape[0])
+        G = self._native.SphSlabGeom()
+        G.nplanes = int(self.grid.shape[0])
+        origin = self.grid.origin.astype(self.np_dtype)
+        for k in range(3):
+            G.origin[k] = float(origin[k]) if k < self.dim else 0.0
+            G.shape[k] = int(self.grid.shape[k]) if k < self.dim else 1
+        G.cell_size = float(self.np_dtype(self.grid.cell_size))
+        G.nranks, G.rank = layout.nranks, rank
+        G.periodic, G.halo = int(layout.periodic), HALO_PLANES
+        for k, c in enumerate(layout.cuts):
+            G.cuts[k] = int(c)
+        G.npeers = len(peers)
+        for k, q in enumerate(peers):
+            G.peer[k] = q
+        P = len(peers)
+        lists = torch.empty((3 * P + 1, max(n, 1)), dtype=torch.int32, device=self.device)
+        counts = torch.empty(3 * P + 3, dtype=torch.int32, device=self.device)
+        rc = self.L.sph_slab_classify(ctypes.byref(G), ctypes.c_void_p(fields["x"].data_ptr()),
+                                      ctypes.c_void_p(fields["wall"].data_ptr()), n, self.dim,
+                                      int(self.f64), ctypes.c_void_p(lists.data_ptr()),
+                                      ctypes.c_void_p(counts.data_ptr()), self.stream)
+        self._native.check(rc, "slab_classify")
+        return lists, counts.cpu().tolist()
+
+    def pack_rows(self, fields, rows, n, out=None):
+        torch = _torch()
+        if out is None:
+            out = torch.empty((n, self.record_words), dtype=torch.int32, device=self.device)
+        if n:
+            R = self._rows(fields)
+            rc = self.L.sph_slab_pack(ctypes.byref(R), self.dim, int(self.f64),
+                                      ctypes.c_void_p(rows.data_ptr()), n,
+                                      ctypes.c_void_p(out.data_ptr()), self.stream)
+            self._native.check(rc, "slab_pack")
+        return out
+
+    def unpack_rows(self, records, fields, off):
+        n = int(records.shape[0])
+        if n:
+            R = self._rows(fields)
+            rec = records.contiguous()
+            rc = self.L.sph_slab_unpack(ctypes.c_void_p(rec.data_ptr()), n, ctypes.byref(R),
+                                        self.dim, int(self.f64), off, self.stream)
+            self._native.check(rc, "slab_unpack")
+
+    def gather_rows(self, src, rows, n, dst, off):
+        if n:
+            Ri, Ro = self._rows(src), self._rows(dst)
+            rc = self.L.sph_slab_gather(ctypes.byref(Ri), ctypes.c_void_p(rows.data_ptr()), n,
+                                        ctypes.byref(Ro), self.dim, int(self.f64), off,
+                                        self.stream)
+            self._native.check(rc, "slab_gather")
+
+    def copy_rows(self, src, dst, n):
+        for f in FIELDS:
+            dst[f][:n].copy_(src[f][:n])
+
     # -- backend protocol ---------------------------------------------------------
 
-    def load(self, local, n_owned, grid):
+    def load(self, local, n_owned, grid, count_oob=True):
         torch = _torch()
         n = int(local["id"].shape[0])
         wall = local["wall"]
@@ -707,7 +901,7 @@ class EngineBackend:
         self._phys = {}
         self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_RESET))
         oob = 0
-        if n_owned:
+        if n_owned and count_oob:
             _, o = self._keys(local["x"][:n_owned])
             oob = int(o.item())
         return oob

@@ -408,7 +408,8 @@ def _bits_to_double(b):
     return struct.unpack("<d", struct.pack("<Q", b))[0]
 
 
-def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=0):
+def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=0,
+                 persist=True):
     """Device storage of one engine (include/sph_b200.h SphEngine) for up to
     n_cap particles of which at most nf_cap fluid and nw_cap wall (the list
     tiles of the two segments are sized separately).  Returns the struct and
@@ -438,6 +439,11 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=
     T["offs_f"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
     T["offs_w"] = torch.empty((ncells + 1,), dtype=i32, device=dev)
     T["lists"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
+    if persist:   # skin lists carried across steps (sph_engine_maintain_lists)
+        T["lists_alt"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
+        T["lcount_alt"] = torch.empty((tiles * 32,), dtype=i32, device=dev)
+        for k in ("key_sorted", "key_prev", "perm", "inv"):
+            T[k] = torch.empty((n,), dtype=i32, device=dev)
     T["elist"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
     T["amask"] = torch.empty((tiles, NEIGHBOR_CAPACITY // 32, 32), dtype=i32, device=dev)
     for k in ("lcount", "acount", "nww"):
@@ -461,6 +467,8 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=
         setattr(E, k, T[k].data_ptr())
     E.owned_id = None      # every particle owned (multi-rank runs set it)
     E.id_range = int(id_range)
+    for k in ("lists_alt", "lcount_alt", "key_sorted", "key_prev", "perm", "inv"):
+        setattr(E, k, T[k].data_ptr() if k in T else None)
     E.ws_bytes = ws_bytes
     (cs, cutoff, h, alpha_d, c0, rho0, avisc, eps_h2) = scalars
     g = np.asarray(g)
@@ -485,6 +493,13 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=
 SKIN_FACTOR_START = float(os.environ.get("SPH_SKIN_START", "2.0"))
 SKIN_FACTOR_FLOOR = float(os.environ.get("SPH_SKIN_FLOOR", "0.5"))
 SKIN_MARGIN = float(os.environ.get("SPH_SKIN_MARGIN", "0.02"))
+
+
+# Skin lists kept across advective steps (epochs): the skin is sized for
+# LIST_EPOCH_STEPS steps of displacement; an epoch ends (full rebuild) when
+# the largest displacement since its build passes LIST_EPOCH_LIMIT x skin.
+LIST_EPOCH_STEPS = int(os.environ.get("SPH_LIST_EPOCH_STEPS", "3"))
+LIST_EPOCH_LIMIT = float(os.environ.get("SPH_LIST_EPOCH_LIMIT", "0.5"))
 
 
 def grid_is_periodic(grid):
@@ -547,6 +562,11 @@ class Simulation:
         self._skin_factor = SKIN_FACTOR_START
         self.last_nfix = 0
         self.list_refresh = "auto"  # sub-step list upkeep: auto | pass | queue
+        # skin lists carried across steps: "auto" (when the skin allows it),
+        # or "off" (rebuilt every step)
+        self.list_epochs = os.environ.get("SPH_LIST_EPOCHS", "auto")
+        self._epoch = None          # (skin, steps) of the lists' epoch
+        self.last_list_mode = None  # "build" | "maintain" (diagnostic)
         registry.attach_engine(self)
 
     def _lib(self):
@@ -754,6 +774,34 @@ class Simulation:
     def _build_lists(self, skin):
         """Ascending-id Verlet lists within cutoff + skin (csrc/engine.cu)."""
         self._call("sph_engine_build_lists", ctypes.c_double(skin))
+        self._epoch = None
+
+    def _lists_for_step(self, vmax, amax, dt):
+        """This step's skin lists: carried over from the previous step
+        (sph_engine_maintain_lists) while the epoch's skin still covers the
+        displacement, else built afresh.  An epoch's skin is sized for
+        LIST_EPOCH_STEPS steps; where that would pass the skin cap (fast
+        flows) every step rebuilds, as before."""
+        E = self._dev["E"]
+        cutoff = float(E.cutoff)
+        est = vmax * dt + amax * dt * dt
+        cap = (0.45 if self.registry.dim == 3 else 1.0) * cutoff
+        per_step = self._skin_factor * est
+        ep = self._epoch
+        if (ep is not None and E.lists_stale and self.list_epochs == "auto"
+                and ep["dmax"] + per_step <= LIST_EPOCH_LIMIT * ep["skin"]):
+            self._call("sph_engine_maintain_lists")
+            ep["steps"] += 1
+            self.last_list_mode = "maintain"
+            return
+        k = LIST_EPOCH_STEPS if self.list_epochs == "auto" else 1
+        skin = min(k * per_step + SKIN_MARGIN * cutoff, cap)
+        if k > 1 and (skin >= cap or E.key_sorted is None):
+            skin, k = self._choose_skin(vmax, amax, dt), 1
+        self._build_lists(skin)
+        self.last_list_mode = "build"
+        if k > 1:
+            self._epoch = {"skin": skin, "steps": 1, "dmax": 0.0}
 
     def _choose_skin(self, vmax, amax, dt):
         """Skin for this step's lists: a multiple of the displacement the
@@ -809,7 +857,7 @@ class Simulation:
             dt = min(dt, end_time - self.time)
         t0 = time.perf_counter()
         with self._kernel_event("skin_build"):
-            self._build_lists(self._choose_skin(vmax, amax, dt))
+            self._lists_for_step(vmax, amax, dt)
         self.phase_seconds["cll"] += time.perf_counter() - t0
         if self.shepard_every and self.step_count > 0 \
                 and self.step_count % self.shepard_every == 0:
@@ -848,6 +896,8 @@ class Simulation:
             few = self.list_refresh == "pass"
         d["E"].few_refreshes = int(few)
         self._adapt_skin(stats.ndisp, nsub)
+        if self._epoch is not None:   # largest path length since the epoch's build
+            self._epoch["dmax"] = _bits_to_double(stats.dmax_bits)
         self.out_of_bounds += stats.oob + self._oob_walls
         self._finish_counts(stats, check=True)
         self.interaction_count += int(stats.interactions)

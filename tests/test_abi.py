@@ -26,7 +26,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_native.EXPORTED)
-    assert lib.sph_abi_version() == _native.ABI_VERSION == 9
+    assert lib.sph_abi_version() == _native.ABI_VERSION == 10
 
 
 def test_struct_layouts_match_header(tmp_path):
@@ -37,7 +37,8 @@ def test_struct_layouts_match_header(tmp_path):
     structs = {"SphSweepArgs_f32": _native.SphSweepArgs_f32,
                "SphSweepArgs_f64": _native.SphSweepArgs_f64,
                "SphStepStats": _native.SphStepStats, "SphEngine": _native.SphEngine,
-               "SphHaloPlan": _native.SphHaloPlan}
+               "SphHaloPlan": _native.SphHaloPlan, "SphRows": _native.SphRows,
+               "SphSlabGeom": _native.SphSlabGeom}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sph_b200.h"',
              'int main(void) {']
     for name, cls in structs.items():

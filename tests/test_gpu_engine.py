@@ -289,3 +289,68 @@ def test_push_checks_ids_and_follows_wall_flag_edits():
         assert sim.advance() == osim.advance()
     for f in FIELDS:
         assert reg.view(f).tobytes() == osim.f[f].tobytes(), f
+
+
+@pytest.mark.parametrize("kind", ["3d", "2d"])
+def test_engine_lists_carried_across_steps_vs_oracle(kind, monkeypatch):
+    """Skin lists kept across advective steps (sph_engine_maintain_lists:
+    renumbered through the re-sort, leavers dropped, arriving movers merged
+    by id) must give the reference's neighbour sets: long epochs with a wide
+    skin force many carried steps, movers and refreshes."""
+    from paper_2603_11868_b200 import physics
+    monkeypatch.setattr(physics, "LIST_EPOCH_STEPS", 8)
+    monkeypatch.setattr(physics, "LIST_EPOCH_LIMIT", 0.9)
+    if kind == "3d":
+        cfg, steps = cases.kleefsman_config(dp=0.02, precision="f32"), 40
+    else:
+        cfg, steps = cases.CaseConfig(case="dambreak2d", dp=0.01, precision="f32"), 80
+    reg, grid = cases.build_case(cfg)
+    osim = O.OracleSim.from_registry(reg, grid)
+    sim = Simulation(reg, grid, CUDA)
+    osim.initialize()
+    sim.initialize()
+    modes = []
+    for step in range(steps):
+        assert sim.advance() == osim.advance(), step
+        assert sim.last_nsub == osim.last_nsub, step
+        assert sim.interaction_count == osim.interaction_count, step
+        modes.append(sim.last_list_mode)
+    assert modes.count("maintain") >= steps // 3, modes
+    for f in FIELDS:
+        assert reg.view(f).tobytes() == osim.f[f].tobytes(), f
+
+
+def test_engine_lists_carried_with_clamped_free_cloud(monkeypatch):
+    """Random velocities (many movers per step, particles leaving the grid
+    and clamping) through carried lists."""
+    from paper_2603_11868_b200 import physics
+    from paper_2603_11868_b200.neighborhood import UniformGrid
+    from paper_2603_11868_b200.variables import VariableRegistry
+    monkeypatch.setattr(physics, "LIST_EPOCH_STEPS", 6)
+    monkeypatch.setattr(physics, "LIST_EPOCH_LIMIT", 0.9)
+    rng = np.random.default_rng(11)
+    n = 4000
+    reg = VariableRegistry(n, 3, dtype=np.float32)
+    physics.setup_state_variables(reg)
+    reg.raw_view("x")[:] = rng.random((n, 3)) * 0.6
+    reg.raw_view("v")[:] = rng.normal(0, 0.05, (n, 3))
+    reg.raw_view("rho")[:] = 1000.0
+    reg.raw_view("m")[:] = 1000.0 * 0.02 ** 3
+    for k, val in (("rho0", 1000.0), ("c0", 20.0), ("h", 0.026), ("dp", 0.02),
+                   ("alpha_visc", 0.02)):
+        reg.register_singular(k, val)
+    reg.register_singular("g", np.array([0.0, 0.0, -9.81]))
+    grid = UniformGrid.from_bounds((0.05, 0.05, 0.05), (0.55, 0.55, 0.55), 0.052)
+    osim = O.OracleSim.from_registry(reg, grid)
+    sim = Simulation(reg, grid, CUDA)
+    osim.initialize()
+    sim.initialize()
+    modes = []
+    for step in range(25):
+        assert sim.advance() == osim.advance(), step
+        assert sim.interaction_count == osim.interaction_count, step
+        assert sim.out_of_bounds == osim.out_of_bounds, step
+        modes.append(sim.last_list_mode)
+    assert "maintain" in modes, modes
+    for f in FIELDS:
+        assert reg.view(f).tobytes() == osim.f[f].tobytes(), f
