@@ -337,7 +337,8 @@ def checkpoint(sim, reg):
     from paper_2603_11868_b200.physics import _ENGINE_FIELDS
     arrays = {f: reg.view(f).copy() for f in _ENGINE_FIELDS}
     attrs = {k: getattr(sim, k) for k in ("step_count", "time", "interaction_count",
-                                          "out_of_bounds", "_skin_factor")}
+                                          "out_of_bounds", "_skin_factor", "_epoch_backoff")}
+    sim._epoch = None   # the re-push below invalidates the lists: a fresh epoch
     few = int(sim._dev["E"].few_refreshes)
     return arrays, attrs, few
 
@@ -353,6 +354,7 @@ def restore(sim, reg, ck, pinned=None):
         var.data[...] = a
     for k, v in attrs.items():
         setattr(sim, k, v)
+    sim._epoch = None
     sim._dev["E"].few_refreshes = few
     sim.host_modified()
 

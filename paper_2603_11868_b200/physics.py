@@ -499,7 +499,10 @@ SKIN_MARGIN = float(os.environ.get("SPH_SKIN_MARGIN", "0.02"))
 # LIST_EPOCH_STEPS steps of displacement; an epoch ends (full rebuild) when
 # the largest displacement since its build passes LIST_EPOCH_LIMIT x skin.
 LIST_EPOCH_STEPS = int(os.environ.get("SPH_LIST_EPOCH_STEPS", "3"))
-LIST_EPOCH_LIMIT = float(os.environ.get("SPH_LIST_EPOCH_LIMIT", "0.5"))
+LIST_EPOCH_LIMIT = float(os.environ.get("SPH_LIST_EPOCH_LIMIT", "0.8"))
+# an epoch that carried no step backs off for this many steps (its wider
+# skin only cost sweep work)
+LIST_EPOCH_BACKOFF = int(os.environ.get("SPH_LIST_EPOCH_BACKOFF", "8"))
 
 
 def grid_is_periodic(grid):
@@ -566,6 +569,7 @@ class Simulation:
         # or "off" (rebuilt every step)
         self.list_epochs = os.environ.get("SPH_LIST_EPOCHS", "auto")
         self._epoch = None          # (skin, steps) of the lists' epoch
+        self._epoch_backoff = 0     # steps left without epochs after a futile one
         self.last_list_mode = None  # "build" | "maintain" (diagnostic)
         registry.attach_engine(self)
 
@@ -788,13 +792,19 @@ class Simulation:
         cap = (0.45 if self.registry.dim == 3 else 1.0) * cutoff
         per_step = self._skin_factor * est
         ep = self._epoch
-        if (ep is not None and E.lists_stale and self.list_epochs == "auto"
+        auto = self.list_epochs == "auto" and self.registry.dim == 3
+        if (ep is not None and E.lists_stale and auto
                 and ep["dmax"] + per_step <= LIST_EPOCH_LIMIT * ep["skin"]):
             self._call("sph_engine_maintain_lists")
             ep["steps"] += 1
             self.last_list_mode = "maintain"
             return
-        k = LIST_EPOCH_STEPS if self.list_epochs == "auto" else 1
+        if ep is not None and ep["steps"] == 1:   # the epoch carried nothing
+            self._epoch_backoff = LIST_EPOCH_BACKOFF
+        elif self._epoch_backoff > 0:
+            self._epoch_backoff -= 1
+        # 2D lists are cheap next to a 2D step's many sub-steps: no epochs
+        k = LIST_EPOCH_STEPS if auto and self._epoch_backoff == 0 else 1
         skin = min(k * per_step + SKIN_MARGIN * cutoff, cap)
         if k > 1 and (skin >= cap or E.key_sorted is None):
             skin, k = self._choose_skin(vmax, amax, dt), 1
