@@ -565,9 +565,12 @@ class Simulation:
         self._skin_factor = SKIN_FACTOR_START
         self.last_nfix = 0
         self.list_refresh = "auto"  # sub-step list upkeep: auto | pass | queue
-        # skin lists carried across steps: "auto" (when the skin allows it),
-        # or "off" (rebuilt every step)
-        self.list_epochs = os.environ.get("SPH_LIST_EPOCHS", "auto")
+        # skin lists carried across steps: "auto" (3D, when the skin allows
+        # it), "always" (any dimension; tests) or "off" (rebuilt every step: the default -- measured on the
+        # dam break, the carried steps save list builds but the displacement
+        # test against the GLOBAL largest displacement then refreshes many
+        # lists per sub-step, profiles/r02/ab)
+        self.list_epochs = os.environ.get("SPH_LIST_EPOCHS", "off")
         self._epoch = None          # (skin, steps) of the lists' epoch
         self._epoch_backoff = 0     # steps left without epochs after a futile one
         self.last_list_mode = None  # "build" | "maintain" (diagnostic)
@@ -792,7 +795,8 @@ class Simulation:
         cap = (0.45 if self.registry.dim == 3 else 1.0) * cutoff
         per_step = self._skin_factor * est
         ep = self._epoch
-        auto = self.list_epochs == "auto" and self.registry.dim == 3
+        auto = (self.list_epochs == "auto" and self.registry.dim == 3) or \
+            self.list_epochs == "always"
         if (ep is not None and E.lists_stale and auto
                 and ep["dmax"] + per_step <= LIST_EPOCH_LIMIT * ep["skin"]):
             self._call("sph_engine_maintain_lists")

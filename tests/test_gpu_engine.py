@@ -300,6 +300,7 @@ def test_engine_lists_carried_across_steps_vs_oracle(kind, monkeypatch):
     from paper_2603_11868_b200 import physics
     monkeypatch.setattr(physics, "LIST_EPOCH_STEPS", 8)
     monkeypatch.setattr(physics, "LIST_EPOCH_LIMIT", 0.9)
+    monkeypatch.setenv("SPH_LIST_EPOCHS", "always")
     if kind == "3d":
         cfg, steps = cases.kleefsman_config(dp=0.02, precision="f32"), 40
     else:
@@ -328,6 +329,7 @@ def test_engine_lists_carried_with_clamped_free_cloud(monkeypatch):
     from paper_2603_11868_b200.variables import VariableRegistry
     monkeypatch.setattr(physics, "LIST_EPOCH_STEPS", 6)
     monkeypatch.setattr(physics, "LIST_EPOCH_LIMIT", 0.9)
+    monkeypatch.setenv("SPH_LIST_EPOCHS", "always")
     rng = np.random.default_rng(11)
     n = 4000
     reg = VariableRegistry(n, 3, dtype=np.float32)
