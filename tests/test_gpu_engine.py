@@ -356,3 +356,11 @@ def test_engine_lists_carried_with_clamped_free_cloud(monkeypatch):
     assert "maintain" in modes, modes
     for f in FIELDS:
         assert reg.view(f).tobytes() == osim.f[f].tobytes(), f
+
+
+def test_engine_vs_oracle_3d_f64():
+    """precision="f64" (every operation binary64) on
+    the 3D Kleefsman case with walls and the obstacle."""
+    cfg = cases.kleefsman_config(dp=0.04, precision="f64")
+    reg, grid = cases.build_case(cfg)
+    _oracle_vs_engine(reg, grid, 8)
