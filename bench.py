@@ -483,22 +483,27 @@ def gpu_arm(args, rank, world, local_rank):
         nbytes = sum(reg.raw_view(f).nbytes for f in _ENGINE_FIELDS)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        nsubs_e = []
+        nsubs_e, h2d, d2h = [], 0, 0
         for _ in range(args.steps):
             sim.advance()                     # push (H2D) happens inside: host dirty
+            h2d += sim.last_push_bytes
             for f in _ENGINE_FIELDS:
                 reg.view(f)                   # pull (D2H) of the step's result
+            d2h += sim.last_pull_bytes
             nsubs_e.append(sim.last_nsub)
         torch.cuda.synchronize()
         secs = time.perf_counter() - t0
         assert nsubs_e == nsubs and sim.interaction_count == interactions_end, \
             "e2e window diverged from the value window"
         e2e = {"value": n * args.steps / secs, "unit": UNIT,
-               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+               "registry_bytes": nbytes,
                "steps": args.steps, "nsub_per_step": nsubs_e,
-               "timer": "host wall clock around push (H2D, pinned) + advance + pull "
-                        "(D2H) of every registry field, same steps as `value` "
-                        "(restored checkpoint)"}
+               "timer": "host wall clock around push (H2D, pinned, every registry field) + "
+                        "advance + pull (D2H of every field the step changed; m, Vol, id, "
+                        "wall, oflow, rho_scratch are not copied back while the device "
+                        "provably holds the pushed values) + registry.view of every field, "
+                        "same steps as `value` (restored checkpoint)"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

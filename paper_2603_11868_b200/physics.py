@@ -393,6 +393,8 @@ SUBSTEP_KERNELS = ("kick_drift", "list_filter", "continuity_du", "wall_pressure"
 
 _ENGINE_FIELDS = ("x", "v", "rho", "p", "m", "Vol", "drho", "dvdt",
                   "rho_scratch", "id", "wall", "nnb", "oflow")
+# fields the engine never writes (oflow: only on overflow, which is tracked)
+_HOST_SAME_FIELDS = ("m", "Vol", "id", "wall", "oflow", "rho_scratch")
 
 
 def _key_to_double(k):
@@ -558,7 +560,13 @@ class Simulation:
         self._dev = None
         self._host_dirty = True     # host registry is authoritative
         self._host_stale = False    # device is ahead of the host registry
+        # fields whose host copy still equals the device's (the engine never
+        # writes them and the registry order has not changed since the push):
+        # a pull skips their device -> host copies
+        self._host_same = set()
         self._norms = None          # (vmax, amax) valid for the device state
+        self.last_push_bytes = 0
+        self.last_pull_bytes = 0
         self._oob_walls = 0
         self.kernel_times = None    # dict name -> [ms per launch] when profiling
         self._pending_events = []
@@ -604,13 +612,18 @@ class Simulation:
                 ctypes.byref(d["E"]), *[ptr(outs[f]) for f in _ENGINE_FIELDS],
                 d["stream"])
             _native.check(rc, "engine_pull")
+            self.last_pull_bytes = 0
             for f in _ENGINE_FIELDS:   # queued back to back, one synchronise
+                if f in self._host_same:
+                    continue
                 host = reg.raw_view(f)
+                self.last_pull_bytes += host.nbytes
                 hv = host.view(np.int32) if host.dtype == np.uint32 else host
                 torch.from_numpy(hv).copy_(outs[f], non_blocking=True)
         d["tstream"].synchronize()
         # the caller may now modify the host arrays in place
         self._host_dirty = True
+        self._host_same = set()
         self._norms = None
 
     @property
@@ -648,12 +661,14 @@ class Simulation:
             self._alloc(nf)
         d = self._dev
         st = Staging(d["device"])
+        host_push = devs is None
         if devs is None:
             # every field's upload is queued on the engine's stream before the
             # push kernels (pinned registries copy asynchronously; the
             # stats read below synchronises before the host may touch them)
             with torch_mod().cuda.stream(d["tstream"]):
                 devs = [_upload_async(reg.raw_view(f), d["device"]) for f in _ENGINE_FIELDS]
+            self.last_push_bytes = sum(reg.raw_view(f).nbytes for f in _ENGINE_FIELDS)
         else:   # caller-provided device tensors: ordered before the push
             d["tstream"].wait_stream(torch_mod().cuda.current_stream(d["device"]))
         # the id-permutation check and the fluid count run on the device
@@ -669,6 +684,10 @@ class Simulation:
             self._alloc(int(stats.fluid_seen))   # the wall flags changed: resize
             d = self._dev
         self._oob_walls = stats.oob_walls
+        # the host arrays now hold what the device holds; the engine never
+        # writes m, Vol, id, wall (nor oflow / rho_scratch outside overflow /
+        # Shepard), so those stay equal until the registry order changes
+        self._host_same = set(_HOST_SAME_FIELDS) if host_push else set()
         del devs, st
         self._host_dirty = False
         self._host_stale = False
@@ -711,6 +730,8 @@ class Simulation:
         return _native.SphStepStats.from_buffer_copy(d["stats_host"].numpy().tobytes())
 
     def _finish_counts(self, stats, check):
+        if stats.overflow:   # the sweeps flagged oflow of some particles
+            self._host_same.discard("oflow")
         if stats.overflow and check:
             raise NeighborOverflowError(
                 f"neighbor buffer capacity {NEIGHBOR_CAPACITY} exceeded")
@@ -776,6 +797,7 @@ class Simulation:
         self._ensure_device()
         self._build_lists(0.0)
         self._call("sph_engine_shepard")
+        self._host_same.discard("rho_scratch")
         self._host_stale = True
 
     def _build_lists(self, skin):
@@ -846,6 +868,7 @@ class Simulation:
                 and self.step_count % self.sort_every == 0:
             t0 = time.perf_counter()
             self._call("sph_engine_ref_sort")
+            self._host_same = set()      # the registry order changed
             self.phase_seconds["sorting"] += time.perf_counter() - t0
         flags = _native.STATS_RESET | (0 if self._norms else _native.STATS_NORMS)
         self._call("sph_engine_stats", ctypes.c_int32(flags))
@@ -877,6 +900,7 @@ class Simulation:
                 and self.step_count % self.shepard_every == 0:
             t0 = time.perf_counter()
             self._call("sph_engine_shepard")
+            self._host_same.discard("rho_scratch")
             self.phase_seconds["interactions"] += time.perf_counter() - t0
         nsub = max(1, int(math.ceil(dt / dt_ac)))
         dts = dt / nsub
