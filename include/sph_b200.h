@@ -423,6 +423,11 @@ int sph_comm_destroy(void* comm);
 /* pack, grouped ncclSend/ncclRecv with every peer, unpack -- all on s */
 int sph_halo_exchange(SphEngine* e, void* comm, const SphHaloPlan* plan, int32_t kind,
                       int32_t cls, cudaStream_t s);
+/* the step statistics (e->stats) of all ranks reduced in place with NCCL
+ * on s: flags & 1 vmax / amax (max); & 2 interactions, overflow and
+ * refresh counts (sum); & 4 min rho (min), max run-precision |v|^2 (max)
+ * and the NaN flags (or) -- the host then reads global values once */
+int sph_stats_allreduce(SphEngine* e, void* comm, int32_t flags, cudaStream_t s);
 /* the nsub sub-steps of a slab rank with the halo refreshes between the
  * phases (XV of fluid ghosts after KICK_DRIFT, RP_NEXT of fluid ghosts after
  * CONTINUITY, RP_NEXT of wall ghosts after WALL), one host call per step */

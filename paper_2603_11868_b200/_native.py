@@ -169,6 +169,7 @@ _PROTOS = {
     "sph_engine_snapshot": (c_i32, [_P, _P, _P]),
     "sph_engine_maintain_lists": (c_i32, [_P, _P]),
     "sph_slab_record_words": (c_i32, [c_i32, c_i32]),
+    "sph_stats_allreduce": (c_i32, [_P, _P, c_i32, _P]),
     "sph_slab_classify": (c_i32, [_P, _P, _P, c_i64, c_i32, c_i32, _P, _P, _P]),
     "sph_slab_pack": (c_i32, [_P, c_i32, c_i32, _P, c_i64, _P, _P]),
     "sph_slab_unpack": (c_i32, [_P, c_i64, _P, c_i32, c_i32, c_i64, _P]),

@@ -29,6 +29,8 @@ struct NcclApi {
     ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
                          cudaStream_t) = nullptr;
     ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                               ncclComm_t, cudaStream_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
 };
 
@@ -50,9 +52,10 @@ NcclApi& nccl()
     api.group_end = (decltype(api.group_end))sym("ncclGroupEnd");
     api.send = (decltype(api.send))sym("ncclSend");
     api.recv = (decltype(api.recv))sym("ncclRecv");
+    api.all_reduce = (decltype(api.all_reduce))sym("ncclAllReduce");
     api.error_string = (decltype(api.error_string))sym("ncclGetErrorString");
     api.ok = api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.group_start &&
-             api.group_end && api.send && api.recv;
+             api.group_end && api.send && api.recv && api.all_reduce;
     return api;
 }
 
@@ -163,6 +166,57 @@ extern "C" int sph_halo_exchange(SphEngine* e, void* comm, const SphHaloPlan* pl
     const int rc2 = nccl_check(api.group_end(), "ncclGroupEnd");
     if (rc || rc2) return rc ? rc : rc2;
     return sph_halo_unpack(e, plan, kind, cls, s);
+}
+
+// the step statistics of all ranks, reduced in place on the engine stream:
+// order-preserving keys and non-negative f64 bits reduce as uint64 max / min,
+// counters as sums; the NaN flags are split into one word per bit (max = OR)
+__global__ void k_stats_split(SphStepStats* st, unsigned int* w)
+{
+    w[0] = st->overflow;
+    w[1] = st->nfix;
+    w[2] = st->nan_flags & 1u;
+    w[3] = (st->nan_flags >> 1) & 1u;
+}
+__global__ void k_stats_merge(SphStepStats* st, const unsigned int* w, int flags)
+{
+    if (flags & 2) {
+        st->overflow = w[0];
+        st->nfix = w[1];
+    }
+    if (flags & 4) st->nan_flags = (w[2] ? 1u : 0u) | (w[3] ? 2u : 0u);
+}
+
+extern "C" int sph_stats_allreduce(SphEngine* e, void* comm, int32_t flags, cudaStream_t s)
+{
+    int rc = need_nccl();
+    if (rc) return rc;
+    if (!e || !e->stats || !comm || !e->ws || e->ws_bytes < 64) return SPH_ERR_INVALID;
+    NcclApi& api = nccl();
+    ncclComm_t c = (ncclComm_t)comm;
+    SphStepStats* st = e->stats;
+    unsigned int* w = reinterpret_cast<unsigned int*>(e->ws);   // free between calls
+    const bool words = (flags & 6) != 0;
+    if (words) note_launch(), k_stats_split<<<1, 1, 0, s>>>(st, w);
+    auto ar = [&](void* p, size_t n, ncclDataType_t t, ncclRedOp_t op) {
+        if (rc) return;
+        rc = nccl_check(api.all_reduce(p, p, n, t, op, c, s), "ncclAllReduce");
+    };
+    if ((rc = nccl_check(api.group_start(), "ncclGroupStart"))) return rc;
+    if (flags & 1) ar(&st->vmax_bits, 2, ncclUint64, ncclMax);   // vmax, amax (f64 bits >= 0)
+    if (flags & 2) {
+        ar(&st->interactions, 1, ncclUint64, ncclSum);
+        ar(w, 2, ncclUint32, ncclSum);                          // overflow, nfix
+    }
+    if (flags & 4) {
+        ar(&st->rho_min_key, 1, ncclUint64, ncclMin);
+        ar(&st->v2max_key, 1, ncclUint64, ncclMax);
+        ar(w + 2, 2, ncclUint32, ncclMax);                      // NaN flag bits
+    }
+    const int rc2 = nccl_check(api.group_end(), "ncclGroupEnd");
+    if (rc || rc2) return rc ? rc : rc2;
+    if (words) note_launch(), k_stats_merge<<<1, 1, 0, s>>>(st, w, flags);
+    return check_launch("stats_allreduce");
 }
 
 extern "C" int sph_engine_substeps_slab(SphEngine* e, void* comm, const SphHaloPlan* plan,

@@ -500,7 +500,8 @@ class DistributedSimulation:
 
     def _finish_counts(self):
         inter, ovf = self.backend.counters()
-        tot = self.comm.allreduce_i64([inter, ovf])
+        tot = [inter, ovf] if getattr(self.backend, "global_stats", False) else \
+            self.comm.allreduce_i64([inter, ovf])
         if tot[1]:
             from .neighborhood import NeighborOverflowError, NEIGHBOR_CAPACITY
             raise NeighborOverflowError(
@@ -512,7 +513,9 @@ class DistributedSimulation:
         from .physics import SimulationUnstableError, timestep_formula
         self._load_step()
         # compute_timestep reads only v and dvdt, which Shepard leaves alone
-        vmax, amax = self.comm.allreduce(self.backend.norms(), "max")
+        norms = self.backend.norms()
+        vmax, amax = norms if getattr(self.backend, "global_stats", False) else \
+            self.comm.allreduce(norms, "max")
         if self.fixed_dt is not None:
             dt_ac = dt_adv = self.fixed_dt
         else:
@@ -549,8 +552,9 @@ class DistributedSimulation:
         self.step_count += 1
         self.time += dt
         rho_min, v2 = self.backend.stability()
-        rho_min = float(self.comm.allreduce([rho_min], "min")[0])
-        v2 = float(self.comm.allreduce([v2], "max")[0])
+        if not getattr(self.backend, "global_stats", False):
+            rho_min = float(self.comm.allreduce([rho_min], "min")[0])
+            v2 = float(self.comm.allreduce([v2], "max")[0])
         c0 = float(self.sing["c0"])
         if rho_min <= 0.0:
             raise SimulationUnstableError(f"non-positive density at step {self.step_count}")
@@ -918,8 +922,20 @@ class EngineBackend:
             skin = min(self._skin_factor * est + 0.02 * cutoff, cap)
         self._call("sph_engine_build_lists", ctypes.c_double(skin))
 
+    @property
+    def global_stats(self):
+        """The statistics are reduced over the ranks on the device (NCCL)."""
+        return self.comm_handle is not None
+
+    def _reduce_stats(self, flags):
+        if self.comm_handle is not None:
+            rc = self.L.sph_stats_allreduce(ctypes.byref(self.E), self.comm_handle,
+                                            ctypes.c_int32(flags), self.stream)
+            self._native.check(rc, "stats_allreduce")
+
     def norms(self):
         self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_NORMS))
+        self._reduce_stats(1)
         s = self._stats()
         from .physics import _bits_to_double
         return [_bits_to_double(s.vmax_bits), _bits_to_double(s.amax_bits)]
@@ -981,17 +997,23 @@ class EngineBackend:
                        ctypes.c_void_p(phys.data_ptr()), k, ctypes.c_void_p(buf.data_ptr()))
 
     def counters(self):
+        frac = None
+        if self.comm_handle is not None:   # this rank's refreshes drive its skin
+            frac = int(self._stats().ndisp) / max(1, self.n)
+        self._reduce_stats(2)
         s = self._stats()
         self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_RESET))
-        frac = int(s.ndisp) / max(1, self.n)
+        if frac is None:
+            frac = int(s.ndisp) / max(1, self.n)
         if frac > 2e-2:
             self._skin_factor = min(self._skin_factor * 1.5, 16.0)
         return int(s.interactions), int(s.overflow)
 
     def stability(self):
-        if self.n_own == 0:
+        if self.n_own == 0 and self.comm_handle is None:
             return np.inf, 0.0
         self._call("sph_engine_stats", ctypes.c_int32(self._native.STATS_NORMS))
+        self._reduce_stats(4)
         s = self._stats()
         from .physics import _key_to_double
         rho_min = math.nan if s.nan_flags & 1 else _key_to_double(s.rho_min_key)

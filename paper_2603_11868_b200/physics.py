@@ -643,7 +643,8 @@ class Simulation:
         n = reg.particle_count
         E, T = engine_alloc(device_of(self.policy), n, nf, n - nf, reg.dim,
                             reg.dtype == np.float64, self.grid,
-                            force_scalars(reg, self.grid), reg.singular("g"))
+                            force_scalars(reg, self.grid), reg.singular("g"),
+                            persist=self.list_epochs != "off")
         engine_set_counts(E, n, nf)
         torch = torch_mod()
         # the engine's stream: every engine call and every copy to or from
