@@ -125,6 +125,12 @@ int sph_selftest_div(double h, int64_t n, uint64_t seed, unsigned long long* bad
  * min mismatching pattern (initialise to 0xffffffff) */
 int sph_selftest_pair_fac(double h, double alpha_d, uint32_t lo_bits, uint32_t hi_bits,
                           unsigned long long* bad, unsigned int* first_bad, cudaStream_t s);
+/* test support: the momentum sweep's binary32 rounding done in the FP64
+ * adder (physics.cuh rn_f32_in_f64) against __double2float_rn on n random
+ * binary64 values (half of them binary32 ties); *bad += mismatches where the
+ * fast path claims validity, *fast += values it handled */
+int sph_selftest_round_f32(int64_t n, uint64_t seed, unsigned long long* bad,
+                           unsigned long long* fast, cudaStream_t s);
 
 /* physics.py:296-310 VMAX_SPEC through particle_reduce (execution.py:191-209):
  * *out (dev double) = max_i sqrt(sum_k f64(v_ik*v_ik)), identity 0.0 */

@@ -152,6 +152,7 @@ _PROTOS = {
     "sph_copy": (c_i32, [_P, _P, c_i64, _P]),
     "sph_selftest_div": (c_i32, [c_f64, c_i64, C.c_uint64, _P, _P]),
     "sph_selftest_pair_fac": (c_i32, [c_f64, c_f64, C.c_uint32, C.c_uint32, _P, _P, _P]),
+    "sph_selftest_round_f32": (c_i32, [c_i64, C.c_uint64, _P, _P, _P]),
     "sph_engine_push": (c_i32, [_P] * 14 + [_P]),
     "sph_engine_pull": (c_i32, [_P] * 14 + [_P]),
     "sph_engine_rebuild_cll": (c_i32, [_P, _P]),

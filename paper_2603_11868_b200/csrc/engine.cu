@@ -1827,7 +1827,8 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
             const vec2<T> RQI = rq[i];
             const T rho_i = RQI.x;
             const T pi_rr = RQI.y;
-            T a[3] = {P.g[0], P.g[1], P.g[2]};
+            DvAcc<T> a;
+            a.init(P.g);
             auto loadf = [&](int j) { return NbrPVR<T>{pos[j], vel[j], rq[j]}; };
             // the accepted entries come from the continuity sweep's accept
             // mask over the skin list (valid lists), else from the exact list
@@ -1914,7 +1915,7 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
             });
             }
             vec4<T> A4;
-            A4.x = a[0]; A4.y = a[1]; A4.z = D == 3 ? a[2] : T(0); A4.w = T(0);
+            A4.x = a.out(0); A4.y = a.out(1); A4.z = D == 3 ? a.out(2) : T(0); A4.w = T(0);
             E.dvdt[i] = A4;
             E.nnb[i] = (uint32_t)acnt;
             if (kick) {

@@ -468,3 +468,46 @@ extern "C" int sph_selftest_pair_fac(double h, double alpha_d, uint32_t lo_bits,
     return check_launch("selftest_pair_fac");
 }
 
+// rn_f32_in_f64 (physics.cuh, the momentum sweep's binary32 rounding in the
+// FP64 adder) against __double2float_rn: random significands over the
+// binade band [2^-160, 2^140), half of them made exact binary32 ties (the
+// 29 low significand bits set to 1 << 28), both signs, zeros.  *bad +=
+// mismatches of the fast path where it claims validity; *fast += values it
+// handled (the rest take the conversion fallback).
+__global__ void k_selftest_round_f32(int64_t n, uint64_t seed, unsigned long long* bad,
+                                     unsigned long long* fast)
+{
+    unsigned long long nb = 0, nf = 0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t st = seed ^ (uint64_t)k * 0x9e3779b97f4a7c15ull;
+        const uint64_t u = splitmix64(st), v = splitmix64(st);
+        uint64_t mant = u & 0xfffffffffffffull;
+        if (v & 1) mant = (mant & ~0x1fffffffull) | 0x10000000ull;   // a binary32 tie
+        const int e = (int)((v >> 1) % 300) - 160;
+        uint64_t bits = ((uint64_t)(e + 1023) << 52) | mant | ((v >> 20) & 1 ? (1ull << 63) : 0);
+        if ((v >> 21) % 1000 == 0) bits &= (1ull << 63);              // +-0
+        const double s = __longlong_as_double((long long)bits);
+        bool ok = true;
+        const double r = rn_f32_in_f64(s, ok);
+        if (ok) {
+            nf++;
+            if (__double_as_longlong(r) != __double_as_longlong(double(__double2float_rn(s))))
+                nb++;
+        }
+    }
+    nb = warp_sum(nb);
+    nf = warp_sum(nf);
+    if (lane_id() == 0) {
+        if (nb) atomicAdd(bad, nb);
+        atomicAdd(fast, nf);
+    }
+}
+
+extern "C" int sph_selftest_round_f32(int64_t n, uint64_t seed, unsigned long long* bad,
+                                      unsigned long long* fast, cudaStream_t s)
+{
+    note_launch(), k_selftest_round_f32<<<148 * 16, 256, 0, s>>>(n, seed, bad, fast);
+    return check_launch("selftest_round_f32");
+}
+
