@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 10
+#define SPH_ABI_VERSION 11
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -291,6 +291,13 @@ typedef struct {
     int32_t* lists_alt; int32_t* lcount_alt;
     int32_t lists_stale;
     int32_t reserved1;
+    /* local displacement bound (f32 runs with the persistent arrays): per
+     * grid cell (dev, ncells) the largest path length since the lists' build
+     * of the particles whose CLL cell it is (cellmax, float bits) and its
+     * maximum over the cell's 3^d block (blockmax); a list's validity test
+     * then uses its own block's bound instead of the global maximum.  NULL:
+     * the global bound (SphStepStats.dmax_bits). */
+    uint32_t* cellmax; uint32_t* blockmax;
 } SphEngine;
 
 size_t sph_engine_workspace_bytes(int64_t n, int64_t ncells, int32_t f64);

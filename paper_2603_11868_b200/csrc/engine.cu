@@ -1122,6 +1122,52 @@ k_mover_fill(const uint32_t* __restrict__ key_sorted, const uint32_t* __restrict
         movers[atomicAdd(&cursor[key_sorted[i]], 1u)] = (uint32_t)i;
 }
 
+// local displacement bound: the largest cellmax over each cell's 3^d block
+template <class T, int D>
+__global__ void __launch_bounds__(256)
+k_blockmax(GridP<T> g, int64_t ncells, const uint32_t* __restrict__ cellmax,
+           uint32_t* __restrict__ blockmax)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    int cc[3];
+    key_coords<T, D>((uint32_t)c, g, cc);
+    int lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+        if (k >= D) { lo[k] = hi[k] = 0; continue; }
+        if (axis_periodic<T>(k)) { lo[k] = cc[k] - 1; hi[k] = cc[k] + 1; }
+        else { lo[k] = max(cc[k] - 1, 0); hi[k] = min(cc[k] + 1, g.s[k] - 1); }
+    }
+    uint32_t m = 0;
+    for (int a = lo[0]; a <= hi[0]; a++)
+        for (int b = lo[1]; b <= hi[1]; b++)
+            for (int z = lo[2]; z <= hi[2]; z++) {
+                const int ax = (a + g.s[0]) % g.s[0], by = (b + g.s[1]) % g.s[1];
+                uint32_t key = (uint32_t)ax * g.s[1] + by;
+                if (D == 3) key = key * g.s[2] + (z + g.s[2]) % g.s[2];
+                m = max(m, cellmax[key]);
+            }
+    blockmax[c] = m;
+}
+
+// a carried epoch's path lengths into the (reset) per-cell maxima
+__global__ void __launch_bounds__(256)
+k_cellmax_seed(const uint32_t* __restrict__ key_sorted, const float* __restrict__ disp,
+               int64_t nf, uint32_t* __restrict__ cellmax)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < nf && disp[i] > 0.0f) atomicMax(&cellmax[key_sorted[i]], __float_as_uint(disp[i]));
+}
+
+template <class T, int D>
+static void launch_blockmax(const SphEngine* e, cudaStream_t s)
+{
+    if (sizeof(T) != 4 || !e->cellmax || !e->blockmax || !e->key_sorted) return;
+    note_launch(), k_blockmax<T, D><<<grid_for(e->ncells, 256), 256, 0, s>>>(
+        grid_of_engine<T>(e), e->ncells, e->cellmax, e->blockmax);
+}
+
 #ifndef SPH_MAINTAIN_ARRIVALS
 #define SPH_MAINTAIN_ARRIVALS 8   // arrivals merged per list (more: the list is rebuilt)
 #endif
@@ -1145,7 +1191,7 @@ k_maintain(Eng<T> E, GridP<T> g, T cs2, T s_eff, const uint32_t* __restrict__ ke
         const uint32_t c0 = E.cell0[i];
         const T dmax = T(__longlong_as_double((long long)E.stats->dmax_bits));
         if (c0 == kInvalidCell || c0 != key_sorted[i] ||
-            RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax) > s_eff) {
+            RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax_for(E, c0, dmax)) > s_eff) {
             need = true;
         } else {
             int cc[3];
@@ -1301,6 +1347,7 @@ k_kick_drift(Eng<T> E, int cv, int crp, GridP<T> g, T half, T full)
         E.pos[i] = P4;
         const T xc[3] = {P4.x, P4.y, P4.z};
         dnew = drift_bookkeeping<T, D>(E, g, i, xo, xn, xc);
+        note_disp(E, i, dnew);
     }
     const unsigned long long b = warp_max_u64(dbits(double(dnew)));
     if (lane_id() == 0 && b) atomicMax(&E.stats->dmax_bits, b);
@@ -1321,7 +1368,8 @@ k_mask(Eng<T> E, GridP<T> g, T s_eff)
         const uint32_t c0 = E.cell0[i];
         if (c0 == kInvalidCell) {
             need = true;
-        } else if (RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax) > s_eff) {
+        } else if (RN<T>::add_ru(RN<T>::sub_ru(E.disp[i], E.disp0[i]), dmax_for(E, c0, dmax)) >
+                   s_eff) {
             E.cell0[i] = kInvalidCell;
             need = true;
             atomicAdd(&E.stats->ndisp, 1u);
@@ -1390,7 +1438,8 @@ k_mark(Eng<T> E, T s_eff)
         if (i < E.n) {
             if (c4[r] == kInvalidCell) {
                 need = true;
-            } else if (RN<T>::add_ru(RN<T>::sub_ru(d4[r], e4[r]), dmax) > s_eff) {
+            } else if (RN<T>::add_ru(RN<T>::sub_ru(d4[r], e4[r]), dmax_for(E, c4[r], dmax)) >
+                       s_eff) {
                 E.cell0[i] = kInvalidCell;
                 need = true;
                 atomicAdd(&E.stats->ndisp, 1u);
@@ -1524,7 +1573,8 @@ k_mark_refresh(const EngAcc<T> acc, const GridP<T> g, Eng<T> E, T cs2, T s_eff)
             if (i >= E.n) continue;
             if (c4[r] == kInvalidCell) {
                 bits |= 1u << r;
-            } else if (RN<T>::add_ru(RN<T>::sub_ru(d4[r], e4[r]), dmax) > s_eff) {
+            } else if (RN<T>::add_ru(RN<T>::sub_ru(d4[r], e4[r]), dmax_for(E, c4[r], dmax)) >
+                       s_eff) {
                 E.cell0[i] = kInvalidCell;
                 bits |= 1u << r;
                 atomicAdd(&E.stats->ndisp, 1u);
@@ -1933,6 +1983,7 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
                     E.pos_next[i] = P4;
                     const T xc[3] = {P4.x, P4.y, P4.z};
                     dnew = drift_bookkeeping<T, D>(E, g, i, xo, xn, xc);
+                    note_disp(E, i, dnew);
                 }
                 E.vel[cv ^ 1][i] = V4;
             }
@@ -2020,6 +2071,10 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
 {
     e->skin = skin > 0.0 ? skin : 0.0;
     cudaMemsetAsync(&e->stats->dmax_bits, 0, sizeof(unsigned long long), s);
+    if (e->cellmax && e->blockmax) {   // fresh lists: every path length is 0
+        cudaMemsetAsync(e->cellmax, 0, sizeof(uint32_t) * (size_t)e->ncells, s);
+        cudaMemsetAsync(e->blockmax, 0, sizeof(uint32_t) * (size_t)e->ncells, s);
+    }
     GridP<T> g = grid_of_engine<T>(e);
     EngAcc<T> acc = acc_of_engine<T>(e);
     Eng<T> E = eng_of<T>(e);
@@ -2101,6 +2156,13 @@ static int maintain_impl(SphEngine* e, cudaStream_t s)
         note_launch(), k_mover_fill<<<grid_for(nf, 256), 256, 0, s>>>(e->key_sorted,
                                                                       e->key_prev, nf, cursor,
                                                                       movers);
+    if (sizeof(T) == 4 && e->cellmax && e->blockmax) {   // local bounds of the carried lists
+        cudaMemsetAsync(e->cellmax, 0, sizeof(uint32_t) * (size_t)e->ncells, s);
+        if (nf > 0)
+            note_launch(), k_cellmax_seed<<<grid_for(nf, 256), 256, 0, s>>>(
+                e->key_sorted, (const float*)e->disp, nf, e->cellmax);
+        launch_blockmax<T, D>(e, s);
+    }
     cudaMemsetAsync(e->qcount, 0, sizeof(uint32_t), s);
     if (e->n > 0)
         note_launch(), k_maintain<T, D><<<grid_for(e->n, 128), 128, 0, s>>>(
@@ -2300,6 +2362,7 @@ static void sub_kick_drift(SphEngine* e, T half, T full, cudaStream_t s)
 template <class T, int D>
 static void sub_lists(SphEngine* e, cudaStream_t s)
 {
+    launch_blockmax<T, D>(e, s);   // local displacement bounds after the drift
     if (split_filter(e)) prepare_lists<T, D>(e, s);
     else mark_and_fix<T, D>(e, s);
 }

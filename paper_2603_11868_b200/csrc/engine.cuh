@@ -42,6 +42,7 @@ struct Eng {
     uint32_t* offs_f; uint32_t* offs_w;
     int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; int32_t* elist;
     uint32_t* amask;
+    uint32_t* cellmax; const uint32_t* blockmax; const uint32_t* key_sorted;
     uint32_t* cell0; T* disp; T* disp0; uint32_t* queue; uint32_t* qcount;
     SphStepStats* stats;
 };
@@ -64,7 +65,12 @@ inline Eng<T> eng_of(const SphEngine* e)
     g.owned_id = e->owned_id;
     g.offs_f = e->offs_f; g.offs_w = e->offs_w;
     g.lists = e->lists; g.lcount = e->lcount; g.acount = e->acount; g.nww = e->nww;
-    g.elist = e->elist; g.amask = e->amask; g.cell0 = e->cell0; g.disp = (T*)e->disp; g.disp0 = (T*)e->disp0;
+    g.elist = e->elist; g.amask = e->amask;
+    const bool local = sizeof(T) == 4 && e->cellmax && e->blockmax && e->key_sorted;
+    g.cellmax = local ? e->cellmax : nullptr;
+    g.blockmax = local ? e->blockmax : nullptr;
+    g.key_sorted = e->key_sorted;
+    g.cell0 = e->cell0; g.disp = (T*)e->disp; g.disp0 = (T*)e->disp0;
     g.queue = e->queue;
     g.qcount = e->qcount; g.stats = e->stats;
     return g;
@@ -106,6 +112,24 @@ inline EngAcc<T> acc_of_engine(const SphEngine* e)
     acc.segs = e->n > e->nf ? 2 : 1;
 #endif
     return acc;
+}
+
+// the displacement bound a list's validity test uses: the largest path
+// length in the list cell's 3^d block (local mode) or over all particles
+template <class T>
+__device__ __forceinline__ T dmax_for(const Eng<T>& E, uint32_t cell, T global)
+{
+    if (sizeof(T) == 4 && E.blockmax && cell != 0xffffffffu)
+        return T(__uint_as_float(E.blockmax[cell]));
+    return global;
+}
+
+// record a fluid particle's path length in its CLL cell's maximum
+template <class T>
+__device__ __forceinline__ void note_disp(const Eng<T>& E, int64_t i, T d)
+{
+    if (sizeof(T) == 4 && E.cellmax && i < E.nf)
+        atomicMax(&E.cellmax[E.key_sorted[i]], __float_as_uint(float(d)));
 }
 
 // list slot of particle i (walls start on a fresh 32-particle tile)

@@ -446,6 +446,9 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=
         T["lcount_alt"] = torch.empty((tiles * 32,), dtype=i32, device=dev)
         for k in ("key_sorted", "key_prev", "perm", "inv"):
             T[k] = torch.empty((n,), dtype=i32, device=dev)
+        if not f64:   # local displacement bounds (csrc engine.cu k_blockmax)
+            for k in ("cellmax", "blockmax"):
+                T[k] = torch.zeros((max(ncells, 1),), dtype=i32, device=dev)
     T["elist"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
     T["amask"] = torch.empty((tiles, NEIGHBOR_CAPACITY // 32, 32), dtype=i32, device=dev)
     for k in ("lcount", "acount", "nww"):
@@ -469,7 +472,8 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=
         setattr(E, k, T[k].data_ptr())
     E.owned_id = None      # every particle owned (multi-rank runs set it)
     E.id_range = int(id_range)
-    for k in ("lists_alt", "lcount_alt", "key_sorted", "key_prev", "perm", "inv"):
+    for k in ("lists_alt", "lcount_alt", "key_sorted", "key_prev", "perm", "inv", "cellmax",
+              "blockmax"):
         setattr(E, k, T[k].data_ptr() if k in T else None)
     E.ws_bytes = ws_bytes
     (cs, cutoff, h, alpha_d, c0, rho0, avisc, eps_h2) = scalars
@@ -505,6 +509,10 @@ LIST_EPOCH_LIMIT = float(os.environ.get("SPH_LIST_EPOCH_LIMIT", "0.8"))
 # an epoch that carried no step backs off for this many steps (its wider
 # skin only cost sweep work)
 LIST_EPOCH_BACKOFF = int(os.environ.get("SPH_LIST_EPOCH_BACKOFF", "8"))
+# with local displacement bounds: carry while the last step refreshed at most
+# this fraction of the lists per sub-step, for at most LIST_EPOCH_MAX steps
+LIST_EPOCH_REFRESH = float(os.environ.get("SPH_LIST_EPOCH_REFRESH", "0.002"))
+LIST_EPOCH_MAX = int(os.environ.get("SPH_LIST_EPOCH_MAX", "6"))
 
 
 def grid_is_periodic(grid):
@@ -820,8 +828,13 @@ class Simulation:
         ep = self._epoch
         auto = (self.list_epochs == "auto" and self.registry.dim == 3) or \
             self.list_epochs == "always"
-        if (ep is not None and E.lists_stale and auto
-                and ep["dmax"] + per_step <= LIST_EPOCH_LIMIT * ep["skin"]):
+        if ep is not None and E.cellmax is not None:
+            # local bounds: a list fails only where its own block moved; carry
+            # while the last step refreshed few lists
+            carry = (ep["refresh"] <= LIST_EPOCH_REFRESH and ep["steps"] < LIST_EPOCH_MAX)
+        else:
+            carry = ep is not None and ep["dmax"] + per_step <= LIST_EPOCH_LIMIT * ep["skin"]
+        if ep is not None and E.lists_stale and auto and carry:
             self._call("sph_engine_maintain_lists")
             ep["steps"] += 1
             self.last_list_mode = "maintain"
@@ -838,7 +851,7 @@ class Simulation:
         self._build_lists(skin)
         self.last_list_mode = "build"
         if k > 1:
-            self._epoch = {"skin": skin, "steps": 1, "dmax": 0.0}
+            self._epoch = {"skin": skin, "steps": 1, "dmax": 0.0, "refresh": 0.0}
 
     def _choose_skin(self, vmax, amax, dt):
         """Skin for this step's lists: a multiple of the displacement the
@@ -937,6 +950,7 @@ class Simulation:
         self._adapt_skin(stats.ndisp, nsub)
         if self._epoch is not None:   # largest path length since the epoch's build
             self._epoch["dmax"] = _bits_to_double(stats.dmax_bits)
+            self._epoch["refresh"] = stats.ndisp / max(1, self.registry.particle_count * nsub)
         self.out_of_bounds += stats.oob + self._oob_walls
         self._finish_counts(stats, check=True)
         self.interaction_count += int(stats.interactions)
