@@ -300,6 +300,8 @@ def test_engine_lists_carried_across_steps_vs_oracle(kind, monkeypatch):
     from paper_2603_11868_b200 import physics
     monkeypatch.setattr(physics, "LIST_EPOCH_STEPS", 8)
     monkeypatch.setattr(physics, "LIST_EPOCH_LIMIT", 0.9)
+    monkeypatch.setattr(physics, "LIST_EPOCH_REFRESH", 1.0)   # carry regardless of refreshes
+    monkeypatch.setattr(physics, "LIST_EPOCH_MAX", 10)
     monkeypatch.setenv("SPH_LIST_EPOCHS", "always")
     if kind == "3d":
         cfg, steps = cases.kleefsman_config(dp=0.02, precision="f32"), 40
@@ -329,6 +331,8 @@ def test_engine_lists_carried_with_clamped_free_cloud(monkeypatch):
     from paper_2603_11868_b200.variables import VariableRegistry
     monkeypatch.setattr(physics, "LIST_EPOCH_STEPS", 6)
     monkeypatch.setattr(physics, "LIST_EPOCH_LIMIT", 0.9)
+    monkeypatch.setattr(physics, "LIST_EPOCH_REFRESH", 1.0)
+    monkeypatch.setattr(physics, "LIST_EPOCH_MAX", 10)
     monkeypatch.setenv("SPH_LIST_EPOCHS", "always")
     rng = np.random.default_rng(11)
     n = 4000
