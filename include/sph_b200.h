@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 11
+#define SPH_ABI_VERSION 12
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -268,12 +268,6 @@ typedef struct {
      * valid (computed by the first list build after a push; walls never
      * move), so later builds skip wall-only candidate blocks */
     int32_t nww_ready;
-    /* this sub-step's accept mask over the skin lists (dev): bit t of word
-     * t/32 of a slot is set when skin entry t passed the exact test
-     * (0 < r2 < c^2); tile layout [slots/32][256/32][32] uint32.  Written by
-     * the fused continuity filter, walked by the momentum sweep (the exact
-     * list elist is then not materialised) */
-    uint32_t* amask;
     /* id space: 0 = ids are a permutation of 0..n-1 (checked at push);
      * > 0 = ids are distinct values below id_range (multi-rank slabs use
      * GLOBAL ids, so the by-id arrays -- rho_scratch_id, oflow_id, wall_id,

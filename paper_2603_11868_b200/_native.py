@@ -102,7 +102,6 @@ class SphEngine(C.Structure):
         ("period", c_f64 * 3),
         ("disp0", P),
         ("few_refreshes", c_i32), ("nww_ready", c_i32),
-        ("amask", P),
         ("id_range", c_i64),
         ("key_sorted", P), ("key_prev", P), ("perm", P), ("inv", P),
         ("lists_alt", P), ("lcount_alt", P),
@@ -128,7 +127,7 @@ class SphSlabGeom(C.Structure):
     ]
 
 
-ABI_VERSION = 11   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 12   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)

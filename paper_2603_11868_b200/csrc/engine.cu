@@ -84,9 +84,6 @@
 #ifndef SPH_CONT_FILTER_QUADS      // continuity: visit accepted entries per list quad
 #define SPH_CONT_FILTER_QUADS (D == 3)   // (measured: 3D -4.5%, 2D +23%)
 #endif
-#ifndef SPH_MASK_LISTS      // fused filter writes an accept mask, momentum walks it
-#define SPH_MASK_LISTS 0     // (measured: continuity -9%, momentum +22%: off)
-#endif
 #ifndef SPH_ELIST_SCALAR     // continuity's exact-list stores: 4-byte stores per entry
 #define SPH_ELIST_SCALAR (D == 3)   // (1) or int4 quads assembled in registers (0); 3D -4% cont, 2D -3% PU/s
 #endif
@@ -173,8 +170,7 @@ template <class T> struct NbrPR { vec4<T> p; vec2<T> rp; };
 #endif
 template <class T, int D, class Load, class Body>
 __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const T (&xi)[3],
-                                            T c2, int nl, Load load, Body body,
-                                            uint32_t* __restrict__ mp = nullptr)
+                                            T c2, int nl, Load load, Body body)
 {
     constexpr int CH = SPH_WALK_CHUNK, NM = CH / 32;
     const int32_t* __restrict__ lp = E.lists + ell_base(slot);
@@ -209,7 +205,6 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
 #pragma unroll
         for (int h = 0; h < NM; h++) {
             uint32_t mh = m[h];
-            if (mp && w0 + 32 * h < nl) mp[((w0 >> 5) + h) * 32] = mh;   // accept mask
             while (mh) {
                 const int u = __ffs(mh) - 1;
                 mh &= mh - 1;
@@ -224,15 +219,13 @@ __device__ __forceinline__ void filter_walk(const Eng<T>& E, int64_t slot, const
 // are gathered together, tested (0 < r2 < c^2, binary32), and each accepted
 // neighbour is visited right away with the position already in registers
 // (body(j, pos_j)); visits stay in list (= ascending id) order.
-// mp != nullptr: the accept bits are also stored as the slot's mask words
 template <class T, int D, class Body>
 __device__ __forceinline__ void filter_quads(const Eng<T>& E, int64_t slot, const T (&xi)[3], T c2,
-                                             int nl, Body body, uint32_t* __restrict__ mp = nullptr)
+                                             int nl, Body body)
 {
     if (nl <= 0) return;
     const int4* __restrict__ q4 = reinterpret_cast<const int4*>(E.lists + ell_base(slot));
     int4 qn = ld_list(q4);
-    uint32_t mw = 0;
     for (int u0 = 0; u0 < nl; u0 += 4) {
         const int4 q = qn;
         if (u0 + 4 < nl) qn = ld_list(q4 + ((u0 >> 2) + 1) * 32);
@@ -246,53 +239,10 @@ __device__ __forceinline__ void filter_quads(const Eng<T>& E, int64_t slot, cons
             T xj[3];
             to3<T>(pj[k], xj);
             const T r2 = accept_r2<T, D>(xi, xj);
-            if (jj[k] >= 0 && (r2 < c2) && (r2 > T(0))) {
-                if (mp) mw |= 1u << ((u0 + k) & 31);
-                body(jj[k], pj[k]);
-            }
-        }
-        if (mp && (((u0 + 4) & 31) == 0 || u0 + 4 >= nl)) {
-            mp[(u0 >> 5) * 32] = mw;
-            mw = 0;
+            if (jj[k] >= 0 && (r2 < c2) && (r2 > T(0))) body(jj[k], pj[k]);
         }
     }
 }
-
-// The accepted entries of a slot's skin list in list (= ascending id)
-// order, from the accept mask: each lane advances through its own set
-// bits, so a warp runs max(accepted) steps as over an exact list; the
-// skin-list quad holding the next entry is loaded once per quad.
-template <class T>
-struct MaskCursor {
-    const int4* __restrict__ q4;
-    const uint32_t* __restrict__ mp;
-    uint32_t m;
-    int wbase, qidx;
-    int4 q;
-    __device__ __forceinline__ void init(const Eng<T>& E, int64_t slot)
-    {
-        q4 = reinterpret_cast<const int4*>(E.lists + ell_base(slot));
-        mp = E.amask + mask_base(slot);
-        m = mp[0];
-        wbase = 0;
-        qidx = -1;
-    }
-    __device__ __forceinline__ int next()
-    {
-        while (!m) {
-            wbase += 32;
-            m = mp[wbase];   // word wbase / 32 sits at 32 * (wbase / 32)
-        }
-        const int e = wbase + __ffs(m) - 1;
-        m &= m - 1;
-        if ((e >> 2) != qidx) {
-            qidx = e >> 2;
-            q = ld_list(q4 + qidx * 32);
-        }
-        const int r = e & 3;
-        return r == 0 ? q.x : (r == 1 ? q.y : (r == 2 ? q.z : q.w));
-    }
-};
 
 __device__ __forceinline__ void enqueue(uint32_t* queue, uint32_t* qcount, bool need,
                                         uint32_t value)
@@ -1638,23 +1588,6 @@ k_cont_du(Eng<T> E, PhysT<T> P, GridP<T> g, int cv, int crp, T full)
         cnt = E.acount[i];
         if (cnt < 0) { flag_overflow(E, i); return; }
         sweep_list<T>(E, i, cnt, loadf, pair);
-    } else if (SPH_MASK_LISTS) {
-        // the accept bits go to the mask the momentum sweep walks
-        uint32_t* __restrict__ mp = E.amask + mask_base(i);
-        cnt = 0;
-        if (SPH_CONT_FILTER_QUADS) {
-            filter_quads<T, D>(E, i, xi, g.c2, E.lcount[i], [&](int j, const vec4<T>& pj) {
-                cnt++;
-                pair(cnt, NbrPV<T>{pj, vel[j]});
-            }, mp);
-        } else {
-            filter_walk<T, D>(E, i, xi, g.c2, E.lcount[i], loadf,
-                              [&](int, const NbrPV<T>& nb) {
-                cnt++;
-                pair(cnt, nb);
-            }, mp);
-        }
-        E.acount[i] = cnt;   // <= lcount <= kCap
     } else {
         // the exact list, also stored a full int4 quad at a time
         int4* __restrict__ eq = reinterpret_cast<int4*>(E.elist + ell_base(i));
@@ -1856,7 +1789,7 @@ k_wall_g(Eng<T> E, PhysT<T> P, GridP<T> g, int b, int zero_drho, int count_facto
 template <class T, int D>
 __global__ void __launch_bounds__(kSweepThreads, SPH_MOM_MINB)
 k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor, GridP<T> g,
-      int fuse, T full, int mask_ok)
+      int fuse, T full)
 {
     pdl_begin();   // PDL: wait for the previous kernel, let the next one launch
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1880,46 +1813,8 @@ k_mom(Eng<T> E, PhysT<T> P, int cv, int brp, int kick, T half, int count_factor,
             DvAcc<T> a;
             a.init(P.g);
             auto loadf = [&](int j) { return NbrPVR<T>{pos[j], vel[j], rq[j]}; };
-            // the accepted entries come from the continuity sweep's accept
-            // mask over the skin list (valid lists), else from the exact list
-            const bool use_mask = SPH_MASK_LISTS && mask_ok && E.cell0[i] != kInvalidCell;
             constexpr bool kIlp = SPH_MOM_ILP && (SPH_MOM_ILP > 1 || D == 2);
-            if (kIlp && use_mask) {
-            auto terms = [&](const NbrPVR<T>& nb, double (&t)[3]) {
-                T xj[3], vj[3], dx[3], r2, vx;
-                to3<T>(nb.p, xj);
-                to3<T>(nb.v, vj);
-                pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-                momentum_terms<T, D>(r2, vx, dx, rho_i, pi_rr, nb.rp.x, nb.rp.y, nb.p.w, P, t);
-            };
-            MaskCursor<T> mc;
-            mc.init(E, i);
-            for (int t0 = 0; t0 < acnt; t0 += 2) {
-                const bool hb = t0 + 1 < acnt;
-                const int ja = mc.next();
-                const int jb = hb ? mc.next() : ja;
-                const NbrPVR<T> na = loadf(ja), nb = loadf(jb);
-                double ta[3], tb[3];
-                terms(na, ta);
-                terms(nb, tb);
-                momentum_accumulate<T, D>(ta, a);
-                if (hb) momentum_accumulate<T, D>(tb, a);
-            }
-            } else if (use_mask) {
-                MaskCursor<T> mc;
-                mc.init(E, i);
-                int jn = acnt > 0 ? mc.next() : 0;
-                for (int t = 0; t < acnt; t++) {
-                    const int j = jn;
-                    if (t + 1 < acnt) jn = mc.next();
-                    const NbrPVR<T> nb = loadf(j);
-                    T xj[3], vj[3], dx[3], r2, vx;
-                    to3<T>(nb.p, xj);
-                    to3<T>(nb.v, vj);
-                    pair_geometry<T, D>(xi, xj, vi, vj, r2, vx, dx);
-                    momentum_pair<T, D>(r2, vx, dx, rho_i, pi_rr, nb.rp.x, nb.rp.y, nb.p.w, P, a);
-                }
-            } else if (kIlp) {
+            if (kIlp) {
             // two pairs per basic block: their terms are independent chains the
             // scheduler interleaves; accumulation stays in list order
             auto terms = [&](const NbrPVR<T>& nb, double (&t)[3]) {
@@ -2304,7 +2199,7 @@ static void init_momentum(SphEngine* e, cudaStream_t s)
         note_launch(), k_rq_fill<T><<<grid_for(e->nf, 256), 256, 0, s>>>(E, e->cur_rp, e->nf);
         note_launch(), k_mom<T, D><<<grid_for(e->nf, kSweepThreads), kSweepThreads, 0, s>>>(
             E, make_phys<T>(phys_of_engine(e)), e->cur_v, e->cur_rp, 0, T(0), 1,
-            grid_of_engine<T>(e), 0, T(0), 0);   // exact lists (prepare_lists)
+            grid_of_engine<T>(e), 0, T(0));
     }
     // momentum writes dvdt = 0 for walls (physics.py:128-131)
     if (nw > 0)
@@ -2431,7 +2326,7 @@ static void sub_momentum(SphEngine* e, T half, T next_full, bool fuse, bool zero
     if (e->nf > 0)
         launch_pdl(pdl_for(e), k_mom<T, D>, grid_for(e->nf, kSweepThreads), kSweepThreads, s, E,
                    make_phys<T>(phys_of_engine(e)), cv, e->cur_rp ^ 1, 1, half, 2,
-                   grid_of_engine<T>(e), fuse ? 1 : 0, next_full, split_filter(e) ? 0 : 1);
+                   grid_of_engine<T>(e), fuse ? 1 : 0, next_full);
     else if (e->n > 0)
         cudaMemcpyAsync(E.vel[cv ^ 1], E.vel[cv], sizeof(vec4<T>) * (size_t)e->n,
                         cudaMemcpyDeviceToDevice, s);

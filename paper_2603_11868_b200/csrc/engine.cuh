@@ -41,7 +41,6 @@ struct Eng {
     const uint8_t* owned_id;
     uint32_t* offs_f; uint32_t* offs_w;
     int32_t* lists; int32_t* lcount; int32_t* acount; int32_t* nww; int32_t* elist;
-    uint32_t* amask;
     uint32_t* cellmax; const uint32_t* blockmax; const uint32_t* key_sorted;
     uint32_t* cell0; T* disp; T* disp0; uint32_t* queue; uint32_t* qcount;
     SphStepStats* stats;
@@ -65,7 +64,7 @@ inline Eng<T> eng_of(const SphEngine* e)
     g.owned_id = e->owned_id;
     g.offs_f = e->offs_f; g.offs_w = e->offs_w;
     g.lists = e->lists; g.lcount = e->lcount; g.acount = e->acount; g.nww = e->nww;
-    g.elist = e->elist; g.amask = e->amask;
+    g.elist = e->elist;
     const bool local = sizeof(T) == 4 && e->cellmax && e->blockmax && e->key_sorted;
     g.cellmax = local ? e->cellmax : nullptr;
     g.blockmax = local ? e->blockmax : nullptr;
@@ -137,13 +136,6 @@ template <class T>
 __device__ __forceinline__ int64_t slot_of(const Eng<T>& E, int64_t i)
 {
     return i < E.nf ? i : E.nf_pad + (i - E.nf);
-}
-
-// accept-mask words of a slot: word w at mask_base(slot) + 32 w (a warp's
-// 32 lanes store / load one contiguous 128-byte row per word)
-__device__ __forceinline__ size_t mask_base(int64_t slot)
-{
-    return (size_t)(slot >> 5) * (kCap / 32 * 32) + (size_t)(slot & 31);
 }
 
 template <class T>

@@ -133,21 +133,6 @@ __global__ void k_pull(Eng<T> E, int cur_v, int cur_rp, T* __restrict__ x, T* __
     vol[r] = E.vol_id[pid];
 }
 
-// offsets of a segment from its sorted keys by filling, per particle i, the
-// cells (key[i-1], key[i]] with i (and the cells after the last key with n):
-// one coalesced pass over the keys and the offsets instead of a binary
-// search per cell (keys carry or_mask in the high bit, stripped)
-__global__ void __launch_bounds__(256)
-k_seg_offsets_fill(const uint32_t* __restrict__ keys, int64_t n, int64_t ncells,
-                   uint32_t or_mask, uint32_t* __restrict__ offsets)
-{
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i > n) return;
-    const int64_t lo = i == 0 ? 0 : (int64_t)(keys[i - 1] & ~or_mask) + 1;
-    const int64_t hi = i == n ? ncells : (int64_t)(keys[i] & ~or_mask);
-    for (int64_t c = lo; c <= hi; c++) offsets[c] = (uint32_t)i;
-}
-
 static void seg_offsets(const uint32_t* keys, int64_t n, int64_t ncells, uint32_t or_mask,
                         uint32_t* offsets, cudaStream_t s);
 
@@ -167,9 +152,6 @@ __global__ void k_seg_offsets(const uint32_t* __restrict__ keys, int64_t n, int6
     offsets[c] = (uint32_t)lo;
 }
 
-#ifndef SPH_SEG_FILL   // the fill variant serialises long runs of empty cells (the tank's
-#define SPH_SEG_FILL 0 // air and headroom: 8.6 ms vs 94 us at 16M): binary search
-#endif
 
 // fluid cell keys for the per-step re-sort (neighborhood.py:105-117 on pos)
 template <class T, int D>
@@ -387,12 +369,8 @@ __global__ void k_snapshot(Eng<T> E, int cv, int crp, T* __restrict__ out)
 static void seg_offsets(const uint32_t* keys, int64_t n, int64_t ncells, uint32_t or_mask,
                         uint32_t* offsets, cudaStream_t s)
 {
-    if (SPH_SEG_FILL)
-        note_launch(), k_seg_offsets_fill<<<grid_for(n + 1, 256), 256, 0, s>>>(
-            keys, n, ncells, or_mask, offsets);
-    else
-        note_launch(), k_seg_offsets<<<grid_for(ncells + 1, 256), 256, 0, s>>>(
-            keys, n, ncells, or_mask, offsets);
+    note_launch(), k_seg_offsets<<<grid_for(ncells + 1, 256), 256, 0, s>>>(keys, n, ncells,
+                                                                         or_mask, offsets);
 }
 
 }  // namespace sph

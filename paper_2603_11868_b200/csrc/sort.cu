@@ -155,10 +155,6 @@ int exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, void* scrat
 // ---------------------------------------------------------------------------
 // radix sort
 // ---------------------------------------------------------------------------
-#ifndef SPH_RADIX_TILE_REORDER
-#define SPH_RADIX_TILE_REORDER 0   // 32-bit keys: tile reordered in shared memory (measured
-                                   // slower on the nearly sorted per-step re-sort: off)
-#endif
 template <class K>
 __global__ void __launch_bounds__(kRsThreads)
 k_radix_hist(const K* __restrict__ keys, int64_t n, int shift, uint32_t* __restrict__ hist,
@@ -237,78 +233,6 @@ k_radix_scatter(const K* __restrict__ kin, const uint32_t* __restrict__ vin, boo
     }
 }
 
-// The same scatter for 32-bit keys with the tile reordered in shared memory
-// first: each item's tile-local position (tile digit offset + warp prefix +
-// rank, i.e. the stable order) takes its key / value, then consecutive
-// threads write consecutive tile positions -- runs of one digit land on
-// consecutive global addresses, so the stores coalesce instead of
-// scattering 32 ways per warp instruction.
-__global__ void __launch_bounds__(kRsThreads)
-k_radix_scatter_tile(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin,
-                     bool vals_identity, uint32_t* __restrict__ kout,
-                     uint32_t* __restrict__ vout, int64_t n, int shift,
-                     const uint32_t* __restrict__ offs, int64_t ntiles)
-{
-    constexpr int kWarps = kRsThreads / 32;
-    __shared__ uint32_t wcnt[kWarps][256];
-    __shared__ uint32_t gbase[256], toff[256];
-    __shared__ uint32_t skey[kRsTile], sval[kRsTile];
-    for (int w = 0; w < kWarps; w++) wcnt[w][threadIdx.x] = 0;
-    gbase[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles + blockIdx.x];
-    __syncthreads();
-
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    const int64_t tbase = (int64_t)blockIdx.x * kRsTile;
-    const int64_t wbase = tbase + (int64_t)warp * (kRsItems * 32);
-    const unsigned lt = lanemask_lt();
-    uint32_t key[kRsItems], val[kRsItems], rank[kRsItems];
-    unsigned dig[kRsItems];
-#pragma unroll
-    for (int k = 0; k < kRsItems; k++) {
-        const int64_t idx = wbase + (int64_t)k * 32 + lane;
-        const bool valid = idx < n;
-        key[k] = valid ? kin[idx] : 0u;
-        val[k] = valid ? (vals_identity ? (uint32_t)idx : vin[idx]) : 0u;
-        const unsigned d = valid ? ((key[k] >> shift) & 255u) : 256u;
-        dig[k] = d;
-        const unsigned peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t before = d < 256u ? wcnt[warp][d] : 0u;
-        __syncwarp();
-        if (d < 256u && lane == (unsigned)(__ffs(peers) - 1))
-            wcnt[warp][d] = before + (uint32_t)__popc(peers);
-        __syncwarp();
-        rank[k] = before + (uint32_t)__popc(peers & lt);
-    }
-    __syncthreads();
-    uint32_t tot = 0;   // this digit's count in the tile; warp prefixes in place
-    for (int w = 0; w < kWarps; w++) {
-        const uint32_t c = wcnt[w][threadIdx.x];
-        wcnt[w][threadIdx.x] = tot;
-        tot += c;
-    }
-    uint32_t all;
-    toff[threadIdx.x] = block_exclusive_scan(tot, all);   // tile digit offsets
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < kRsItems; k++) {
-        const unsigned d = dig[k];
-        if (d < 256u) {
-            const uint32_t p = toff[d] + wcnt[warp][d] + rank[k];
-            skey[p] = key[k];
-            sval[p] = val[k];
-        }
-    }
-    __syncthreads();
-    const int m = (int)min((int64_t)kRsTile, n - tbase);
-    for (int p = threadIdx.x; p < m; p += kRsThreads) {
-        const uint32_t k = skey[p];
-        const unsigned d = (k >> shift) & 255u;
-        const uint32_t pos = gbase[d] + ((uint32_t)p - toff[d]);
-        kout[pos] = k;
-        vout[pos] = sval[p];
-    }
-}
-
 size_t radix_hist_bytes(int64_t n)
 {
     int64_t tiles = rs_blocks(n);
@@ -336,12 +260,8 @@ static int radix_sort_impl(K* k0, K* k1, uint32_t* v0, uint32_t* v1, int64_t n, 
         note_launch(), k_radix_hist<K><<<(unsigned)tiles, kRsThreads, 0, s>>>(kin, n, shift, table, tiles);
         int rc = exclusive_scan_u32(table, table, 256 * tiles, scan_tmp, s);
         if (rc) return rc;
-        if (sizeof(K) == 4 && SPH_RADIX_TILE_REORDER)
-            note_launch(), k_radix_scatter_tile<<<(unsigned)tiles, kRsThreads, 0, s>>>(
-                (const uint32_t*)kin, vin, ident, (uint32_t*)kout, vout, n, shift, table, tiles);
-        else
-            note_launch(), k_radix_scatter<K><<<(unsigned)tiles, kRsThreads, 0, s>>>(
-                kin, vin, ident, kout, vout, n, shift, table, tiles);
+        note_launch(), k_radix_scatter<K><<<(unsigned)tiles, kRsThreads, 0, s>>>(
+            kin, vin, ident, kout, vout, n, shift, table, tiles);
         if ((rc = check_launch("radix_scatter"))) return rc;
         ident = false;
         K* tk = kin; kin = kout; kout = tk;

@@ -450,7 +450,6 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=
             for k in ("cellmax", "blockmax"):
                 T[k] = torch.zeros((max(ncells, 1),), dtype=i32, device=dev)
     T["elist"] = torch.empty((tiles, NEIGHBOR_CAPACITY, 32), dtype=i32, device=dev)
-    T["amask"] = torch.empty((tiles, NEIGHBOR_CAPACITY // 32, 32), dtype=i32, device=dev)
     for k in ("lcount", "acount", "nww"):
         T[k] = torch.empty((tiles * 32,), dtype=i32, device=dev)
     T["qcount"] = torch.zeros((4,), dtype=i32, device=dev)
@@ -467,7 +466,7 @@ def engine_alloc(dev, n_cap, nf_cap, nw_cap, d, f64, grid, scalars, g, id_range=
     E.rq = T["rq"].data_ptr()
     for k in ("dvdt", "drho", "id", "nnb", "refpos", "rho_scratch_id",
               "oflow_id", "wall_id", "vol_id", "offs_f", "offs_w", "lists",
-              "lcount", "acount", "nww", "elist", "amask", "cell0", "disp", "disp0", "queue",
+              "lcount", "acount", "nww", "elist", "cell0", "disp", "disp0", "queue",
               "qcount", "ws", "stats"):
         setattr(E, k, T[k].data_ptr())
     E.owned_id = None      # every particle owned (multi-rank runs set it)
