@@ -77,3 +77,32 @@ def test_bench_config3_3d4m_bitwise_vs_oracle():
 
 def test_bench_config4_3d16m_bitwise_vs_oracle():
     _run("3d16m")
+
+
+def test_bench_window_config3_bitwise_vs_oracle():
+    """The bench's whole measured window at config 3 -- initialize, W = 5
+    warm-up and K = 20 timed steps (nsub 7-8) -- step for step against the
+    oracle: dt, nsub, interaction and clamp counts every step, every field
+    at the end (~2.5 min of oracle time on 16 threads)."""
+    import torch
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    cfg = BENCH_CASES["3d4m"][0]()
+    reg_h, grid_h = cases.build_case(cfg)
+    osim = O.OracleSim.from_registry(reg_h, grid_h)
+    del reg_h
+    reg, grid, state = cases.build_case_device(cfg, torch.device("cuda", 0))
+    sim = Simulation(reg, grid, P.ExecutionPolicy.cuda(0))
+    sim.load_device_state(state)
+    del state
+    osim.initialize()
+    sim.initialize()
+    nsubs = []
+    for step in range(25):
+        assert sim.advance() == osim.advance(), step
+        assert sim.last_nsub == osim.last_nsub, step
+        assert sim.interaction_count == osim.interaction_count, step
+        assert sim.out_of_bounds == osim.out_of_bounds, step
+        nsubs.append(sim.last_nsub)
+    assert nsubs[5:] == [7] * 9 + [8] * 11   # the bench line's nsub_per_step
+    bad = [f for f in FIELDS if reg.view(f).tobytes() != osim.f[f].tobytes()]
+    assert not bad, bad
