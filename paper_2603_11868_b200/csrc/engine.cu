@@ -72,6 +72,9 @@
 #ifndef SPH_SKIN_FMA
 #define SPH_SKIN_FMA 1          // skin test r2 with FMAs (not rounded like the reference)
 #endif
+#ifndef SPH_SKIN_STAGE
+#define SPH_SKIN_STAGE 1        // k_skin_tile: survivors staged in shared memory, int4 stores
+#endif
 #ifndef SPH_SKIN_WALL_SKIP
 #define SPH_SKIN_WALL_SKIP 1    // skip wall-only blocks once the wall-wall counts are known
 #endif
@@ -476,6 +479,10 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
     __shared__ vec4<T> spos[kC];       // positions in sorted order
     __shared__ uint32_t run_start[2 * 9], run_pre[2 * 9 + 1];
     __shared__ int s_kept;
+    // per warp: the two particles' survivors, flushed as int4 quads (f32
+    // only: the f64 tile would drop the 3D build below 8 CTAs per SM)
+    constexpr bool kStage = SPH_SKIN_STAGE && sizeof(T) == 4;
+    __shared__ __align__(16) int32_t stage[kStage ? NW : 1][2][kStage ? kCap : 4];
     const unsigned tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
     const unsigned lt = lanemask_lt();
     const int64_t nf = E.nf;
@@ -651,11 +658,17 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                     const unsigned bB = __ballot_sync(0xffffffffu, stB);
                     if (stA) {
                         const int p = cntA + __popc(bA & lt);
-                        if (p < kCap) lpA[ell_off(p)] = (int32_t)j;
+                        if (p < kCap) {
+                            if (kStage) stage[kStage ? warp : 0][0][p] = (int32_t)j;
+                            else lpA[ell_off(p)] = (int32_t)j;
+                        }
                     }
                     if (stB) {
                         const int p = cntB + __popc(bB & lt);
-                        if (p < kCap) lpB[ell_off(p)] = (int32_t)j;
+                        if (p < kCap) {
+                            if (kStage) stage[kStage ? warp : 0][1][p] = (int32_t)j;
+                            else lpB[ell_off(p)] = (int32_t)j;
+                        }
                     }
                     cntA += __popc(bA);
                     cntB += __popc(bB);
@@ -677,6 +690,18 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
 #else
             scan(std::false_type{});
 #endif
+            if (kStage) {   // the staged lists out as whole quads (tile-ELL)
+                __syncwarp();
+                const int qa = (min(cntA, kCap) + 3) >> 2;
+                const int qb = hasB ? (min(cntB, kCap) + 3) >> 2 : 0;
+                const int4* sa = reinterpret_cast<const int4*>(stage[kStage ? warp : 0][0]);
+                const int4* sb = reinterpret_cast<const int4*>(stage[kStage ? warp : 0][1]);
+                for (int q = (int)lane; q < qa + qb; q += 32) {
+                    if (q < qa) reinterpret_cast<int4*>(lpA)[q * 32] = sa[q];
+                    else reinterpret_cast<int4*>(lpB)[(q - qa) * 32] = sb[q - qa];
+                }
+                __syncwarp();
+            }
             if (lane < 2 && (lane == 0 || hasB)) {
                 const int64_t i = lane ? iB : iA;
                 const int64_t slot = lane ? slB : slA;
