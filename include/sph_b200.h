@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 12
+#define SPH_ABI_VERSION 13
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -303,6 +303,18 @@ int sph_engine_push(SphEngine* e, const void* x, const void* v, const void* rho,
                     const void* m, const void* vol, const void* drho, const void* dvdt,
                     const void* rho_scratch, const uint32_t* id, const uint32_t* wall,
                     const uint32_t* nnb, const uint32_t* oflow, cudaStream_t s);
+/* the same push in two halves, so that the registry's upload can overlap
+ * the first step's list build: push_begin needs only x, id and wall (id
+ * checks, cell order, positions, refpos; counts the fluid clamps of this
+ * cell order into stats->oob, which the following step's CLL would count);
+ * push_end gathers every other field by refpos.  push_begin + push_end on
+ * one stream == sph_engine_push. */
+int sph_engine_push_begin(SphEngine* e, const void* x, const uint32_t* id, const uint32_t* wall,
+                          cudaStream_t s);
+int sph_engine_push_end(SphEngine* e, const void* v, const void* rho, const void* p,
+                        const void* m, const void* vol, const void* drho, const void* dvdt,
+                        const void* rho_scratch, const uint32_t* nnb, const uint32_t* oflow,
+                        cudaStream_t s);
 int sph_engine_pull(const SphEngine* e, void* x, void* v, void* rho, void* p, void* m, void* vol,
                     void* drho, void* dvdt, void* rho_scratch, uint32_t* id, uint32_t* wall,
                     uint32_t* nnb, uint32_t* oflow, cudaStream_t s);

@@ -127,7 +127,7 @@ class SphSlabGeom(C.Structure):
     ]
 
 
-ABI_VERSION = 12   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 13   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)
@@ -154,6 +154,8 @@ _PROTOS = {
     "sph_selftest_pair_fac": (c_i32, [c_f64, c_f64, C.c_uint32, C.c_uint32, _P, _P, _P]),
     "sph_selftest_round_f32": (c_i32, [c_i64, C.c_uint64, _P, _P, _P]),
     "sph_engine_push": (c_i32, [_P] * 14 + [_P]),
+    "sph_engine_push_begin": (c_i32, [_P] * 4 + [_P]),
+    "sph_engine_push_end": (c_i32, [_P] * 11 + [_P]),
     "sph_engine_pull": (c_i32, [_P] * 14 + [_P]),
     "sph_engine_rebuild_cll": (c_i32, [_P, _P]),
     "sph_engine_ref_sort": (c_i32, [_P, _P]),

@@ -53,7 +53,7 @@ __global__ void k_id_check(const uint32_t* __restrict__ cnt, int64_t n, SphStepS
 template <class T, int D>
 __global__ void k_push_keys(const T* __restrict__ x, const uint32_t* __restrict__ wall, int64_t n,
                             GridP<T> g, int key_bits, uint32_t* __restrict__ keys,
-                            uint32_t* __restrict__ oob_walls)
+                            uint32_t* __restrict__ oob_walls, uint32_t* __restrict__ oob_fluid)
 {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int cl = 0;
@@ -68,39 +68,60 @@ __global__ void k_push_keys(const T* __restrict__ x, const uint32_t* __restrict_
     }
     unsigned b = __ballot_sync(0xffffffffu, cl && is_wall);
     if (lane_id() == 0 && b) atomicAdd(oob_walls, (uint32_t)__popc(b));
+    // fluid clamps: what this step's CLL build counts (k_fluid_keys) when the
+    // push's cell order stands in for it
+    b = __ballot_sync(0xffffffffu, cl && r < n && !is_wall);
+    if (lane_id() == 0 && b) atomicAdd(oob_fluid, (uint32_t)__popc(b));
 }
 
+// push, first half: the particle's place (cell order), position, identity;
+// refpos[i] = its registry row, which the second half gathers by (the mass
+// in pos.w comes with the second half: the list build does not read it)
 template <class T, int D>
-__global__ void k_push_gather(Eng<T> E, const uint32_t* __restrict__ perm, const T* __restrict__ x,
-                              const T* __restrict__ v, const T* __restrict__ rho,
-                              const T* __restrict__ p, const T* __restrict__ m,
-                              const T* __restrict__ vol, const T* __restrict__ drho,
-                              const T* __restrict__ dvdt, const T* __restrict__ rho_scratch,
-                              const uint32_t* __restrict__ id, const uint32_t* __restrict__ wall,
-                              const uint32_t* __restrict__ nnb, const uint32_t* __restrict__ oflow)
+__global__ void k_push_place(Eng<T> E, const uint32_t* __restrict__ perm, const T* __restrict__ x,
+                             const uint32_t* __restrict__ id, const uint32_t* __restrict__ wall)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= E.n) return;
     uint32_t r = perm[i];
-    vec4<T> P4, V4, A4;
-    P4.x = x[r * D]; P4.y = x[r * D + 1]; P4.z = D == 3 ? x[r * D + 2] : T(0); P4.w = m[r];
+    vec4<T> P4;
+    P4.x = x[r * D]; P4.y = x[r * D + 1]; P4.z = D == 3 ? x[r * D + 2] : T(0); P4.w = T(0);
+    E.pos[i] = P4; E.pos_next[i] = P4;   // walls stay valid in both buffers
+    uint32_t pid = id[r];
+    E.id[i] = pid;
+    E.refpos[i] = r;
+    if (pid >= (uint64_t)E.idr) return;   // reported by k_id_count (push_error)
+    E.wall_id[pid] = wall[r];
+}
+
+// push, second half: every other field from registry row refpos[i]
+template <class T, int D>
+__global__ void k_push_fields(Eng<T> E, const T* __restrict__ v, const T* __restrict__ rho,
+                              const T* __restrict__ p, const T* __restrict__ m,
+                              const T* __restrict__ vol,
+                              const T* __restrict__ drho, const T* __restrict__ dvdt,
+                              const T* __restrict__ rho_scratch, const uint32_t* __restrict__ nnb,
+                              const uint32_t* __restrict__ oflow)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= E.n) return;
+    uint32_t r = E.refpos[i];
+    vec4<T> V4, A4;
     V4.x = v[r * D]; V4.y = v[r * D + 1]; V4.z = D == 3 ? v[r * D + 2] : T(0); V4.w = T(0);
     A4.x = dvdt[r * D]; A4.y = dvdt[r * D + 1]; A4.z = D == 3 ? dvdt[r * D + 2] : T(0);
     A4.w = T(0);
     vec2<T> RP; RP.x = rho[r]; RP.y = p[r];
-    E.pos[i] = P4; E.pos_next[i] = P4;   // walls stay valid in both buffers
+    reinterpret_cast<T*>(&E.pos[i])[3] = m[r];
+    reinterpret_cast<T*>(&E.pos_next[i])[3] = m[r];
     E.vel[0][i] = V4; E.vel[1][i] = V4;
     E.rp[0][i] = RP; E.rp[1][i] = RP;
     E.dvdt[i] = A4;
     E.drho[i] = drho[r];
-    uint32_t pid = id[r];
-    E.id[i] = pid;
     E.nnb[i] = nnb[r];
-    E.refpos[i] = r;
-    if (pid >= (uint64_t)E.idr) return;   // reported by k_id_count (push_error)
+    uint32_t pid = E.id[i];
+    if (pid >= (uint64_t)E.idr) return;
     E.rho_scratch_id[pid] = rho_scratch[r];
     E.oflow_id[pid] = oflow[r];
-    E.wall_id[pid] = wall[r];
     E.vol_id[pid] = vol[r];
 }
 
@@ -468,10 +489,8 @@ static int validate_ws(const SphEngine* e)
 }
 
 template <class T, int D>
-static int push_impl(SphEngine* e, const void* x, const void* v, const void* rho, const void* p,
-                     const void* m, const void* vol, const void* drho, const void* dvdt,
-                     const void* rho_scratch, const uint32_t* id, const uint32_t* wall,
-                     const uint32_t* nnb, const uint32_t* oflow, cudaStream_t s)
+static int push_begin_impl(SphEngine* e, const void* x, const uint32_t* id,
+                           const uint32_t* wall, cudaStream_t s)
 {
     Bump bump(e->ws, e->ws_bytes);
     SortBufs sb = sort_bufs(e, bump);
@@ -492,17 +511,15 @@ static int push_impl(SphEngine* e, const void* x, const void* v, const void* rho
             note_launch(), k_id_check<<<grid_for(n, 256), 256, 0, s>>>(cnt, n, e->stats);
         }
         note_launch(), k_push_keys<T, D><<<grid_for(n, 256), 256, 0, s>>>(
-            (const T*)x, wall, n, g, e->key_bits, sb.k0, &e->stats->oob_walls);
+            (const T*)x, wall, n, g, e->key_bits, sb.k0, &e->stats->oob_walls, &e->stats->oob);
         int which = 0;
         int rc = radix_sort_u32(sb.k0, sb.k1, sb.v0, sb.v1, n, e->key_bits + 1, true, sb.hist,
                                 &which, s);
         if (rc) return rc;
         const uint32_t* sk = which ? sb.k1 : sb.k0;
         const uint32_t* perm = which ? sb.v1 : sb.v0;
-        note_launch(), k_push_gather<T, D><<<grid_for(n, 256), 256, 0, s>>>(
-            E, perm, (const T*)x, (const T*)v, (const T*)rho, (const T*)p, (const T*)m,
-            (const T*)vol, (const T*)drho, (const T*)dvdt, (const T*)rho_scratch, id, wall, nnb,
-            oflow);
+        note_launch(), k_push_place<T, D><<<grid_for(n, 256), 256, 0, s>>>(
+            E, perm, (const T*)x, id, wall);
         // fluid offsets over sk[0, nf), wall offsets over sk[nf, n) (flag bit set)
         seg_offsets(sk, e->nf, e->ncells, 0u, e->offs_f, s);
         seg_offsets(sk + e->nf, n - e->nf, e->ncells, 1u << e->key_bits, e->offs_w, s);
@@ -520,7 +537,39 @@ static int push_impl(SphEngine* e, const void* x, const void* v, const void* rho
     e->lists_ready = 0;
     e->lists_stale = 0;
     e->nww_ready = 0;
-    return check_launch("engine_push");
+    return check_launch("engine_push_begin");
+}
+
+template <class T, int D>
+static int push_end_impl(SphEngine* e, const void* v, const void* rho, const void* p,
+                         const void* m, const void* vol, const void* drho, const void* dvdt,
+                         const void* rho_scratch, const uint32_t* nnb, const uint32_t* oflow,
+                         cudaStream_t s)
+{
+    if (e->n > 0)
+        note_launch(), k_push_fields<T, D><<<grid_for(e->n, 256), 256, 0, s>>>(
+            eng_of<T>(e), (const T*)v, (const T*)rho, (const T*)p, (const T*)m, (const T*)vol,
+            (const T*)drho, (const T*)dvdt, (const T*)rho_scratch, nnb, oflow);
+    return check_launch("engine_push_end");
+}
+
+extern "C" int sph_engine_push_begin(SphEngine* e, const void* x, const uint32_t* id,
+                                     const uint32_t* wall, cudaStream_t s)
+{
+    int rc = validate_ws(e);
+    if (rc) return rc;
+    return SPH_DISPATCH(e, push_begin_impl, e, x, id, wall, s);
+}
+
+extern "C" int sph_engine_push_end(SphEngine* e, const void* v, const void* rho, const void* p,
+                                   const void* m, const void* vol, const void* drho, const void* dvdt,
+                                   const void* rho_scratch, const uint32_t* nnb,
+                                   const uint32_t* oflow, cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc) return rc;
+    return SPH_DISPATCH(e, push_end_impl, e, v, rho, p, m, vol, drho, dvdt, rho_scratch, nnb,
+                        oflow, s);
 }
 
 extern "C" int sph_engine_push(SphEngine* e, const void* x, const void* v, const void* rho,
@@ -529,10 +578,9 @@ extern "C" int sph_engine_push(SphEngine* e, const void* x, const void* v, const
                                const uint32_t* wall, const uint32_t* nnb, const uint32_t* oflow,
                                cudaStream_t s)
 {
-    int rc = validate_ws(e);
+    int rc = sph_engine_push_begin(e, x, id, wall, s);
     if (rc) return rc;
-    return SPH_DISPATCH(e, push_impl, e, x, v, rho, p, m, vol, drho, dvdt, rho_scratch, id, wall,
-                        nnb, oflow, s);
+    return sph_engine_push_end(e, v, rho, p, m, vol, drho, dvdt, rho_scratch, nnb, oflow, s);
 }
 
 template <class T, int D>

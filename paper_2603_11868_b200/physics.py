@@ -395,6 +395,13 @@ _ENGINE_FIELDS = ("x", "v", "rho", "p", "m", "Vol", "drho", "dvdt",
                   "rho_scratch", "id", "wall", "nnb", "oflow")
 # fields the engine never writes (oflow: only on overflow, which is tracked)
 _HOST_SAME_FIELDS = ("m", "Vol", "id", "wall", "oflow", "rho_scratch")
+# the two halves of an overlapped push (sph_engine_push_begin / _end): the
+# fields that place the particles, then the rest
+_PUSH_FIRST = ("x", "id", "wall")
+_PUSH_REST = ("v", "rho", "p", "m", "Vol", "drho", "dvdt", "rho_scratch", "nnb", "oflow")
+# a step that starts from a host push uploads the second half behind its own
+# skin-list build (SPH_PUSH_OVERLAP=0: the plain push)
+PUSH_OVERLAP = os.environ.get("SPH_PUSH_OVERLAP", "1") != "0"
 
 
 def _key_to_double(k):
@@ -589,6 +596,9 @@ class Simulation:
         self._epoch = None          # (skin, steps) of the lists' epoch
         self._epoch_backoff = 0     # steps left without epochs after a futile one
         self.last_list_mode = None  # "build" | "maintain" (diagnostic)
+        self._last_step = None      # (vmax, amax, dt) of the last step: skin forecast
+        self.push_overlap = PUSH_OVERLAP
+        self.last_push_overlapped = False
         registry.attach_engine(self)
 
     def _lib(self):
@@ -660,7 +670,8 @@ class Simulation:
         self._dev = {"device": T["pos0"].device, "E": E, "T": T, "tdtype": T["pos0"].dtype,
                      "tstream": tstream, "stream": C_void(tstream.cuda_stream),
                      "stats_host": torch.empty(T["stats"].shape, dtype=torch.uint8,
-                                               pin_memory=True)}
+                                               pin_memory=True),
+                     "cstream": None}   # upload stream of overlapped pushes (lazy)
 
     def _push(self, devs=None, nf=None):
         """Registry -> device SoA (physics layout, cell order)."""
@@ -697,6 +708,76 @@ class Simulation:
         # Shepard), so those stay equal until the registry order changes
         self._host_same = set(_HOST_SAME_FIELDS) if host_push else set()
         del devs, st
+        self._host_dirty = False
+        self._host_stale = False
+        self._norms = None
+
+    def _overlap_ready(self):
+        """A host push can be split around the step's list build: the
+        device is allocated for this registry, the previous step's norms and
+        dt forecast the skin (the skin affects speed only: csrc/engine.cu
+        rebuilds any list a particle outruns), and lists are rebuilt every
+        step (no epochs)."""
+        d = self._dev
+        if not (self.push_overlap and self._host_dirty and d is not None and self._last_step
+                and self.list_epochs == "off"):
+            return False
+        reg = self.registry
+        return d["E"].n == reg.particle_count and d["E"].nf > 0
+
+    def _push_overlapped(self):
+        """Host push in two halves around this step's list build: x, id and
+        wall are uploaded and placed (sph_engine_push_begin: cell order, the
+        CLL of this step) while the other ten fields are still in
+        flight on a copy stream; the skin lists are built from the placed
+        positions with the forecast skin; sph_engine_push_end gathers the
+        rest once it has landed.  Nothing synchronises here: the step's
+        first stats read checks the push (push_error / fluid_seen)."""
+        torch = torch_mod()
+        d = self._dev
+        reg = self.registry
+        ts = d["tstream"]
+        if d["cstream"] is None:   # copy stream + device landing buffers, kept
+            d["cstream"] = torch.cuda.Stream(device=d["device"])
+            d["landing"] = {}
+            d["push_events"] = (torch.cuda.Event(), torch.cuda.Event())
+        cs = d["cstream"]
+        land = d["landing"]
+        ev_first, ev_rest = d["push_events"]
+
+        def upload(f):
+            a = np.ascontiguousarray(reg.raw_view(f))
+            if a.dtype == np.uint32:
+                a = a.view(np.int32)
+            src = torch.from_numpy(a)
+            dst = land.get(f)
+            if dst is None or dst.shape != src.shape or dst.dtype != src.dtype:
+                dst = land[f] = torch.empty(src.shape, dtype=src.dtype, device=d["device"])
+            dst.copy_(src, non_blocking=True)
+            return dst
+
+        cs.wait_stream(ts)   # the last push's landing buffers are consumed
+        with torch.cuda.stream(cs):
+            first = [upload(f) for f in _PUSH_FIRST]
+            ev_first.record(cs)
+            rest = [upload(f) for f in _PUSH_REST]
+            ev_rest.record(cs)
+        self.last_push_bytes = sum(reg.raw_view(f).nbytes for f in _ENGINE_FIELDS)
+        ts.wait_event(ev_first)
+        rc = self._lib().sph_engine_push_begin(ctypes.byref(d["E"]),
+                                               *[ptr(t) for t in first], d["stream"])
+        _native.check(rc, "engine_push_begin")
+        vmax, amax, dt = self._last_step
+        t0 = time.perf_counter()
+        with self._kernel_event("skin_build"):
+            self._build_lists(self._choose_skin(vmax, amax, dt))
+        self.last_list_mode = "build"
+        self.phase_seconds["cll"] += time.perf_counter() - t0
+        ts.wait_event(ev_rest)
+        rc = self._lib().sph_engine_push_end(ctypes.byref(d["E"]),
+                                             *[ptr(t) for t in rest], d["stream"])
+        _native.check(rc, "engine_push_end")
+        self._host_same = set(_HOST_SAME_FIELDS)
         self._host_dirty = False
         self._host_stale = False
         self._norms = None
@@ -874,7 +955,14 @@ class Simulation:
 
     def advance(self, end_time=None):
         """One advective step (physics.py:489-552); returns the dt taken."""
-        self._ensure_device()
+        overlapped = self._overlap_ready()
+        if overlapped:
+            # the push's cell order is this step's CLL (the rebuild would
+            # re-sort an already sorted layout: identity) and its clamp count
+            self._push_overlapped()
+        else:
+            self._ensure_device()
+        self.last_push_overlapped = overlapped
         d = self._dev
         L = self._lib()
         if self.sort_every and self.step_count > 0 \
@@ -883,15 +971,27 @@ class Simulation:
             self._call("sph_engine_ref_sort")
             self._host_same = set()      # the registry order changed
             self.phase_seconds["sorting"] += time.perf_counter() - t0
-        flags = _native.STATS_RESET | (0 if self._norms else _native.STATS_NORMS)
-        self._call("sph_engine_stats", ctypes.c_int32(flags))
-        self._rebuild_cll()
+        if overlapped:   # counters were zeroed by the push
+            self._call("sph_engine_stats", ctypes.c_int32(_native.STATS_NORMS))
+        else:
+            flags = _native.STATS_RESET | (0 if self._norms else _native.STATS_NORMS)
+            self._call("sph_engine_stats", ctypes.c_int32(flags))
+            self._rebuild_cll()
         # compute_timestep (physics.py:502-511) reads only v and dvdt, which the
         # Shepard filter does not touch, so the step's dt is known before the
         # lists are built and sizes their skin
         t0 = time.perf_counter()
         if self._norms is None:
             s = self._read_stats()
+            if overlapped:
+                if s.push_error:
+                    self._host_dirty = True
+                    raise ValueError("registry ids must be a permutation of 0..N-1")
+                if s.fluid_seen != d["E"].nf:   # the wall flags changed: plain push
+                    self._host_dirty = True
+                    self._last_step = None
+                    return self.advance(end_time)
+                self._oob_walls = s.oob_walls
             self._norms = (_bits_to_double(s.vmax_bits), _bits_to_double(s.amax_bits))
         vmax, amax = self._norms
         if self.fixed_dt is not None:
@@ -905,10 +1005,12 @@ class Simulation:
         dt = dt_adv
         if end_time is not None:
             dt = min(dt, end_time - self.time)
-        t0 = time.perf_counter()
-        with self._kernel_event("skin_build"):
-            self._lists_for_step(vmax, amax, dt)
-        self.phase_seconds["cll"] += time.perf_counter() - t0
+        if not overlapped:
+            t0 = time.perf_counter()
+            with self._kernel_event("skin_build"):
+                self._lists_for_step(vmax, amax, dt)
+            self.phase_seconds["cll"] += time.perf_counter() - t0
+        self._last_step = (vmax, amax, dt)
         if self.shepard_every and self.step_count > 0 \
                 and self.step_count % self.shepard_every == 0:
             t0 = time.perf_counter()

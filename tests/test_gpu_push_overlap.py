@@ -1,0 +1,100 @@
+"""The overlapped host push (physics.Simulation._push_overlapped).
+
+A step that starts from host-authoritative state (the registry was viewed,
+and so may have been edited, since the last step) uploads x, id and wall
+first, lays the particles out and builds the step's skin lists while the
+other ten fields are still in flight, and skips the step's CLL re-sort (the
+push's cell order is that CLL).  These tests hold it to the plain push
+(sph_engine_push + rebuild + lists sized by this step's dt) bit for bit,
+every field every step, plus dt, nsub and the interaction and clamp counts,
+and to the CPU oracle on a clamped cloud.
+"""
+
+import numpy as np
+import pytest
+
+from _util import FIELDS
+
+import paper_2603_11868_b200 as P
+from paper_2603_11868_b200 import cases
+from paper_2603_11868_b200.physics import Simulation
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+CUDA = P.ExecutionPolicy.cuda()
+
+
+def _clamped_cloud():
+    from paper_2603_11868_b200.neighborhood import UniformGrid
+    from paper_2603_11868_b200.physics import setup_state_variables
+    from paper_2603_11868_b200.variables import VariableRegistry
+    rng = np.random.default_rng(5)
+    n = 3000
+    reg = VariableRegistry(n, 2, dtype=np.float32)
+    setup_state_variables(reg)
+    reg.raw_view("x")[:] = rng.random((n, 2)) * 1.0
+    reg.raw_view("v")[:] = rng.normal(0, 0.3, (n, 2))
+    reg.raw_view("rho")[:] = 1000.0
+    reg.raw_view("m")[:] = 1000.0 * 0.02 ** 2
+    for k, val in (("rho0", 1000.0), ("c0", 20.0), ("h", 0.026), ("dp", 0.02),
+                   ("alpha_visc", 0.02)):
+        reg.register_singular(k, val)
+    reg.register_singular("g", np.array([0.0, -9.81]))
+    grid = UniformGrid.from_bounds((0.1, 0.1), (0.9, 0.9), 0.052)
+    return reg, grid
+
+
+CASES = {
+    "2d_sort_shepard": (lambda: cases.build_case(
+        cases.CaseConfig(case="dambreak2d", dp=0.05, precision="f32")),
+        dict(sort_every=3, shepard_every=4), 14),
+    "3d": (lambda: cases.build_case(cases.kleefsman_config(dp=0.03, precision="f32")), {}, 4),
+    "3d_f64": (lambda: cases.build_case(cases.kleefsman_config(dp=0.04, precision="f64")), {}, 3),
+    "clamped_cloud": (_clamped_cloud, {}, 6),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_overlapped_push_matches_plain_push(name):
+    make, kw, steps = CASES[name]
+    reg_a, grid = make()
+    reg_b, _ = make()
+    a = Simulation(reg_a, grid, CUDA, **kw)
+    b = Simulation(reg_b, grid, CUDA, **kw)
+    b.push_overlap = False
+    a.initialize()
+    b.initialize()
+    for step in range(steps):
+        assert a.advance() == b.advance(), step
+        assert a.last_push_overlapped == (step > 0), step   # step 0: no dt forecast yet
+        assert not b.last_push_overlapped
+        assert a.last_nsub == b.last_nsub, step
+        assert a.interaction_count == b.interaction_count, step
+        assert a.out_of_bounds == b.out_of_bounds, step
+        # views pull: host-authoritative again, so the next step pushes
+        bad = [f for f in FIELDS if reg_a.view(f).tobytes() != reg_b.view(f).tobytes()]
+        assert not bad, (step, bad)
+    if name == "clamped_cloud":
+        assert a.out_of_bounds > 0
+
+
+def test_overlapped_push_with_host_edits_vs_oracle():
+    """Edits between steps (velocities, a position out of the grid) reach
+    the overlapped push; the clamp count follows the oracle's."""
+    reg, grid = _clamped_cloud()
+    sim = Simulation(reg, grid, CUDA)
+    osim = O.OracleSim.from_registry(reg, grid)
+    sim.initialize()
+    osim.initialize()
+    for step in range(5):
+        if step >= 2:   # the same in-place edits on both sides
+            for v, x in ((reg.view("v"), reg.view("x")), (osim.f["v"], osim.f["x"])):
+                v[step::97] *= np.float32(0.5)
+                x[step * 7] = np.float32(-0.25)
+        assert sim.advance() == osim.advance(), step
+        assert sim.last_push_overlapped == (step > 0), step
+        assert sim.last_nsub == osim.last_nsub, step
+        assert sim.interaction_count == osim.interaction_count, step
+        assert sim.out_of_bounds == osim.out_of_bounds, step
+        bad = [f for f in FIELDS if reg.view(f).tobytes() != osim.f[f].tobytes()]
+        assert not bad, (step, bad)
