@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 13
+#define SPH_ABI_VERSION 14
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -318,6 +318,13 @@ int sph_engine_push_end(SphEngine* e, const void* v, const void* rho, const void
 int sph_engine_pull(const SphEngine* e, void* x, void* v, void* rho, void* p, void* m, void* vol,
                     void* drho, void* dvdt, void* rho_scratch, uint32_t* id, uint32_t* wall,
                     uint32_t* nnb, uint32_t* oflow, cudaStream_t s);
+/* the fields of mask only (bit k = the k-th array argument of
+ * sph_engine_pull: x, v, rho, p, m, vol, drho, dvdt, rho_scratch, id, wall,
+ * nnb, oflow); the others may be NULL */
+int sph_engine_pull_fields(const SphEngine* e, uint32_t mask, void* x, void* v, void* rho,
+                           void* p, void* m, void* vol, void* drho, void* dvdt,
+                           void* rho_scratch, uint32_t* id, uint32_t* wall, uint32_t* nnb,
+                           uint32_t* oflow, cudaStream_t s);
 /* physics.py:446-449 _rebuild_cll on the engine layout: re-sort the fluid
  * segment by cell, rebuild the segment offsets; counts clamps into stats. */
 int sph_engine_rebuild_cll(SphEngine* e, cudaStream_t s);
@@ -354,6 +361,12 @@ int sph_engine_substeps(SphEngine* e, double half_dt, double full_dt, int32_t ns
                         cudaStream_t s);
 /* the same, synchronised, with the CUDA-event time of each of the five
  * parts summed over the sub-steps (ms_out[5]; see sph_engine_substep_timed) */
+/* sph_engine_substeps, recording x_final on s once the last sub-step's
+ * positions are final and rp_final once its rho, p and drho are (after its
+ * wall-pressure sweep): a registry pull of those fields can start there,
+ * overlapping the step's momentum sweep */
+int sph_engine_substeps_marked(SphEngine* e, double half_dt, double full_dt, int32_t nsub,
+                               cudaEvent_t x_final, cudaEvent_t rp_final, cudaStream_t s);
 int sph_engine_substeps_timed(SphEngine* e, double half_dt, double full_dt, int32_t nsub,
                               float* ms_out, cudaStream_t s);
 /* the same sub-step, synchronised, with CUDA-event times (ms) of its five

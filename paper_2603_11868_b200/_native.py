@@ -127,7 +127,7 @@ class SphSlabGeom(C.Structure):
     ]
 
 
-ABI_VERSION = 13   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 14   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)
@@ -157,6 +157,7 @@ _PROTOS = {
     "sph_engine_push_begin": (c_i32, [_P] * 4 + [_P]),
     "sph_engine_push_end": (c_i32, [_P] * 11 + [_P]),
     "sph_engine_pull": (c_i32, [_P] * 14 + [_P]),
+    "sph_engine_pull_fields": (c_i32, [_P, C.c_uint32] + [_P] * 13 + [_P]),
     "sph_engine_rebuild_cll": (c_i32, [_P, _P]),
     "sph_engine_ref_sort": (c_i32, [_P, _P]),
     "sph_engine_initialize": (c_i32, [_P, _P]),
@@ -167,6 +168,7 @@ _PROTOS = {
     "sph_engine_stats": (c_i32, [_P, c_i32, _P]),
     "sph_engine_substeps": (c_i32, [_P, c_f64, c_f64, c_i32, _P]),
     "sph_engine_substeps_timed": (c_i32, [_P, c_f64, c_f64, c_i32, _P, _P]),
+    "sph_engine_substeps_marked": (c_i32, [_P, c_f64, c_f64, c_i32, _P, _P, _P]),
     "sph_engine_phase": (c_i32, [_P, c_i32, c_f64, c_f64, _P]),
     "sph_engine_probe": (c_i32, [_P, _P, c_f64, _P, c_i32, _P, _P]),
     "sph_engine_snapshot": (c_i32, [_P, _P, _P]),

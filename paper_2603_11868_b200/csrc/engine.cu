@@ -2368,17 +2368,19 @@ static void sub_momentum(SphEngine* e, T half, T next_full, bool fuse, bool zero
 // + fix-ups | continuity+DU | wall pressure | momentum+kick (bench.py timing)
 template <class T, int D>
 static void substep_parts(SphEngine* e, T half, T full, bool fuse, cudaEvent_t* ev,
-                          cudaStream_t s)
+                          cudaStream_t s, cudaEvent_t* marks = nullptr)
 {
     if (ev) cudaEventRecord(ev[0], s);
     if (!e->drifted) sub_kick_drift<T, D>(e, half, full, s);
     e->drifted = 0;
+    if (marks) cudaEventRecord(marks[0], s);   // positions final
     if (ev) cudaEventRecord(ev[1], s);
     sub_lists<T, D>(e, s);
     if (ev) cudaEventRecord(ev[2], s);
     sub_continuity<T, D>(e, full, s);
     if (ev) cudaEventRecord(ev[3], s);
     sub_wall<T, D>(e, s);
+    if (marks) cudaEventRecord(marks[1], s);   // rho, p (fluid and walls), drho final
     if (ev) cudaEventRecord(ev[4], s);
     sub_momentum<T, D>(e, half, full, fuse, !fuse, s);
     if (ev) cudaEventRecord(ev[5], s);
@@ -2421,7 +2423,7 @@ extern "C" int sph_engine_substep_timed(SphEngine* e, double half_dt, double ful
 // until the last sub-step), so the timed step runs as the untimed one does
 template <class T, int D>
 static int substeps_impl(SphEngine* e, double half_d, double full_d, int nsub, float* ms,
-                         cudaStream_t s)
+                         cudaStream_t s, cudaEvent_t* marks = nullptr)
 {
     const T half = T(half_d), full = T(full_d);
     cudaEvent_t* ev = nullptr;
@@ -2431,7 +2433,12 @@ static int substeps_impl(SphEngine* e, double half_d, double full_d, int nsub, f
         for (int k = 0; k < 5; k++) ms[k] = 0.0f;
     }
     for (int k = 0; k < nsub; k++)
-        substep_parts<T, D>(e, half, full, k + 1 < nsub, ms ? ev + 6 * k : nullptr, s);
+        substep_parts<T, D>(e, half, full, k + 1 < nsub, ms ? ev + 6 * k : nullptr, s,
+                            k + 1 == nsub ? marks : nullptr);
+    if (marks && nsub == 0) {
+        cudaEventRecord(marks[0], s);
+        cudaEventRecord(marks[1], s);
+    }
     if (ms) {
         if (nsub > 0) cudaEventSynchronize(ev[6 * nsub - 1]);
         for (int k = 0; k < nsub; k++)
@@ -2453,6 +2460,18 @@ extern "C" int sph_engine_substeps(SphEngine* e, double half_dt, double full_dt,
     if (rc || (rc = require_lists(e))) return rc;
     if (nsub < 0 || e->drifted) return SPH_ERR_INVALID;
     return SPH_DISPATCH(e, substeps_impl, e, half_dt, full_dt, (int)nsub, (float*)nullptr, s);
+}
+
+extern "C" int sph_engine_substeps_marked(SphEngine* e, double half_dt, double full_dt,
+                                          int32_t nsub, cudaEvent_t x_final,
+                                          cudaEvent_t rp_final, cudaStream_t s)
+{
+    int rc = engine_begin(e, s);
+    if (rc || (rc = require_lists(e))) return rc;
+    if (nsub < 0 || e->drifted || !x_final || !rp_final) return SPH_ERR_INVALID;
+    cudaEvent_t marks[2] = {x_final, rp_final};
+    return SPH_DISPATCH(e, substeps_impl, e, half_dt, full_dt, (int)nsub, (float*)nullptr, s,
+                        marks);
 }
 
 extern "C" int sph_engine_substeps_timed(SphEngine* e, double half_dt, double full_dt,

@@ -125,33 +125,48 @@ __global__ void k_push_fields(Eng<T> E, const T* __restrict__ v, const T* __rest
     E.vol_id[pid] = vol[r];
 }
 
+// registry-order copies of the fields in mask (bit k: field k of x, v, rho,
+// p, m, Vol, drho, dvdt, rho_scratch, id, wall, nnb, oflow)
 template <class T, int D>
-__global__ void k_pull(Eng<T> E, int cur_v, int cur_rp, T* __restrict__ x, T* __restrict__ v,
-                       T* __restrict__ rho, T* __restrict__ p, T* __restrict__ m,
-                       T* __restrict__ vol, T* __restrict__ drho, T* __restrict__ dvdt,
-                       T* __restrict__ rho_scratch, uint32_t* __restrict__ id,
-                       uint32_t* __restrict__ wall, uint32_t* __restrict__ nnb,
-                       uint32_t* __restrict__ oflow)
+__global__ void k_pull(Eng<T> E, int cur_v, int cur_rp, uint32_t mask, T* __restrict__ x,
+                       T* __restrict__ v, T* __restrict__ rho, T* __restrict__ p,
+                       T* __restrict__ m, T* __restrict__ vol, T* __restrict__ drho,
+                       T* __restrict__ dvdt, T* __restrict__ rho_scratch,
+                       uint32_t* __restrict__ id, uint32_t* __restrict__ wall,
+                       uint32_t* __restrict__ nnb, uint32_t* __restrict__ oflow)
 {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= E.n) return;
-    uint32_t r = E.refpos[i];
-    uint32_t pid = E.id[i];
-    vec4<T> P4 = E.pos[i], V4 = E.vel[cur_v][i], A4 = E.dvdt[i];
-    vec2<T> RP = E.rp[cur_rp][i];
-    x[r * D] = P4.x; x[r * D + 1] = P4.y;
-    v[r * D] = V4.x; v[r * D + 1] = V4.y;
-    dvdt[r * D] = A4.x; dvdt[r * D + 1] = A4.y;
-    if (D == 3) { x[r * D + 2] = P4.z; v[r * D + 2] = V4.z; dvdt[r * D + 2] = A4.z; }
-    m[r] = P4.w;
-    rho[r] = RP.x; p[r] = RP.y;
-    drho[r] = E.drho[i];
-    id[r] = pid;
-    nnb[r] = E.nnb[i];
-    rho_scratch[r] = E.rho_scratch_id[pid];
-    oflow[r] = E.oflow_id[pid];
-    wall[r] = E.wall_id[pid];
-    vol[r] = E.vol_id[pid];
+    const uint32_t r = E.refpos[i];
+    const uint32_t pid = E.id[i];
+    if (mask & (1u << 0)) {
+        const vec4<T> P4 = E.pos[i];
+        x[r * D] = P4.x; x[r * D + 1] = P4.y;
+        if (D == 3) x[r * D + 2] = P4.z;
+    }
+    if (mask & (1u << 1)) {
+        const vec4<T> V4 = E.vel[cur_v][i];
+        v[r * D] = V4.x; v[r * D + 1] = V4.y;
+        if (D == 3) v[r * D + 2] = V4.z;
+    }
+    if (mask & (3u << 2)) {
+        const vec2<T> RP = E.rp[cur_rp][i];
+        if (mask & (1u << 2)) rho[r] = RP.x;
+        if (mask & (1u << 3)) p[r] = RP.y;
+    }
+    if (mask & (1u << 4)) m[r] = E.pos[i].w;
+    if (mask & (1u << 5)) vol[r] = E.vol_id[pid];
+    if (mask & (1u << 6)) drho[r] = E.drho[i];
+    if (mask & (1u << 7)) {
+        const vec4<T> A4 = E.dvdt[i];
+        dvdt[r * D] = A4.x; dvdt[r * D + 1] = A4.y;
+        if (D == 3) dvdt[r * D + 2] = A4.z;
+    }
+    if (mask & (1u << 8)) rho_scratch[r] = E.rho_scratch_id[pid];
+    if (mask & (1u << 9)) id[r] = pid;
+    if (mask & (1u << 10)) wall[r] = E.wall_id[pid];
+    if (mask & (1u << 11)) nnb[r] = E.nnb[i];
+    if (mask & (1u << 12)) oflow[r] = E.oflow_id[pid];
 }
 
 static void seg_offsets(const uint32_t* keys, int64_t n, int64_t ncells, uint32_t or_mask,
@@ -584,15 +599,15 @@ extern "C" int sph_engine_push(SphEngine* e, const void* x, const void* v, const
 }
 
 template <class T, int D>
-static int pull_impl(const SphEngine* e, void* x, void* v, void* rho, void* p, void* m, void* vol,
-                     void* drho, void* dvdt, void* rho_scratch, uint32_t* id, uint32_t* wall,
-                     uint32_t* nnb, uint32_t* oflow, cudaStream_t s)
+static int pull_impl(const SphEngine* e, uint32_t mask, void* x, void* v, void* rho, void* p,
+                     void* m, void* vol, void* drho, void* dvdt, void* rho_scratch, uint32_t* id,
+                     uint32_t* wall, uint32_t* nnb, uint32_t* oflow, cudaStream_t s)
 {
-    if (e->n <= 0) return SPH_OK;
+    if (e->n <= 0 || !mask) return SPH_OK;
     Eng<T> E = eng_of<T>(e);
     note_launch(), k_pull<T, D><<<grid_for(e->n, 256), 256, 0, s>>>(
-        E, e->cur_v, e->cur_rp, (T*)x, (T*)v, (T*)rho, (T*)p, (T*)m, (T*)vol, (T*)drho, (T*)dvdt,
-        (T*)rho_scratch, id, wall, nnb, oflow);
+        E, e->cur_v, e->cur_rp, mask, (T*)x, (T*)v, (T*)rho, (T*)p, (T*)m, (T*)vol, (T*)drho,
+        (T*)dvdt, (T*)rho_scratch, id, wall, nnb, oflow);
     return check_launch("engine_pull");
 }
 
@@ -601,10 +616,24 @@ extern "C" int sph_engine_pull(const SphEngine* e, void* x, void* v, void* rho, 
                                uint32_t* id, uint32_t* wall, uint32_t* nnb, uint32_t* oflow,
                                cudaStream_t s)
 {
+    return sph_engine_pull_fields(e, 0x1fffu, x, v, rho, p, m, vol, drho, dvdt, rho_scratch, id,
+                                  wall, nnb, oflow, s);
+}
+
+extern "C" int sph_engine_pull_fields(const SphEngine* e, uint32_t mask, void* x, void* v,
+                                      void* rho, void* p, void* m, void* vol, void* drho,
+                                      void* dvdt, void* rho_scratch, uint32_t* id,
+                                      uint32_t* wall, uint32_t* nnb, uint32_t* oflow,
+                                      cudaStream_t s)
+{
     int rc = engine_validate(e);
     if (rc) return rc;
-    return SPH_DISPATCH(e, pull_impl, e, x, v, rho, p, m, vol, drho, dvdt, rho_scratch, id, wall,
-                        nnb, oflow, s);
+    void* ptrs[13] = {x, v, rho, p, m, vol, drho, dvdt, rho_scratch, id, wall, nnb, oflow};
+    for (int k = 0; k < 13; k++)
+        if (((mask >> k) & 1u) && !ptrs[k]) return SPH_ERR_INVALID;
+    if (mask >> 13) return SPH_ERR_INVALID;
+    return SPH_DISPATCH(e, pull_impl, e, mask, x, v, rho, p, m, vol, drho, dvdt, rho_scratch, id,
+                        wall, nnb, oflow, s);
 }
 
 template <class T, int D>

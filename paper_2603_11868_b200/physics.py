@@ -402,6 +402,13 @@ _PUSH_REST = ("v", "rho", "p", "m", "Vol", "drho", "dvdt", "rho_scratch", "nnb",
 # a step that starts from a host push uploads the second half behind its own
 # skin-list build (SPH_PUSH_OVERLAP=0: the plain push)
 PUSH_OVERLAP = os.environ.get("SPH_PUSH_OVERLAP", "1") != "0"
+# ... and a step whose result was viewed after each of the last two steps
+# pulls it within the step, overlapping the D2H copies with the last
+# sub-step's sweeps (SPH_EAGER_PULL=0: pulls on view only)
+EAGER_PULL = os.environ.get("SPH_EAGER_PULL", "1") != "0"
+# registry fields by the engine event after which the step's values are final
+_PULL_AT_X = ("x",)
+_PULL_AT_RP = ("rho", "p", "drho")
 
 
 def _key_to_double(k):
@@ -599,6 +606,10 @@ class Simulation:
         self._last_step = None      # (vmax, amax, dt) of the last step: skin forecast
         self.push_overlap = PUSH_OVERLAP
         self.last_push_overlapped = False
+        self.eager_pull = EAGER_PULL
+        self.last_pull_overlapped = False
+        self._viewed = False        # a registry view since the last step
+        self._view_streak = 0       # consecutive steps followed by a view
         registry.attach_engine(self)
 
     def _lib(self):
@@ -613,7 +624,16 @@ class Simulation:
 
     def pull_to_host(self):
         """Write the device state into the registry (reference order)."""
-        if self._dev is None or not self._host_stale:
+        self._viewed = True
+        if self._dev is None:
+            return
+        if not self._host_stale:
+            if not self._host_dirty:
+                # the step already pulled its result (_pull_overlapped): the
+                # host copy is current, and from now on the caller may edit it
+                self._host_dirty = True
+                self._host_same = set()
+                self._norms = None
             return
         self._host_stale = False
         d = self._dev
@@ -737,22 +757,12 @@ class Simulation:
         d = self._dev
         reg = self.registry
         ts = d["tstream"]
-        if d["cstream"] is None:   # copy stream + device landing buffers, kept
-            d["cstream"] = torch.cuda.Stream(device=d["device"])
-            d["landing"] = {}
-            d["push_events"] = (torch.cuda.Event(), torch.cuda.Event())
-        cs = d["cstream"]
-        land = d["landing"]
+        cs = self._copy_stream()
         ev_first, ev_rest = d["push_events"]
 
         def upload(f):
-            a = np.ascontiguousarray(reg.raw_view(f))
-            if a.dtype == np.uint32:
-                a = a.view(np.int32)
-            src = torch.from_numpy(a)
-            dst = land.get(f)
-            if dst is None or dst.shape != src.shape or dst.dtype != src.dtype:
-                dst = land[f] = torch.empty(src.shape, dtype=src.dtype, device=d["device"])
+            src = self._host_tensor(f)
+            dst = self._landing(f, src)
             dst.copy_(src, non_blocking=True)
             return dst
 
@@ -781,6 +791,73 @@ class Simulation:
         self._host_dirty = False
         self._host_stale = False
         self._norms = None
+
+    def _copy_stream(self):
+        """The engine's host-transfer stream, its events and its device
+        landing buffers (registry layout, reused by every overlapped push
+        and pull; created on first use)."""
+        torch = torch_mod()
+        d = self._dev
+        if d["cstream"] is None:
+            d["cstream"] = torch.cuda.Stream(device=d["device"])
+            d["landing"] = {}
+            d["push_events"] = (torch.cuda.Event(), torch.cuda.Event())
+            ev = [torch.cuda.Event() for _ in range(3)]
+            for e in ev:   # materialise the events: their handles go to the library
+                e.record(d["tstream"])
+            d["pull_events"] = ev
+        return d["cstream"]
+
+    def _host_tensor(self, f):
+        a = np.ascontiguousarray(self.registry.raw_view(f))
+        if a.dtype == np.uint32:
+            a = a.view(np.int32)
+        return torch_mod().from_numpy(a)
+
+    def _landing(self, f, like):
+        d = self._dev
+        dst = d["landing"].get(f)
+        if dst is None or dst.shape != like.shape or dst.dtype != like.dtype:
+            dst = d["landing"][f] = torch_mod().empty(like.shape, dtype=like.dtype,
+                                                      device=d["device"])
+        return dst
+
+    def _eager_pull_ready(self):
+        """Pull this step's result within the step: the result of each of
+        the last two steps was viewed, and the registry is in pinned host
+        memory (a pageable copy would block the host mid-step)."""
+        if not (self.eager_pull and self._viewed and self._view_streak >= 1
+                and self.kernel_times is None and self.registry.particle_count):
+            return False
+        return all(self._host_tensor(f).is_pinned() for f in _ENGINE_FIELDS)
+
+    def _pull_overlapped(self, marks, ev_end):
+        """Queue the step's registry pull on the copy stream: x once the last
+        sub-step's positions are final, rho / p / drho after its wall
+        sweep (both during the momentum sweep), the rest after the step;
+        fields the host provably still holds (_host_same) are skipped."""
+        torch = torch_mod()
+        d = self._dev
+        cs = self._copy_stream()
+        late = tuple(f for f in _ENGINE_FIELDS
+                     if f not in _PULL_AT_X + _PULL_AT_RP and f not in self._host_same)
+        lib = self._lib()
+        nbytes = 0
+        with torch.cuda.stream(cs):
+            for ev, fields in ((marks[0], _PULL_AT_X), (marks[1], _PULL_AT_RP),
+                               (ev_end, late)):
+                cs.wait_event(ev)
+                hosts = {f: self._host_tensor(f) for f in fields}
+                lands = {f: self._landing(f, hosts[f]) for f in fields}
+                mask = sum(1 << _ENGINE_FIELDS.index(f) for f in fields)
+                args = [ptr(lands[f]) if f in lands else None for f in _ENGINE_FIELDS]
+                rc = lib.sph_engine_pull_fields(ctypes.byref(d["E"]), mask, *args,
+                                                C_void(cs.cuda_stream))
+                _native.check(rc, "engine_pull_fields")
+                for f in fields:
+                    hosts[f].copy_(lands[f], non_blocking=True)
+                    nbytes += hosts[f].numel() * hosts[f].element_size()
+        self.last_pull_bytes = nbytes
 
     def load_device_state(self, state):
         """Start from registry-order device tensors (``cases.build_case_device``;
@@ -1024,7 +1101,18 @@ class Simulation:
         full = float(dtype(dts))
         t0 = time.perf_counter()
         E = ctypes.byref(d["E"])
-        if self.kernel_times is None:
+        eager = self._eager_pull_ready()
+        viewed = self._viewed
+        if eager:
+            self._copy_stream()
+            marks = d["pull_events"]
+            rc = L.sph_engine_substeps_marked(E, half, full, nsub,
+                                              C_void(marks[0].cuda_event),
+                                              C_void(marks[1].cuda_event), d["stream"])
+            _native.check(rc, "engine_substeps_marked")
+            marks[2].record(d["tstream"])
+            self._pull_overlapped(marks, marks[2])
+        elif self.kernel_times is None:
             rc = L.sph_engine_substeps(E, half, full, nsub, d["stream"])
             _native.check(rc, "engine_substeps")
         else:   # per-kernel CUDA-event timing (bench.py roofline pass)
@@ -1038,7 +1126,14 @@ class Simulation:
         self.phase_seconds["interactions"] += time.perf_counter() - t0
         if self.kernel_times is not None:
             self._collect_events()
-        self._host_stale = True
+        self._view_streak = self._view_streak + 1 if viewed else 0
+        self._viewed = False
+        self.last_pull_overlapped = eager
+        if eager:   # the host holds the step's result; the device stays authoritative
+            d["cstream"].synchronize()
+            self._host_stale = bool(stats.overflow)   # oflow changed: pull on view
+        else:
+            self._host_stale = True
         self.last_nsub = nsub
         self.last_nfix = int(stats.nfix)
         # list refreshes were rare: the next step checks and refreshes in one

@@ -1,4 +1,5 @@
-"""The overlapped host push (physics.Simulation._push_overlapped).
+"""The overlapped host push and pull (physics.Simulation._push_overlapped,
+_pull_overlapped).
 
 A step that starts from host-authoritative state (the registry was viewed,
 and so may have been edited, since the last step) uploads x, id and wall
@@ -7,7 +8,10 @@ other ten fields are still in flight, and skips the step's CLL re-sort (the
 push's cell order is that CLL).  These tests hold it to the plain push
 (sph_engine_push + rebuild + lists sized by this step's dt) bit for bit,
 every field every step, plus dt, nsub and the interaction and clamp counts,
-and to the CPU oracle on a clamped cloud.
+and to the CPU oracle on a clamped cloud.  With the registry in pinned
+memory and its result viewed after every step, the step also pulls its own
+result (x and rho / p / drho during the last momentum sweep), which the
+same comparisons cover.
 """
 
 import numpy as np
@@ -44,6 +48,20 @@ def _clamped_cloud():
     return reg, grid
 
 
+def _pin(reg):
+    """Registry storage -> pinned host memory (as bench.py's e2e arm)."""
+    import torch
+    for name in reg.discrete_names():
+        var = reg._discrete[name]
+        a = var.data
+        t = torch.empty(a.shape, dtype=torch.int32 if a.dtype == np.uint32
+                        else torch.from_numpy(a[:0]).dtype, pin_memory=True)
+        pinned = t.numpy().view(a.dtype)
+        pinned[...] = a
+        var.data = pinned
+    return reg
+
+
 CASES = {
     "2d_sort_shepard": (lambda: cases.build_case(
         cases.CaseConfig(case="dambreak2d", dp=0.05, precision="f32")),
@@ -54,20 +72,26 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("pinned", [False, True])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_overlapped_push_matches_plain_push(name):
+def test_overlapped_push_matches_plain_push(name, pinned):
     make, kw, steps = CASES[name]
     reg_a, grid = make()
     reg_b, _ = make()
+    if pinned:
+        _pin(reg_a)
     a = Simulation(reg_a, grid, CUDA, **kw)
     b = Simulation(reg_b, grid, CUDA, **kw)
     b.push_overlap = False
+    b.eager_pull = False
     a.initialize()
     b.initialize()
     for step in range(steps):
         assert a.advance() == b.advance(), step
         assert a.last_push_overlapped == (step > 0), step   # step 0: no dt forecast yet
-        assert not b.last_push_overlapped
+        # the result of each of the two previous steps was viewed
+        assert a.last_pull_overlapped == (pinned and step >= 2), step
+        assert not b.last_push_overlapped and not b.last_pull_overlapped
         assert a.last_nsub == b.last_nsub, step
         assert a.interaction_count == b.interaction_count, step
         assert a.out_of_bounds == b.out_of_bounds, step
@@ -76,12 +100,24 @@ def test_overlapped_push_matches_plain_push(name):
         assert not bad, (step, bad)
     if name == "clamped_cloud":
         assert a.out_of_bounds > 0
+    # then no views: after the first step (which still pushes the viewed
+    # registry), the device stays authoritative -- nothing is pushed or pulled
+    for step in range(3):
+        assert a.advance() == b.advance()
+        if step:
+            assert not a.last_push_overlapped and not a.last_pull_overlapped
+    bad = [f for f in FIELDS if reg_a.view(f).tobytes() != reg_b.view(f).tobytes()]
+    assert not bad, bad
 
 
-def test_overlapped_push_with_host_edits_vs_oracle():
+@pytest.mark.parametrize("pinned", [False, True])
+def test_overlapped_push_with_host_edits_vs_oracle(pinned):
     """Edits between steps (velocities, a position out of the grid) reach
-    the overlapped push; the clamp count follows the oracle's."""
+    the overlapped push, also after a step that pulled its own result; the
+    clamp count follows the oracle's."""
     reg, grid = _clamped_cloud()
+    if pinned:
+        _pin(reg)
     sim = Simulation(reg, grid, CUDA)
     osim = O.OracleSim.from_registry(reg, grid)
     sim.initialize()
@@ -93,6 +129,7 @@ def test_overlapped_push_with_host_edits_vs_oracle():
                 x[step * 7] = np.float32(-0.25)
         assert sim.advance() == osim.advance(), step
         assert sim.last_push_overlapped == (step > 0), step
+        assert sim.last_pull_overlapped == (pinned and step >= 2), step
         assert sim.last_nsub == osim.last_nsub, step
         assert sim.interaction_count == osim.interaction_count, step
         assert sim.out_of_bounds == osim.out_of_bounds, step
