@@ -88,9 +88,12 @@ __global__ void k_push_place(Eng<T> E, const uint32_t* __restrict__ perm, const 
     P4.x = x[r * D]; P4.y = x[r * D + 1]; P4.z = D == 3 ? x[r * D + 2] : T(0); P4.w = T(0);
     E.pos[i] = P4; E.pos_next[i] = P4;   // walls stay valid in both buffers
     uint32_t pid = id[r];
+    // an out-of-range id (reported by k_id_count as push_error, raised by
+    // the host before the state is used) is stored as 0, so that the list
+    // build an overlapped push queues before that check indexes in bounds
+    if (pid >= (uint64_t)E.idr) pid = 0;
     E.id[i] = pid;
     E.refpos[i] = r;
-    if (pid >= (uint64_t)E.idr) return;   // reported by k_id_count (push_error)
     E.wall_id[pid] = wall[r];
 }
 
@@ -118,8 +121,7 @@ __global__ void k_push_fields(Eng<T> E, const T* __restrict__ v, const T* __rest
     E.dvdt[i] = A4;
     E.drho[i] = drho[r];
     E.nnb[i] = nnb[r];
-    uint32_t pid = E.id[i];
-    if (pid >= (uint64_t)E.idr) return;
+    const uint32_t pid = E.id[i];   // in range (k_push_place)
     E.rho_scratch_id[pid] = rho_scratch[r];
     E.oflow_id[pid] = oflow[r];
     E.vol_id[pid] = vol[r];

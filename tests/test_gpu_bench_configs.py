@@ -106,3 +106,34 @@ def test_bench_window_config3_bitwise_vs_oracle():
     assert nsubs[5:] == [7] * 9 + [8] * 11   # the bench line's nsub_per_step
     bad = [f for f in FIELDS if reg.view(f).tobytes() != osim.f[f].tobytes()]
     assert not bad, bad
+
+
+def test_bench_config2_e2e_path_bitwise_vs_oracle():
+    """bench.py's e2e arm at config 2: host-built registry in pinned memory,
+    every field viewed after every step -- so steps from the second on push
+    with the overlapped upload and from the third on pull their own result
+    during the last momentum sweep -- step for step against the oracle."""
+    import torch
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    cfg = BENCH_CASES["2d1m"][0]()
+    reg, grid = cases.build_case(cfg)
+    osim = O.OracleSim.from_registry(reg, grid)
+    for name in reg.discrete_names():   # pinned registry storage (bench.pinned_like)
+        var = reg._discrete[name]
+        a = var.data
+        t = torch.empty(a.shape, dtype=torch.int32 if a.dtype == np.uint32
+                        else torch.from_numpy(a[:0]).dtype, pin_memory=True)
+        t.numpy().view(a.dtype)[...] = a
+        var.data = t.numpy().view(a.dtype)
+    sim = Simulation(reg, grid, P.ExecutionPolicy.cuda(0))
+    osim.initialize()
+    sim.initialize()
+    for step in range(5):
+        assert sim.advance() == osim.advance(), step
+        assert sim.last_push_overlapped == (step > 0), step
+        assert sim.last_pull_overlapped == (step > 1), step
+        assert sim.last_nsub == osim.last_nsub, step
+        assert sim.interaction_count == osim.interaction_count, step
+        assert sim.out_of_bounds == osim.out_of_bounds, step
+        bad = [f for f in FIELDS if reg.view(f).tobytes() != osim.f[f].tobytes()]
+        assert not bad, (step, bad)

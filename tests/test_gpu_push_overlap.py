@@ -135,3 +135,30 @@ def test_overlapped_push_with_host_edits_vs_oracle(pinned):
         assert sim.out_of_bounds == osim.out_of_bounds, step
         bad = [f for f in FIELDS if reg.view(f).tobytes() != osim.f[f].tobytes()]
         assert not bad, (step, bad)
+
+
+@pytest.mark.parametrize("bad_id", ["duplicate", "out_of_range"])
+def test_overlapped_push_rejects_bad_ids_and_recovers(bad_id):
+    """The id check of an overlapped push is read after the step's list
+    build was queued: a duplicate or out-of-range id still raises
+    ValueError (no device fault), and once the ids are repaired the run goes
+    on bit for bit with the oracle."""
+    reg, grid = cases.build_case(cases.CaseConfig(case="dambreak2d", dp=0.05,
+                                                  precision="f32"))
+    sim = Simulation(reg, grid, CUDA)
+    sim.initialize()
+    sim.advance()
+    ids = reg.view("id")
+    saved = ids.copy()
+    ids[3] = ids[4] if bad_id == "duplicate" else np.uint32(10 ** 9)
+    with pytest.raises(ValueError):
+        sim.advance()
+    reg.view("id")[:] = saved
+    osim = O.OracleSim.from_registry(reg, grid)
+    osim.st.step_count = sim.step_count
+    osim.st.time = sim.time
+    for step in range(3):
+        assert sim.advance() == osim.advance(), step
+        assert sim.last_push_overlapped   # every step follows a view
+        for f in FIELDS:
+            assert reg.view(f).tobytes() == osim.f[f].tobytes(), (step, f)
