@@ -491,7 +491,7 @@ def gpu_arm(args, rank, world, local_rank):
         nbytes = sum(reg.raw_view(f).nbytes for f in _ENGINE_FIELDS)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        nsubs_e, h2d, d2h, n_ovl = [], 0, 0, 0
+        nsubs_e, h2d, d2h, n_ovl, n_pull = [], 0, 0, 0, 0
         trace = os.environ.get("SPH_BENCH_TRACE") == "1"
         for _ in range(args.steps):
             ta = time.perf_counter()
@@ -503,6 +503,7 @@ def gpu_arm(args, rank, world, local_rank):
             d2h += sim.last_pull_bytes
             nsubs_e.append(sim.last_nsub)
             n_ovl += int(sim.last_push_overlapped)
+            n_pull += int(sim.last_pull_overlapped)
             if trace:
                 print(f"e2e step: advance {1e3 * (tb - ta):.2f} ms, views "
                       f"{1e3 * (time.perf_counter() - tb):.2f} ms, overlapped push "
@@ -516,13 +517,16 @@ def gpu_arm(args, rank, world, local_rank):
                "registry_bytes": nbytes,
                "steps": args.steps, "nsub_per_step": nsubs_e,
                "overlapped_push_steps": int(n_ovl),
+               "overlapped_pull_steps": int(n_pull),
                "timer": "host wall clock around push (H2D, pinned, every registry field; "
                         "10 of the 13 fields upload behind the step's skin-list build) + "
-                        "advance + pull (D2H of every field the step changed; m, Vol, id, "
-                        "wall, oflow, rho_scratch are not copied back while the device "
-                        "provably holds the pushed values) + registry.view of every field, "
-                        "same steps as `value` (restored checkpoint, after one untimed "
-                        "round trip)"}
+                        "advance + pull (D2H of every field the step changed, into the "
+                        "registry's host arrays; x and rho/p/drho during the last "
+                        "momentum sweep once the step's results are viewed every step; "
+                        "m, Vol, id, wall, oflow, rho_scratch are not copied back while "
+                        "the device provably holds the pushed values) + registry.view of "
+                        "every field, same steps as `value` (restored checkpoint, after "
+                        "one untimed round trip)"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
