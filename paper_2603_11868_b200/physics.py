@@ -1177,12 +1177,14 @@ class Simulation:
         reg = self.registry
         n, d = reg.particle_count, reg.dim
         if self._dev is None or not self._host_stale:
-            ids = reg.view("id").astype(np.int64)
+            # the host arrays are current (read without a view: a view would
+            # hand them to the caller and make the next step push)
+            ids = reg.raw_view("id").astype(np.int64)
             out = np.empty((n, 2 * d + 2), reg.dtype)
-            out[ids, :d] = reg.view("x")
-            out[ids, d:2 * d] = reg.view("v")
-            out[ids, 2 * d] = reg.view("rho")
-            out[ids, 2 * d + 1] = reg.view("p")
+            out[ids, :d] = reg.raw_view("x")
+            out[ids, d:2 * d] = reg.raw_view("v")
+            out[ids, 2 * d] = reg.raw_view("rho")
+            out[ids, 2 * d + 1] = reg.raw_view("p")
             return out
         torch = torch_mod()
         dv = self._dev
