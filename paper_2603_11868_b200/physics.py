@@ -824,12 +824,14 @@ class Simulation:
 
     def _eager_pull_ready(self):
         """Pull this step's result within the step: the result of each of
-        the last two steps was viewed, and the registry is in pinned host
-        memory (a pageable copy would block the host mid-step)."""
+        the last two steps was viewed, and the registry is in contiguous
+        pinned host memory (a pageable copy would block the host mid-step)."""
         if not (self.eager_pull and self._viewed and self._view_streak >= 1
                 and self.kernel_times is None and self.registry.particle_count):
             return False
-        return all(self._host_tensor(f).is_pinned() for f in _ENGINE_FIELDS)
+        reg = self.registry
+        return all(reg.raw_view(f).flags.c_contiguous and self._host_tensor(f).is_pinned()
+                   for f in _ENGINE_FIELDS)
 
     def _pull_overlapped(self, marks, ev_end):
         """Queue the step's registry pull on the copy stream: x once the last
