@@ -1,4 +1,4 @@
-"""Bitwise parity at the benchmark configurations (BASELINE.json configs 2-4).
+"""Bitwise parity at the benchmark configurations (BASELINE.json configs 2-5).
 
 bench.py times the engine on the 2D 1M, 3D 4M and 3D 16M dam breaks, built
 on the device (cases.build_case_device).  These tests run exactly that path
@@ -77,6 +77,27 @@ def test_bench_config3_3d4m_bitwise_vs_oracle():
 
 def test_bench_config4_3d16m_bitwise_vs_oracle():
     _run("3d16m")
+
+
+def test_bench_config5_taylor_green_8m_bitwise_vs_oracle():
+    """bench.py --config tg8m: the 200^3 periodic Taylor-Green box on one GPU
+    (libsphb200_periodic.so, host placement as the bench) against the
+    oracle's periodic restatement for two steps (nsub 3)."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
+    cfg = cases.taylor_green_config(3, 200, precision="f32")
+    reg, grid = cases.build_case(cfg)
+    osim = O.OracleSim.from_registry(reg, grid)
+    sim = Simulation(reg, grid, P.ExecutionPolicy.cuda(0))
+    osim.initialize()
+    sim.initialize()
+    assert sim.interaction_count == osim.interaction_count
+    for step in range(2):
+        assert sim.advance() == osim.advance(), step
+        assert sim.last_nsub == osim.last_nsub, step
+        assert sim.interaction_count == osim.interaction_count, step
+        assert sim.out_of_bounds == osim.out_of_bounds, step
+    bad = [f for f in FIELDS if reg.view(f).tobytes() != osim.f[f].tobytes()]
+    assert not bad, bad
 
 
 def test_bench_window_config3_bitwise_vs_oracle():
