@@ -305,10 +305,11 @@ int sph_engine_push(SphEngine* e, const void* x, const void* v, const void* rho,
                     const uint32_t* nnb, const uint32_t* oflow, cudaStream_t s);
 /* the same push in two halves, so that the registry's upload can overlap
  * the first step's list build: push_begin needs only x, id and wall (id
- * checks, cell order, positions, refpos; counts the fluid clamps of this
- * cell order into stats->oob, which the following step's CLL would count);
- * push_end gathers every other field by refpos.  push_begin + push_end on
- * one stream == sph_engine_push. */
+ * range check, fluid count, cell order, positions, refpos; counts the fluid
+ * clamps of this cell order into stats->oob, which the following step's CLL
+ * would count); push_end gathers every other field by refpos and checks the
+ * ids for duplicates.  push_begin + push_end on one stream ==
+ * sph_engine_push; stats->push_error / fluid_seen are final after push_end. */
 int sph_engine_push_begin(SphEngine* e, const void* x, const uint32_t* id, const uint32_t* wall,
                           cudaStream_t s);
 int sph_engine_push_end(SphEngine* e, const void* v, const void* rho, const void* p,

@@ -14,34 +14,15 @@
 namespace sph {
 
 // push-time registry checks (the former host-side O(n) scans): ids must be
-// a permutation of 0..n-1 (counted by id), and the fluid count is reported
-__global__ void k_id_count(const uint32_t* __restrict__ id, const uint32_t* __restrict__ wall,
-                           int64_t n, uint32_t* __restrict__ cnt, SphStepStats* st)
+// a permutation of 0..n-1.  k_push_place flags an out-of-range id; the
+// duplicate count runs in the second half of the push (k_id_count over the
+// placed ids, off the path to the list build), so the first half needs no
+// scratch that the list build reuses.
+__global__ void k_id_count(const uint32_t* __restrict__ id, int64_t n,
+                           uint32_t* __restrict__ cnt)
 {
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool fluid = false;
-    if (r < n) {
-        const uint32_t pid = id[r];
-        if (pid < (uint64_t)n) atomicAdd(&cnt[pid], 1u);
-        else st->push_error = 1;
-        fluid = wall[r] == 0;
-    }
-    const unsigned b = __ballot_sync(0xffffffffu, fluid);
-    if (lane_id() == 0 && b) atomicAdd(&st->fluid_seen, (unsigned)__popc(b));
-}
-
-// id_range mode: ids only range-checked (distinct by the caller's contract)
-__global__ void k_id_range(const uint32_t* __restrict__ id, const uint32_t* __restrict__ wall,
-                           int64_t n, int64_t id_range, SphStepStats* st)
-{
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool fluid = false;
-    if (r < n) {
-        if (id[r] >= (uint64_t)id_range) st->push_error = 1;
-        fluid = wall[r] == 0;
-    }
-    const unsigned b = __ballot_sync(0xffffffffu, fluid);
-    if (lane_id() == 0 && b) atomicAdd(&st->fluid_seen, (unsigned)__popc(b));
+    if (r < n) atomicAdd(&cnt[id[r]], 1u);   // placed ids are in range
 }
 
 __global__ void k_id_check(const uint32_t* __restrict__ cnt, int64_t n, SphStepStats* st)
@@ -50,10 +31,12 @@ __global__ void k_id_check(const uint32_t* __restrict__ cnt, int64_t n, SphStepS
     if (r < n && cnt[r] != 1u) st->push_error = 1;
 }
 
+// cell keys of the push (the wall flag above the cell bits), the clamp
+// counts, and the fluid count the host checks against the allocation
 template <class T, int D>
 __global__ void k_push_keys(const T* __restrict__ x, const uint32_t* __restrict__ wall, int64_t n,
                             GridP<T> g, int key_bits, uint32_t* __restrict__ keys,
-                            uint32_t* __restrict__ oob_walls, uint32_t* __restrict__ oob_fluid)
+                            SphStepStats* __restrict__ st)
 {
     int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int cl = 0;
@@ -67,11 +50,13 @@ __global__ void k_push_keys(const T* __restrict__ x, const uint32_t* __restrict_
         keys[r] = lin | (is_wall ? (1u << key_bits) : 0u);
     }
     unsigned b = __ballot_sync(0xffffffffu, cl && is_wall);
-    if (lane_id() == 0 && b) atomicAdd(oob_walls, (uint32_t)__popc(b));
+    if (lane_id() == 0 && b) atomicAdd(&st->oob_walls, (uint32_t)__popc(b));
     // fluid clamps: what this step's CLL build counts (k_fluid_keys) when the
     // push's cell order stands in for it
     b = __ballot_sync(0xffffffffu, cl && r < n && !is_wall);
-    if (lane_id() == 0 && b) atomicAdd(oob_fluid, (uint32_t)__popc(b));
+    if (lane_id() == 0 && b) atomicAdd(&st->oob, (uint32_t)__popc(b));
+    b = __ballot_sync(0xffffffffu, r < n && !is_wall);
+    if (lane_id() == 0 && b) atomicAdd(&st->fluid_seen, (uint32_t)__popc(b));
 }
 
 // push, first half: the particle's place (cell order), position, identity;
@@ -88,10 +73,13 @@ __global__ void k_push_place(Eng<T> E, const uint32_t* __restrict__ perm, const 
     P4.x = x[r * D]; P4.y = x[r * D + 1]; P4.z = D == 3 ? x[r * D + 2] : T(0); P4.w = T(0);
     E.pos[i] = P4; E.pos_next[i] = P4;   // walls stay valid in both buffers
     uint32_t pid = id[r];
-    // an out-of-range id (reported by k_id_count as push_error, raised by
-    // the host before the state is used) is stored as 0, so that the list
-    // build an overlapped push queues before that check indexes in bounds
-    if (pid >= (uint64_t)E.idr) pid = 0;
+    // an out-of-range id is reported (push_error, raised by the host before
+    // the state is used) and stored as 0, so that the list build an
+    // overlapped push queues before that check indexes in bounds
+    if (pid >= (uint64_t)E.idr) {
+        E.stats->push_error = 1;
+        pid = 0;
+    }
     E.id[i] = pid;
     E.refpos[i] = r;
     E.wall_id[pid] = wall[r];
@@ -517,18 +505,8 @@ static int push_begin_impl(SphEngine* e, const void* x, const uint32_t* id,
     const int64_t n = e->n;
     cudaMemsetAsync(e->stats, 0, sizeof(SphStepStats), s);
     if (n > 0) {
-        if (e->id_range > 0) {
-            note_launch(), k_id_range<<<grid_for(n, 256), 256, 0, s>>>(id, wall, n, e->id_range,
-                                                                       e->stats);
-        } else {
-            uint32_t* cnt = bump.take<uint32_t>(n);
-            if (!cnt) return SPH_ERR_WORKSPACE;
-            cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)n, s);
-            note_launch(), k_id_count<<<grid_for(n, 256), 256, 0, s>>>(id, wall, n, cnt, e->stats);
-            note_launch(), k_id_check<<<grid_for(n, 256), 256, 0, s>>>(cnt, n, e->stats);
-        }
         note_launch(), k_push_keys<T, D><<<grid_for(n, 256), 256, 0, s>>>(
-            (const T*)x, wall, n, g, e->key_bits, sb.k0, &e->stats->oob_walls, &e->stats->oob);
+            (const T*)x, wall, n, g, e->key_bits, sb.k0, e->stats);
         int which = 0;
         int rc = radix_sort_u32(sb.k0, sb.k1, sb.v0, sb.v1, n, e->key_bits + 1, true, sb.hist,
                                 &which, s);
@@ -563,10 +541,20 @@ static int push_end_impl(SphEngine* e, const void* v, const void* rho, const voi
                          const void* rho_scratch, const uint32_t* nnb, const uint32_t* oflow,
                          cudaStream_t s)
 {
-    if (e->n > 0)
-        note_launch(), k_push_fields<T, D><<<grid_for(e->n, 256), 256, 0, s>>>(
+    const int64_t n = e->n;
+    if (n > 0) {
+        note_launch(), k_push_fields<T, D><<<grid_for(n, 256), 256, 0, s>>>(
             eng_of<T>(e), (const T*)v, (const T*)rho, (const T*)p, (const T*)m, (const T*)vol,
             (const T*)drho, (const T*)dvdt, (const T*)rho_scratch, nnb, oflow);
+        if (e->id_range <= 0) {   // duplicates (id_range mode: distinct by contract)
+            Bump bump(e->ws, e->ws_bytes);
+            uint32_t* cnt = bump.take<uint32_t>(n);
+            if (!cnt) return SPH_ERR_WORKSPACE;
+            cudaMemsetAsync(cnt, 0, sizeof(uint32_t) * (size_t)n, s);
+            note_launch(), k_id_count<<<grid_for(n, 256), 256, 0, s>>>(e->id, n, cnt);
+            note_launch(), k_id_check<<<grid_for(n, 256), 256, 0, s>>>(cnt, n, e->stats);
+        }
+    }
     return check_launch("engine_push_end");
 }
 
@@ -583,7 +571,7 @@ extern "C" int sph_engine_push_end(SphEngine* e, const void* v, const void* rho,
                                    const void* rho_scratch, const uint32_t* nnb,
                                    const uint32_t* oflow, cudaStream_t s)
 {
-    int rc = engine_validate(e);
+    int rc = validate_ws(e);
     if (rc) return rc;
     return SPH_DISPATCH(e, push_end_impl, e, v, rho, p, m, vol, drho, dvdt, rho_scratch, nnb,
                         oflow, s);
