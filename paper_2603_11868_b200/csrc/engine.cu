@@ -72,6 +72,9 @@
 #ifndef SPH_SKIN_FMA
 #define SPH_SKIN_FMA 1          // skin test r2 with FMAs (not rounded like the reference)
 #endif
+#ifndef SPH_SKIN_SORT_ASC
+#define SPH_SKIN_SORT_ASC 1     // skin tile: all-ascending bitonic that never touches the padding
+#endif
 #ifndef SPH_SKIN_STAGE
 #define SPH_SKIN_STAGE 1        // k_skin_tile: survivors staged in shared memory, int4 stores
 #endif
@@ -466,6 +469,110 @@ __device__ __forceinline__ void block_bitonic(K* key, int P)
     }
 }
 
+// All-ascending bitonic network (each merge level starts with a "flip"
+// stage, partner i ^ (k - 1), then half-cleaners i ^ j; every comparator
+// puts the smaller key at the lower index).  With the M real keys first and
+// +inf (0xffffffff) padding after them, a comparator whose upper index is
+// >= M would compare with +inf and leave both keys in place, so it is
+// skipped: padding is never read or written and 64-key chunks wholly past
+// M are never loaded -- the work follows M, not the power of two P.
+// In registers: 2 keys per lane (positions base + 2 lane + r) of a 64-key
+// chunk; keys are unsigned, so each comparator is one min or max.
+template <class K>
+__device__ __forceinline__ K cmp_keep(K v, K o, bool keep_min)
+{
+    return keep_min ? (o < v ? o : v) : (o < v ? v : o);
+}
+
+// flip stage of block size KB (4..64) within a chunk: element 2 l + r pairs
+// with element 2 l' + 1 - r of lane l' = l ^ (KB / 2 - 1)
+template <int KB, class K>
+__device__ __forceinline__ void chunk_flip(K (&v)[2], unsigned lane)
+{
+    if constexpr (KB == 2) {
+        const K a = v[0], b = v[1];
+        v[0] = a < b ? a : b;
+        v[1] = a < b ? b : a;
+    } else {
+        const K o0 = __shfl_xor_sync(0xffffffffu, v[0], KB / 2 - 1);
+        const K o1 = __shfl_xor_sync(0xffffffffu, v[1], KB / 2 - 1);
+        const bool lower = (lane & (KB / 4)) == 0;
+        v[0] = cmp_keep(v[0], o1, lower);
+        v[1] = cmp_keep(v[1], o0, lower);
+    }
+}
+
+// half-cleaner stages J, J/2, .., 1 within a chunk (partner i ^ j)
+template <int J, class K>
+__device__ __forceinline__ void chunk_clean(K (&v)[2], unsigned lane)
+{
+    if constexpr (J >= 2) {
+        const bool lower = (lane & (J / 2)) == 0;
+        const K o0 = __shfl_xor_sync(0xffffffffu, v[0], J / 2);
+        const K o1 = __shfl_xor_sync(0xffffffffu, v[1], J / 2);
+        v[0] = cmp_keep(v[0], o0, lower);
+        v[1] = cmp_keep(v[1], o1, lower);
+        chunk_clean<J / 2>(v, lane);
+    } else if constexpr (J == 1) {
+        const K a = v[0], b = v[1];
+        v[0] = a < b ? a : b;
+        v[1] = a < b ? b : a;
+    }
+}
+
+template <int KB, class K>
+__device__ __forceinline__ void chunk_sort_levels(K (&v)[2], unsigned lane)
+{
+    chunk_flip<KB>(v, lane);
+    chunk_clean<KB / 4>(v, lane);
+    if constexpr (KB < 64) chunk_sort_levels<KB * 2>(v, lane);
+}
+
+template <int NT, class K>
+__device__ __forceinline__ void block_sort_asc(K* key, int P, int M)
+{
+    constexpr int NW = NT / 32;
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const int nchunks = (M + 63) >> 6;   // chunks holding a real key
+    for (int c = warp; c < nchunks; c += NW) {   // levels k = 2 .. 64
+        const int base = c << 6;
+        K v[2] = {key[base + 2 * lane], key[base + 2 * lane + 1]};
+        chunk_sort_levels<2>(v, lane);
+        key[base + 2 * lane] = v[0];
+        key[base + 2 * lane + 1] = v[1];
+    }
+    __syncthreads();
+    for (int k = 128; k <= P; k <<= 1) {
+        for (int q = threadIdx.x; q < (P >> 1); q += NT) {   // flip stage
+            const int h = k >> 1, t = q & (h - 1), blk = (q & ~(h - 1)) << 1;
+            const int lo = blk + t, hi = blk + k - 1 - t;
+            if (hi < M) {
+                const K x0 = key[lo], x1 = key[hi];
+                if (x1 < x0) { key[lo] = x1; key[hi] = x0; }
+            }
+        }
+        __syncthreads();
+        for (int j = k >> 2; j >= 64; j >>= 1) {
+            for (int q = threadIdx.x; q < (P >> 1); q += NT) {
+                const int lo = ((q & ~(j - 1)) << 1) | (q & (j - 1)), hi = lo + j;
+                if (hi < M) {
+                    const K x0 = key[lo], x1 = key[hi];
+                    if (x1 < x0) { key[lo] = x1; key[hi] = x0; }
+                }
+            }
+            __syncthreads();
+        }
+        for (int c = warp; c < nchunks; c += NW) {   // j = 32 .. 1 in registers
+            const int base = c << 6;
+            K v[2] = {key[base + 2 * lane], key[base + 2 * lane + 1]};
+            chunk_clean<32>(v, lane);
+            key[base + 2 * lane] = v[0];
+            key[base + 2 * lane + 1] = v[1];
+        }
+        __syncthreads();
+    }
+}
+
 template <class T, int D>
 __global__ void __launch_bounds__(SkinTile<T, D>::kThreads, SPH_SKIN_THREADS_PER_SM / SkinTile<T, D>::kThreads)
 k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
@@ -517,6 +624,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         const int nruns = 2 * rps;
 #endif
         if (warp == 0) {   // run bounds of both segments + exclusive prefix
+            if (SPH_SKIN_SORT_ASC && lane == 0) s_kept = 0;
             int64_t s0 = 0, s1 = 0;
             if ((int)lane < nruns) {
                 const int seg = (int)lane / rps, rr = (int)lane - seg * rps;
@@ -574,6 +682,43 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
             __syncthreads();
             continue;
         }
+#if SPH_SKIN_SORT_ASC
+        // kept candidates' ids appended in any order (warp-aggregated), then
+        // sorted by a network that never touches the slots past them
+        int r = 0;   // k only grows: each thread's run search resumes where it stopped
+        const CellReach<T, D> reach(cc, g, cs2);
+        for (int kb = 0; kb < M; kb += NT) {
+            const int k = kb + (int)tid;
+            bool keep = false;
+            uint32_t key = 0;
+            if (k < M) {
+                while (r + 1 < nruns && run_pre[r + 1] <= (uint32_t)k) r++;
+                const uint32_t ph = run_start[r] + ((uint32_t)k - run_pre[r]);
+                keep = true;
+                if (SPH_SKIN_PRUNE) {
+                    vec4<T> p = E.pos[ph];
+                    tile_image<T, D>(p, cc, g);
+                    keep = reach.reaches(p);
+                }
+                if (keep) key = E.id[ph];
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, keep);
+            if (b) {
+                const int leader = __ffs(b) - 1;
+                int base = 0;
+                if ((int)lane == leader) base = atomicAdd(&s_kept, __popc(b));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                if (keep) sj[base + __popc(b & lt)] = key;
+            }
+        }
+        __syncthreads();
+        const int Mk = s_kept;   // candidates kept
+        int P = 64;
+        while (P < Mk) P <<= 1;
+        for (int k = Mk + (int)tid; k < ((Mk + 63) & ~63); k += NT) sj[k] = 0xffffffffu;
+        __syncthreads();
+        block_sort_asc<NT>(sj, P, Mk);   // ids are unique: a total order
+#else
         int P = 64;
         while (P < M) P <<= 1;
         int r = 0;   // k only grows: each thread's run search resumes where it stopped
@@ -604,6 +749,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         __syncthreads();
         const int Mk = s_kept;   // candidates kept, first after the sort
         block_bitonic<NT>(sj, P);   // ids are unique: a total order
+#endif
         const int Mp = (Mk + 31) & ~31;
         for (int k = tid; k < Mp; k += NT) {
             vec4<T> p;
