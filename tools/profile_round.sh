@@ -12,7 +12,7 @@ done
 for c in ${CONFIGS:-3d4m 2d1m tg8m}; do
   python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null || exit 1
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches_$c.csv python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null 2>&1
-  ncu --set full --clock-control none --import-source on -k regex:"k_cont_du|k_mom|k_kick_drift|k_wall|k_mark|k_mask|k_fix_build" -s ${SWEEP_SKIP:-30} -c 7 -o gpurun_out/${R}_sweeps_$c python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"k_cont_du|k_mom|k_kick_drift|k_wall|k_mark|k_mask|k_fix_build" -s $([ $c = tg8m ] && echo 12 || echo ${SWEEP_SKIP:-30}) -c 7 -o gpurun_out/${R}_sweeps_$c python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null 2>&1
   ncu --set full --clock-control none --import-source on -k regex:"k_skin_tile|k_skin_warp|k_radix_scatter|k_radix_hist|k_fluid_gather|k_fluid_keys|k_seg_offsets|k_stats" -s 0 -c 14 -o gpurun_out/${R}_step_$c python tools/profile_step.py --config $c --steps 1 --warmup 1 > /dev/null 2>&1
 done
 echo done
