@@ -75,6 +75,9 @@
 #ifndef SPH_SKIN_SORT_ASC
 #define SPH_SKIN_SORT_ASC 1     // skin tile: all-ascending bitonic that never touches the padding
 #endif
+#ifndef SPH_SKIN_SORT_K4
+#define SPH_SKIN_SORT_K4 1      // ... with 4 keys per lane (128-key register chunks)
+#endif
 #ifndef SPH_SKIN_STAGE
 #define SPH_SKIN_STAGE 1        // k_skin_tile: survivors staged in shared memory, int4 stores
 #endif
@@ -573,6 +576,116 @@ __device__ __forceinline__ void block_sort_asc(K* key, int P, int M)
     }
 }
 
+// The same network with 4 keys per lane (positions base + 4 lane + r of a
+// 128-key chunk): partner distances 1 and 2 stay inside a thread.
+template <class K>
+__device__ __forceinline__ void cas_pair(K& a, K& b)
+{
+    const K lo = a < b ? a : b, hi = a < b ? b : a;
+    a = lo;
+    b = hi;
+}
+
+template <int KB, class K>
+__device__ __forceinline__ void chunk4_flip(K (&v)[4], unsigned lane)
+{
+    if constexpr (KB == 2) {
+        cas_pair(v[0], v[1]);
+        cas_pair(v[2], v[3]);
+    } else if constexpr (KB == 4) {
+        cas_pair(v[0], v[3]);
+        cas_pair(v[1], v[2]);
+    } else {   // element 4 l + r pairs with 4 l' + 3 - r, l' = l ^ (KB / 4 - 1)
+        K o[4];
+#pragma unroll
+        for (int r = 0; r < 4; r++) o[r] = __shfl_xor_sync(0xffffffffu, v[r], KB / 4 - 1);
+        const bool lower = (lane & (KB / 8)) == 0;
+#pragma unroll
+        for (int r = 0; r < 4; r++) v[r] = cmp_keep(v[r], o[3 - r], lower);
+    }
+}
+
+template <int J, class K>
+__device__ __forceinline__ void chunk4_clean(K (&v)[4], unsigned lane)
+{
+    if constexpr (J >= 4) {
+        const bool lower = (lane & (J / 4)) == 0;
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const K o = __shfl_xor_sync(0xffffffffu, v[r], J / 4);
+            v[r] = cmp_keep(v[r], o, lower);
+        }
+        chunk4_clean<J / 2>(v, lane);
+    } else if constexpr (J == 2) {
+        cas_pair(v[0], v[2]);
+        cas_pair(v[1], v[3]);
+        chunk4_clean<1>(v, lane);
+    } else if constexpr (J == 1) {
+        cas_pair(v[0], v[1]);
+        cas_pair(v[2], v[3]);
+    }
+}
+
+template <int KB, class K>
+__device__ __forceinline__ void chunk4_sort_levels(K (&v)[4], unsigned lane)
+{
+    chunk4_flip<KB>(v, lane);
+    chunk4_clean<KB / 4>(v, lane);
+    if constexpr (KB < 128) chunk4_sort_levels<KB * 2>(v, lane);
+}
+
+// P >= 128; keys [M, roundup(M, 128)) hold +inf
+template <int NT, class K>
+__device__ __forceinline__ void block_sort_asc4(K* key, int P, int M)
+{
+    constexpr int NW = NT / 32;
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const int nchunks = (M + 127) >> 7;
+    auto ld4 = [&](int base, K (&v)[4]) {
+        const uint4 q = *reinterpret_cast<const uint4*>(key + base + 4 * lane);
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    };
+    auto st4 = [&](int base, const K (&v)[4]) {
+        *reinterpret_cast<uint4*>(key + base + 4 * lane) = make_uint4(v[0], v[1], v[2], v[3]);
+    };
+    for (int c = warp; c < nchunks; c += NW) {   // levels k = 2 .. 128
+        K v[4];
+        ld4(c << 7, v);
+        chunk4_sort_levels<2>(v, lane);
+        st4(c << 7, v);
+    }
+    __syncthreads();
+    for (int k = 256; k <= P; k <<= 1) {
+        const int h = k >> 1;
+        const int qf = ((M + k - 1) / k) * h;   // flip pairs of blocks that hold a real key
+        for (int q = threadIdx.x; q < qf; q += NT) {
+            const int t = q & (h - 1), blk = (q & ~(h - 1)) << 1;
+            const int lo = blk + t, hi = blk + k - 1 - t;
+            if (hi < M) {
+                const K x0 = key[lo], x1 = key[hi];
+                if (x1 < x0) { key[lo] = x1; key[hi] = x0; }
+            }
+        }
+        __syncthreads();
+        for (int j = k >> 2; j >= 128; j >>= 1) {
+            for (int q = threadIdx.x; q < (P >> 1); q += NT) {
+                const int lo = ((q & ~(j - 1)) << 1) | (q & (j - 1)), hi = lo + j;
+                if (hi >= M) break;   // hi grows with q: no later pair is real
+                const K x0 = key[lo], x1 = key[hi];
+                if (x1 < x0) { key[lo] = x1; key[hi] = x0; }
+            }
+            __syncthreads();
+        }
+        for (int c = warp; c < nchunks; c += NW) {   // j = 64 .. 1 in registers
+            K v[4];
+            ld4(c << 7, v);
+            chunk4_clean<64>(v, lane);
+            st4(c << 7, v);
+        }
+        __syncthreads();
+    }
+}
+
 template <class T, int D>
 __global__ void __launch_bounds__(SkinTile<T, D>::kThreads, SPH_SKIN_THREADS_PER_SM / SkinTile<T, D>::kThreads)
 k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
@@ -582,7 +695,8 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
     constexpr int NT = SkinTile<T, D>::kThreads, NW = NT / 32, kC = SkinTile<T, D>::kCands;
     constexpr int kP = kC <= 64 ? 64 : (kC <= 128 ? 128 : (kC <= 256 ? 256 : (kC <= 512 ? 512
                                      : (kC <= 1024 ? 1024 : 2048))));
-    __shared__ uint32_t sj[kP];        // candidate ids, sorted; then their indices j
+    static_assert(kP >= 128, "the 4-key sort works on 128-key chunks");
+    __shared__ __align__(16) uint32_t sj[kP];   // candidate ids, sorted; then their indices j
     __shared__ vec4<T> spos[kC];       // positions in sorted order
     __shared__ uint32_t run_start[2 * 9], run_pre[2 * 9 + 1];
     __shared__ int s_kept;
@@ -713,11 +827,15 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         }
         __syncthreads();
         const int Mk = s_kept;   // candidates kept
-        int P = 64;
+        constexpr int kChunk = SPH_SKIN_SORT_K4 ? 128 : 64;
+        int P = kChunk;
         while (P < Mk) P <<= 1;
-        for (int k = Mk + (int)tid; k < ((Mk + 63) & ~63); k += NT) sj[k] = 0xffffffffu;
+        for (int k = Mk + (int)tid; k < ((Mk + kChunk - 1) & ~(kChunk - 1)); k += NT)
+            sj[k] = 0xffffffffu;
         __syncthreads();
-        block_sort_asc<NT>(sj, P, Mk);   // ids are unique: a total order
+        // ids are unique: a total order
+        if (SPH_SKIN_SORT_K4) block_sort_asc4<NT>(sj, P, Mk);
+        else block_sort_asc<NT>(sj, P, Mk);
 #else
         int P = 64;
         while (P < M) P <<= 1;
