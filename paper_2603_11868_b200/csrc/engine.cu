@@ -657,7 +657,7 @@ __device__ __forceinline__ void block_sort_asc4(K* key, int P, int M)
     __syncthreads();
     for (int k = 256; k <= P; k <<= 1) {
         const int h = k >> 1;
-        const int qf = ((M + k - 1) / k) * h;   // flip pairs of blocks that hold a real key
+        const int qf = ((M + k - 1) & ~(k - 1)) >> 1;   // flip pairs of blocks holding a real key
         for (int q = threadIdx.x; q < qf; q += NT) {
             const int t = q & (h - 1), blk = (q & ~(h - 1)) << 1;
             const int lo = blk + t, hi = blk + k - 1 - t;
@@ -710,18 +710,21 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
     const T inf = T(INFINITY);
     const uint32_t ncells = *(volatile const uint32_t*)ncells_p;
     for (uint32_t ci = blockIdx.x; ci < ncells; ci += gridDim.x) {
-        const int64_t c = cells[ci];
+        const uint32_t c = cells[ci];   // cell keys are 32-bit: 32-bit divisions
         const uint32_t f0 = E.offs_f[c], f1 = E.offs_f[c + 1];
         const uint32_t w0 = E.offs_w[c], w1 = E.offs_w[c + 1];
         const int ntf = (int)(f1 - f0), nt = ntf + (int)(w1 - w0);
         int cc[3];
         if (D == 3) {
-            cc[2] = (int)(c % g.s[2]);
-            cc[1] = (int)((c / g.s[2]) % g.s[1]);
-            cc[0] = (int)(c / ((int64_t)g.s[1] * g.s[2]));
+            const uint32_t s2 = (uint32_t)g.s[2], s1 = (uint32_t)g.s[1];
+            const uint32_t col = c / s2;
+            cc[2] = (int)(c - col * s2);
+            cc[0] = (int)(col / s1);
+            cc[1] = (int)(col - (uint32_t)cc[0] * s1);
         } else {
-            cc[1] = (int)(c % g.s[1]);
-            cc[0] = (int)(c / g.s[1]);
+            const uint32_t s1 = (uint32_t)g.s[1];
+            cc[0] = (int)(c / s1);
+            cc[1] = (int)(c - (uint32_t)cc[0] * s1);
             cc[2] = 0;
         }
 #if SPH_PERIODIC
@@ -1094,18 +1097,21 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
     const T inf = T(INFINITY);
     const uint32_t ncells = *(volatile const uint32_t*)ncells_p;
     for (uint32_t ci = blockIdx.x * NW + warp; ci < ncells; ci += gridDim.x * NW) {
-        const int64_t c = cells[ci];
+        const uint32_t c = cells[ci];   // cell keys are 32-bit: 32-bit divisions
         const uint32_t f0 = E.offs_f[c], f1 = E.offs_f[c + 1];
         const uint32_t w0 = E.offs_w[c], w1 = E.offs_w[c + 1];
         const int ntf = (int)(f1 - f0), nt = ntf + (int)(w1 - w0);
         int cc[3];
         if (D == 3) {
-            cc[2] = (int)(c % g.s[2]);
-            cc[1] = (int)((c / g.s[2]) % g.s[1]);
-            cc[0] = (int)(c / ((int64_t)g.s[1] * g.s[2]));
+            const uint32_t s2 = (uint32_t)g.s[2], s1 = (uint32_t)g.s[1];
+            const uint32_t col = c / s2;
+            cc[2] = (int)(c - col * s2);
+            cc[0] = (int)(col / s1);
+            cc[1] = (int)(col - (uint32_t)cc[0] * s1);
         } else {
-            cc[1] = (int)(c % g.s[1]);
-            cc[0] = (int)(c / g.s[1]);
+            const uint32_t s1 = (uint32_t)g.s[1];
+            cc[0] = (int)(c / s1);
+            cc[1] = (int)(c - (uint32_t)cc[0] * s1);
             cc[2] = 0;
         }
 #if SPH_PERIODIC
