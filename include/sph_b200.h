@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 14
+#define SPH_ABI_VERSION 15
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -284,7 +284,11 @@ typedef struct {
     uint32_t* key_sorted; uint32_t* key_prev; uint32_t* perm; uint32_t* inv;
     int32_t* lists_alt; int32_t* lcount_alt;
     int32_t lists_stale;
-    int32_t reserved1;
+    /* library state: 1 while the cell order and offsets were computed from
+     * the current positions (set by a push or a CLL rebuild, cleared by
+     * anything that moves particles), so a list build can take each
+     * particle's cell from the CLL instead of recomputing it */
+    int32_t cll_fresh;
     /* local displacement bound (f32 runs with the persistent arrays): per
      * grid cell (dev, ncells) the largest path length since the lists' build
      * of the particles whose CLL cell it is (cellmax, float bits) and its

@@ -105,7 +105,7 @@ class SphEngine(C.Structure):
         ("id_range", c_i64),
         ("key_sorted", P), ("key_prev", P), ("perm", P), ("inv", P),
         ("lists_alt", P), ("lcount_alt", P),
-        ("lists_stale", c_i32), ("reserved1", c_i32),
+        ("lists_stale", c_i32), ("cll_fresh", c_i32),
         ("cellmax", P), ("blockmax", P),
     ]
 
@@ -127,7 +127,7 @@ class SphSlabGeom(C.Structure):
     ]
 
 
-ABI_VERSION = 14   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 15   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)

@@ -78,6 +78,9 @@
 #ifndef SPH_SKIN_SORT_K4
 #define SPH_SKIN_SORT_K4 1      // ... with 4 keys per lane (128-key register chunks)
 #endif
+#ifndef SPH_LIST_FRESH
+#define SPH_LIST_FRESH 1        // list builds on a fresh CLL take each particle's cell from it
+#endif
 #ifndef SPH_SKIN_STAGE
 #define SPH_SKIN_STAGE 1        // k_skin_tile: survivors staged in shared memory, int4 stores
 #endif
@@ -690,7 +693,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(SkinTile<T, D>::kThreads, SPH_SKIN_THREADS_PER_SM / SkinTile<T, D>::kThreads)
 k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
             const uint32_t* __restrict__ cells, const uint32_t* __restrict__ ncells_p,
-            const uint32_t* __restrict__ phys_of_id, int wall_pairs)
+            const uint32_t* __restrict__ phys_of_id, int wall_pairs, int fresh)
 {
     constexpr int NT = SkinTile<T, D>::kThreads, NW = NT / 32, kC = SkinTile<T, D>::kCands;
     constexpr int kP = kC <= 64 ? 64 : (kC <= 128 ? 128 : (kC <= 256 ? 256 : (kC <= 512 ? 512
@@ -785,8 +788,8 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                 T xi[3];
                 to3<T>(E.pos[i], xi);
                 int cxyz[3];
-                E.cell0[i] = cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c ? (uint32_t)c
-                                                                          : kInvalidCell;
+                E.cell0[i] = fresh || cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c
+                                 ? (uint32_t)c : kInvalidCell;
                 E.lcount[E.nf_pad + (i - nf)] = 0;
                 E.disp[i] = T(0);
                 E.disp0[i] = T(0);
@@ -978,7 +981,9 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
                 xi[1] = lane ? xb[1] : xa[1];
                 xi[2] = lane ? xb[2] : xa[2];
                 int cxyz[3];
-                const bool ok = cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c && cnt <= kCap;
+                // fresh CLL: the particle's cell is c by construction
+                const bool ok = (fresh || cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c) &&
+                                cnt <= kCap;
                 E.cell0[i] = ok ? (uint32_t)c : kInvalidCell;
                 E.lcount[slot] = ok ? cnt : 0;
                 if (wall_pairs) E.nww[slot] = lane ? naB : naA;
@@ -1084,7 +1089,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(256, SPH_SKINW_MINB)
 k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cells,
             const uint32_t* __restrict__ ncells_p, const uint32_t* __restrict__ phys_of_id,
-            uint32_t* __restrict__ big, uint32_t* __restrict__ nbig)
+            uint32_t* __restrict__ big, uint32_t* __restrict__ nbig, int fresh)
 {
     constexpr int NW = 8, kW = 128;
     __shared__ uint32_t wsj[NW][kW];
@@ -1239,7 +1244,7 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
                 xi[1] = lane ? xb[1] : xa[1];
                 xi[2] = lane ? xb[2] : xa[2];
                 int cxyz[3];
-                const bool ok = cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c;
+                const bool ok = fresh || cell_key_of<T, D>(xi, g, cxyz) == (uint32_t)c;
                 E.cell0[i] = ok ? (uint32_t)c : kInvalidCell;
                 E.lcount[slot] = ok ? (lane ? cntB : cntA) : 0;
                 E.nww[slot] = lane ? naB : naA;
@@ -2291,12 +2296,14 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
             const int64_t wb = (want + 7) / 8;
             note_launch(), k_skin_warp<T, D><<<(unsigned)(wb < 148 * 8 ? wb : 148 * 8), 256, 0,
                                                s>>>(g, cs2, E, cells, counts, phys_of_id, big,
-                                                    counts + 1);
+                                                    counts + 1, SPH_LIST_FRESH ? e->cll_fresh : 0);
             note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, big,
-                                                                  counts + 1, phys_of_id, 1);
+                                                                  counts + 1, phys_of_id, 1,
+                                                                  SPH_LIST_FRESH ? e->cll_fresh : 0);
         } else {        // 3D blocks hold ~450: a thread block per cell
             note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, cells, counts,
-                                                                  phys_of_id, wall_pairs);
+                                                                  phys_of_id, wall_pairs,
+                                                                  SPH_LIST_FRESH ? e->cll_fresh : 0);
         }
         note_launch(), k_skin_big<T, D><<<148 * 2, kNlThreads, 0, s>>>(acc, g, cs2, E);
     }
@@ -2641,6 +2648,7 @@ static void substep_parts(SphEngine* e, T half, T full, bool fuse, cudaEvent_t* 
                           cudaStream_t s, cudaEvent_t* marks = nullptr)
 {
     if (ev) cudaEventRecord(ev[0], s);
+    e->cll_fresh = 0;   // particles move from here on
     if (!e->drifted) sub_kick_drift<T, D>(e, half, full, s);
     e->drifted = 0;
     if (marks) cudaEventRecord(marks[0], s);   // positions final
@@ -2756,6 +2764,7 @@ extern "C" int sph_engine_substeps_timed(SphEngine* e, double half_dt, double fu
 template <class T, int D>
 static int phase_impl(SphEngine* e, int phase, double half_d, double full_d, cudaStream_t s)
 {
+    e->cll_fresh = 0;   // a phase may move particles (kick + drift)
     const T half = T(half_d), full = T(full_d);
     switch (phase) {
     case SPH_PHASE_KICK_DRIFT:   // already applied by a MOMENTUM_NEXT phase?
@@ -2888,5 +2897,6 @@ extern "C" int sph_engine_unpack(SphEngine* e, int32_t kind, const int32_t* phys
     int rc = engine_begin(e, s);
     if (rc) return rc;
     if (sph_engine_halo_width(kind) < 0 || count < 0) return SPH_ERR_INVALID;
+    if (kind == SPH_HALO_XV) e->cll_fresh = 0;   // ghosts' positions change
     return SPH_DISPATCH(e, unpack_impl, e, kind, phys, count, in, s);
 }

@@ -532,6 +532,7 @@ static int push_begin_impl(SphEngine* e, const void* x, const uint32_t* id,
     e->lists_ready = 0;
     e->lists_stale = 0;
     e->nww_ready = 0;
+    e->cll_fresh = 1;
     return check_launch("engine_push_begin");
 }
 
@@ -633,6 +634,7 @@ static int rebuild_impl(SphEngine* e, cudaStream_t s)
     // lists valid until now can be carried across this rebuild (maintain)
     e->lists_stale = e->lists_ready && e->key_sorted ? 1 : 0;
     e->lists_ready = 0;
+    e->cll_fresh = 1;   // walls never move: their order stays current
     if (nf <= 0) return SPH_OK;
     Bump bump(e->ws, e->ws_bytes);
     SortBufs sb = sort_bufs(e, bump);

@@ -14,6 +14,8 @@ result (x and rho / p / drho during the last momentum sweep), which the
 same comparisons cover.
 """
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -162,3 +164,28 @@ def test_overlapped_push_rejects_bad_ids_and_recovers(bad_id):
         assert sim.last_push_overlapped   # every step follows a view
         for f in FIELDS:
             assert reg.view(f).tobytes() == osim.f[f].tobytes(), (step, f)
+
+
+def test_cll_fresh_flag_follows_particle_motion():
+    """SphEngine.cll_fresh (list builds on a fresh CLL take each particle's
+    cell from the CLL instead of recomputing it): set by a push and by a CLL
+    rebuild, cleared by anything that moves particles."""
+    from paper_2603_11868_b200 import _native
+    reg, grid = cases.build_case(cases.CaseConfig(case="dambreak2d", dp=0.05,
+                                                  precision="f32"))
+    sim = Simulation(reg, grid, CUDA)
+    sim.initialize()
+    E = sim._dev["E"]
+    assert E.cll_fresh == 1          # push + rebuild, then the initial sweeps move nothing
+    sim.advance()
+    assert E.cll_fresh == 0          # the step's sub-steps drifted the particles
+    sim._rebuild_cll()
+    assert E.cll_fresh == 1
+    sim._build_lists(0.0)            # a list build moves nothing
+    assert E.cll_fresh == 1
+    sim._call("sph_engine_phase", ctypes.c_int32(_native.PHASE_KICK_DRIFT),
+              ctypes.c_double(1e-6), ctypes.c_double(2e-6))
+    assert E.cll_fresh == 0
+    reg.view("x")                    # pull, then the next step pushes
+    sim.advance()
+    assert E.cll_fresh == 0 and sim.last_push_overlapped
