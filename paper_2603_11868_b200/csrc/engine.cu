@@ -81,6 +81,9 @@
 #ifndef SPH_LIST_FRESH
 #define SPH_LIST_FRESH 1        // list builds on a fresh CLL take each particle's cell from it
 #endif
+#ifndef SPH_SKIN_BLOCKED
+#define SPH_SKIN_BLOCKED 1      // skin tile: each thread loads a contiguous candidate range
+#endif
 #ifndef SPH_SKIN_STAGE
 #define SPH_SKIN_STAGE 1        // k_skin_tile: survivors staged in shared memory, int4 stores
 #endif
@@ -807,8 +810,11 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         // sorted by a network that never touches the slots past them
         int r = 0;   // k only grows: each thread's run search resumes where it stopped
         const CellReach<T, D> reach(cc, g, cs2);
-        for (int kb = 0; kb < M; kb += NT) {
-            const int k = kb + (int)tid;
+        // SPH_SKIN_BLOCKED: thread t takes candidates [t per, t per + per), so
+        // its run search moves past few run boundaries; else k = t + NT i
+        const int per = SPH_SKIN_BLOCKED ? (M + NT - 1) / NT : 1;
+        for (int kb = 0; kb < (SPH_SKIN_BLOCKED ? per : M); kb += (SPH_SKIN_BLOCKED ? 1 : NT)) {
+            const int k = SPH_SKIN_BLOCKED ? (int)tid * per + kb : kb + (int)tid;
             bool keep = false;
             uint32_t key = 0;
             if (k < M) {
