@@ -71,6 +71,8 @@ CASES = {
     "3d": (lambda: cases.build_case(cases.kleefsman_config(dp=0.03, precision="f32")), {}, 4),
     "3d_f64": (lambda: cases.build_case(cases.kleefsman_config(dp=0.04, precision="f64")), {}, 3),
     "clamped_cloud": (_clamped_cloud, {}, 6),
+    "taylor_green_periodic": (lambda: cases.build_case(
+        cases.taylor_green_config(3, 24, precision="f32")), {}, 4),
 }
 
 
