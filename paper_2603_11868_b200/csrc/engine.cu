@@ -84,6 +84,9 @@
 #ifndef SPH_SKIN_BLOCKED
 #define SPH_SKIN_BLOCKED 1      // skin tile: each thread loads a contiguous candidate range
 #endif
+#ifndef SPH_SKIN_DYN
+#define SPH_SKIN_DYN 1          // skin tile: cells handed out by an atomic counter
+#endif
 #ifndef SPH_SKIN_STAGE
 #define SPH_SKIN_STAGE 1        // k_skin_tile: survivors staged in shared memory, int4 stores
 #endif
@@ -696,7 +699,8 @@ template <class T, int D>
 __global__ void __launch_bounds__(SkinTile<T, D>::kThreads, SPH_SKIN_THREADS_PER_SM / SkinTile<T, D>::kThreads)
 k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
             const uint32_t* __restrict__ cells, const uint32_t* __restrict__ ncells_p,
-            const uint32_t* __restrict__ phys_of_id, int wall_pairs, int fresh)
+            const uint32_t* __restrict__ phys_of_id, int wall_pairs, int fresh,
+            uint32_t* __restrict__ work)
 {
     constexpr int NT = SkinTile<T, D>::kThreads, NW = NT / 32, kC = SkinTile<T, D>::kCands;
     constexpr int kP = kC <= 64 ? 64 : (kC <= 128 ? 128 : (kC <= 256 ? 256 : (kC <= 512 ? 512
@@ -715,7 +719,17 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
     const int64_t nf = E.nf;
     const T inf = T(INFINITY);
     const uint32_t ncells = *(volatile const uint32_t*)ncells_p;
-    for (uint32_t ci = blockIdx.x; ci < ncells; ci += gridDim.x) {
+    // SPH_SKIN_DYN: after its first cell a CTA takes the next unclaimed one
+    // (*work counts the cells claimed beyond the first gridDim.x), so cells of
+    // uneven cost spread over the CTAs; else a static grid stride
+    __shared__ uint32_t s_next;
+    auto next_cell = [&](uint32_t cur) -> uint32_t {
+        if (!SPH_SKIN_DYN) return cur + gridDim.x;
+        if (tid == 0) s_next = gridDim.x + atomicAdd(work, 1u);
+        __syncthreads();
+        return s_next;
+    };
+    for (uint32_t ci = blockIdx.x; ci < ncells; ci = next_cell(ci)) {
         const uint32_t c = cells[ci];   // cell keys are 32-bit: 32-bit divisions
         const uint32_t f0 = E.offs_f[c], f1 = E.offs_f[c + 1];
         const uint32_t w0 = E.offs_w[c], w1 = E.offs_w[c + 1];
@@ -1095,7 +1109,8 @@ template <class T, int D>
 __global__ void __launch_bounds__(256, SPH_SKINW_MINB)
 k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cells,
             const uint32_t* __restrict__ ncells_p, const uint32_t* __restrict__ phys_of_id,
-            uint32_t* __restrict__ big, uint32_t* __restrict__ nbig, int fresh)
+            uint32_t* __restrict__ big, uint32_t* __restrict__ nbig, int fresh,
+            uint32_t* __restrict__ work)
 {
     constexpr int NW = 8, kW = 128;
     __shared__ uint32_t wsj[NW][kW];
@@ -1107,7 +1122,13 @@ k_skin_warp(const GridP<T> g, T cs2, Eng<T> E, const uint32_t* __restrict__ cell
     const int64_t nf = E.nf;
     const T inf = T(INFINITY);
     const uint32_t ncells = *(volatile const uint32_t*)ncells_p;
-    for (uint32_t ci = blockIdx.x * NW + warp; ci < ncells; ci += gridDim.x * NW) {
+    auto next_cell = [&](uint32_t cur) -> uint32_t {   // as k_skin_tile, per warp
+        if (!SPH_SKIN_DYN) return cur + gridDim.x * NW;
+        uint32_t v = 0;
+        if (lane == 0) v = gridDim.x * NW + atomicAdd(work, 1u);
+        return __shfl_sync(0xffffffffu, v, 0);
+    };
+    for (uint32_t ci = blockIdx.x * NW + warp; ci < ncells; ci = next_cell(ci)) {
         const uint32_t c = cells[ci];   // cell keys are 32-bit: 32-bit divisions
         const uint32_t f0 = E.offs_f[c], f1 = E.offs_f[c + 1];
         const uint32_t w0 = E.offs_w[c], w1 = E.offs_w[c + 1];
@@ -2292,24 +2313,27 @@ static int build_lists_impl(SphEngine* e, double skin, cudaStream_t s)
         uint32_t* phys_of_id = bump.take<uint32_t>(e->id_range > e->n ? e->id_range : e->n);
         uint32_t* cells = bump.take<uint32_t>(e->n);   // nonempty cells <= n
         uint32_t* big = bump.take<uint32_t>(e->n);     // cells with > 128 candidates
-        uint32_t* counts = bump.take<uint32_t>(2);
+        uint32_t* counts = bump.take<uint32_t>(4);   // nonempty, big, tile / warp work counters
         if (!counts) return SPH_ERR_WORKSPACE;
         note_launch(), k_phys_of_id<<<grid_for(e->n, 256), 256, 0, s>>>(e->id, e->n, phys_of_id);
-        cudaMemsetAsync(counts, 0, 2 * sizeof(uint32_t), s);
+        cudaMemsetAsync(counts, 0, 4 * sizeof(uint32_t), s);
         note_launch(), k_nonempty_cells<<<grid_for(e->ncells, 256), 256, 0, s>>>(
             e->offs_f, e->offs_w, e->ncells, cells, counts);
         if (D == 2) {   // 2D blocks hold ~60 candidates: a warp per cell
             const int64_t wb = (want + 7) / 8;
             note_launch(), k_skin_warp<T, D><<<(unsigned)(wb < 148 * 8 ? wb : 148 * 8), 256, 0,
                                                s>>>(g, cs2, E, cells, counts, phys_of_id, big,
-                                                    counts + 1, SPH_LIST_FRESH ? e->cll_fresh : 0);
+                                                    counts + 1, SPH_LIST_FRESH ? e->cll_fresh : 0,
+                                                    counts + 3);
             note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, big,
                                                                   counts + 1, phys_of_id, 1,
-                                                                  SPH_LIST_FRESH ? e->cll_fresh : 0);
+                                                                  SPH_LIST_FRESH ? e->cll_fresh : 0,
+                                                                  counts + 2);
         } else {        // 3D blocks hold ~450: a thread block per cell
             note_launch(), k_skin_tile<T, D><<<blocks, NT, 0, s>>>(acc, g, cs2, E, cells, counts,
                                                                   phys_of_id, wall_pairs,
-                                                                  SPH_LIST_FRESH ? e->cll_fresh : 0);
+                                                                  SPH_LIST_FRESH ? e->cll_fresh : 0,
+                                                                  counts + 2);
         }
         note_launch(), k_skin_big<T, D><<<148 * 2, kNlThreads, 0, s>>>(acc, g, cs2, E);
     }
