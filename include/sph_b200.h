@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SPH_ABI_VERSION 15
+#define SPH_ABI_VERSION 16
 #define SPH_NEIGHBOR_CAPACITY 256   /* neighborhood.py:30 NEIGHBOR_CAPACITY */
 
 /* status codes; mapped to the reference's exception classes by the host */
@@ -320,6 +320,14 @@ int sph_engine_push_end(SphEngine* e, const void* v, const void* rho, const void
                         const void* m, const void* vol, const void* drho, const void* dvdt,
                         const void* rho_scratch, const uint32_t* nnb, const uint32_t* oflow,
                         cudaStream_t s);
+/* push_end may leave vol, rho_scratch and oflow NULL and deliver them later
+ * with push_tail (registry-order ids + those fields; any may be NULL), e.g.
+ * after the step's sub-steps: the step reads none of them (rho_scratch only
+ * on a Shepard step, which must not defer it); a deferred oflow yields
+ * to the overflow flags (1) the step set meanwhile, as the pushed value
+ * would have. */
+int sph_engine_push_tail(SphEngine* e, const uint32_t* id, const void* vol,
+                         const void* rho_scratch, const uint32_t* oflow, cudaStream_t s);
 int sph_engine_pull(const SphEngine* e, void* x, void* v, void* rho, void* p, void* m, void* vol,
                     void* drho, void* dvdt, void* rho_scratch, uint32_t* id, uint32_t* wall,
                     uint32_t* nnb, uint32_t* oflow, cudaStream_t s);

@@ -127,7 +127,7 @@ class SphSlabGeom(C.Structure):
     ]
 
 
-ABI_VERSION = 15   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
+ABI_VERSION = 16   # include/sph_b200.h SPH_ABI_VERSION (SphEngine layout)
 STATS_RESET = 1
 STATS_NORMS = 2
 # sph_engine_phase / halo records (include/sph_b200.h)
@@ -156,6 +156,7 @@ _PROTOS = {
     "sph_engine_push": (c_i32, [_P] * 14 + [_P]),
     "sph_engine_push_begin": (c_i32, [_P] * 4 + [_P]),
     "sph_engine_push_end": (c_i32, [_P] * 11 + [_P]),
+    "sph_engine_push_tail": (c_i32, [_P] * 5 + [_P]),
     "sph_engine_pull": (c_i32, [_P] * 14 + [_P]),
     "sph_engine_pull_fields": (c_i32, [_P, C.c_uint32] + [_P] * 13 + [_P]),
     "sph_engine_rebuild_cll": (c_i32, [_P, _P]),

@@ -110,9 +110,27 @@ __global__ void k_push_fields(Eng<T> E, const T* __restrict__ v, const T* __rest
     E.drho[i] = drho[r];
     E.nnb[i] = nnb[r];
     const uint32_t pid = E.id[i];   // in range (k_push_place)
-    E.rho_scratch_id[pid] = rho_scratch[r];
-    E.oflow_id[pid] = oflow[r];
-    E.vol_id[pid] = vol[r];
+    if (rho_scratch) E.rho_scratch_id[pid] = rho_scratch[r];   // else: sph_engine_push_tail
+    if (oflow) E.oflow_id[pid] = oflow[r];
+    if (vol) E.vol_id[pid] = vol[r];
+}
+
+// the by-id fields a push deferred (registry order in, by id out): oflow
+// keeps the flags the step's sweeps set meanwhile
+template <class T>
+__global__ void k_push_tail(Eng<T> E, const uint32_t* __restrict__ id, int64_t n,
+                            const T* __restrict__ vol, const T* __restrict__ rho_scratch,
+                            const uint32_t* __restrict__ oflow)
+{
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t pid = id[r];
+    if (pid >= (uint64_t)E.idr) return;   // the push reported it (push_error)
+    if (vol) E.vol_id[pid] = vol[r];
+    if (rho_scratch) E.rho_scratch_id[pid] = rho_scratch[r];
+    // flagged by this step's sweeps: 1 (as the plain push's value would have
+    // been overwritten); else the pushed value
+    if (oflow && E.oflow_id[pid] == 0u) E.oflow_id[pid] = oflow[r];
 }
 
 // registry-order copies of the fields in mask (bit k: field k of x, v, rho,
@@ -544,6 +562,8 @@ static int push_end_impl(SphEngine* e, const void* v, const void* rho, const voi
 {
     const int64_t n = e->n;
     if (n > 0) {
+        if (!oflow)   // deferred to sph_engine_push_tail, which ORs into these
+            cudaMemsetAsync(e->oflow_id, 0, sizeof(uint32_t) * (size_t)eng_of<T>(e).idr, s);
         note_launch(), k_push_fields<T, D><<<grid_for(n, 256), 256, 0, s>>>(
             eng_of<T>(e), (const T*)v, (const T*)rho, (const T*)p, (const T*)m, (const T*)vol,
             (const T*)drho, (const T*)dvdt, (const T*)rho_scratch, nnb, oflow);
@@ -557,6 +577,26 @@ static int push_end_impl(SphEngine* e, const void* v, const void* rho, const voi
         }
     }
     return check_launch("engine_push_end");
+}
+
+template <class T, int D>
+static int push_tail_impl(SphEngine* e, const uint32_t* id, const void* vol,
+                          const void* rho_scratch, const uint32_t* oflow, cudaStream_t s)
+{
+    if (e->n > 0)
+        note_launch(), k_push_tail<T><<<grid_for(e->n, 256), 256, 0, s>>>(
+            eng_of<T>(e), id, e->n, (const T*)vol, (const T*)rho_scratch, oflow);
+    return check_launch("engine_push_tail");
+}
+
+extern "C" int sph_engine_push_tail(SphEngine* e, const uint32_t* id, const void* vol,
+                                    const void* rho_scratch, const uint32_t* oflow,
+                                    cudaStream_t s)
+{
+    int rc = engine_validate(e);
+    if (rc) return rc;
+    if (!id) return SPH_ERR_INVALID;
+    return SPH_DISPATCH(e, push_tail_impl, e, id, vol, rho_scratch, oflow, s);
 }
 
 extern "C" int sph_engine_push_begin(SphEngine* e, const void* x, const uint32_t* id,

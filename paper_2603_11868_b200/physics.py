@@ -399,6 +399,9 @@ _HOST_SAME_FIELDS = ("m", "Vol", "id", "wall", "oflow", "rho_scratch")
 # fields that place the particles, then the rest
 _PUSH_FIRST = ("x", "id", "wall")
 _PUSH_REST = ("v", "rho", "p", "m", "Vol", "drho", "dvdt", "rho_scratch", "nnb", "oflow")
+# by-id fields the step itself never reads (rho_scratch: except on a Shepard
+# step): uploaded last and delivered after the sub-steps (sph_engine_push_tail)
+_PUSH_TAIL = ("Vol", "rho_scratch", "oflow")
 # a step that starts from a host push uploads the second half behind its own
 # skin-list build (SPH_PUSH_OVERLAP=0: the plain push)
 PUSH_OVERLAP = os.environ.get("SPH_PUSH_OVERLAP", "1") != "0"
@@ -606,6 +609,7 @@ class Simulation:
         self._last_step = None      # (vmax, amax, dt) of the last step: skin forecast
         self.push_overlap = PUSH_OVERLAP
         self.last_push_overlapped = False
+        self._pending_tail = None   # (event, {field: landing tensor}) of a split push
         self.eager_pull = EAGER_PULL
         self.last_pull_overlapped = False
         self._viewed = False        # a registry view since the last step
@@ -758,7 +762,10 @@ class Simulation:
         reg = self.registry
         ts = d["tstream"]
         cs = self._copy_stream()
-        ev_first, ev_rest = d["push_events"]
+        ev_first, ev_rest, ev_tail = d["push_events"]
+        shepard = self.shepard_every and self.step_count > 0 \
+            and self.step_count % self.shepard_every == 0
+        tail = tuple(f for f in _PUSH_TAIL if not (shepard and f == "rho_scratch"))
 
         def upload(f):
             src = self._host_tensor(f)
@@ -770,8 +777,10 @@ class Simulation:
         with torch.cuda.stream(cs):
             first = [upload(f) for f in _PUSH_FIRST]
             ev_first.record(cs)
-            rest = [upload(f) for f in _PUSH_REST]
+            rest = {f: upload(f) for f in _PUSH_REST if f not in tail}
             ev_rest.record(cs)
+            late = {f: upload(f) for f in tail}
+            ev_tail.record(cs)
         self.last_push_bytes = sum(reg.raw_view(f).nbytes for f in _ENGINE_FIELDS)
         ts.wait_event(ev_first)
         rc = self._lib().sph_engine_push_begin(ctypes.byref(d["E"]),
@@ -784,13 +793,30 @@ class Simulation:
         self.last_list_mode = "build"
         self.phase_seconds["cll"] += time.perf_counter() - t0
         ts.wait_event(ev_rest)
-        rc = self._lib().sph_engine_push_end(ctypes.byref(d["E"]),
-                                             *[ptr(t) for t in rest], d["stream"])
+        rc = self._lib().sph_engine_push_end(
+            ctypes.byref(d["E"]), *[ptr(rest[f]) if f in rest else None for f in _PUSH_REST],
+            d["stream"])
         _native.check(rc, "engine_push_end")
+        late["id"] = first[_PUSH_FIRST.index("id")]
+        self._pending_tail = (ev_tail, late)
         self._host_same = set(_HOST_SAME_FIELDS)
         self._host_dirty = False
         self._host_stale = False
         self._norms = None
+
+    def _deliver_tail(self):
+        """Queue the deferred by-id fields of the last split push (after the
+        step's sub-steps: nothing before reads them)."""
+        if self._pending_tail is None:
+            return
+        ev, late = self._pending_tail
+        self._pending_tail = None
+        d = self._dev
+        d["tstream"].wait_event(ev)
+        rc = self._lib().sph_engine_push_tail(
+            ctypes.byref(d["E"]), ptr(late["id"]),
+            *[ptr(late[f]) if f in late else None for f in _PUSH_TAIL], d["stream"])
+        _native.check(rc, "engine_push_tail")
 
     def _copy_stream(self):
         """The engine's host-transfer stream, its events and its device
@@ -801,7 +827,7 @@ class Simulation:
         if d["cstream"] is None:
             d["cstream"] = torch.cuda.Stream(device=d["device"])
             d["landing"] = {}
-            d["push_events"] = (torch.cuda.Event(), torch.cuda.Event())
+            d["push_events"] = (torch.cuda.Event(), torch.cuda.Event(), torch.cuda.Event())
             ev = [torch.cuda.Event() for _ in range(3)]
             for e in ev:   # materialise the events: their handles go to the library
                 e.record(d["tstream"])
@@ -1065,9 +1091,11 @@ class Simulation:
             if overlapped:
                 if s.push_error:
                     self._host_dirty = True
+                    self._pending_tail = None
                     raise ValueError("registry ids must be a permutation of 0..N-1")
                 if s.fluid_seen != d["E"].nf:   # the wall flags changed: plain push
                     self._host_dirty = True
+                    self._pending_tail = None
                     self._last_step = None
                     return self.advance(end_time)
                 self._oob_walls = s.oob_walls
@@ -1112,15 +1140,18 @@ class Simulation:
                                               C_void(marks[0].cuda_event),
                                               C_void(marks[1].cuda_event), d["stream"])
             _native.check(rc, "engine_substeps_marked")
+            self._deliver_tail()
             marks[2].record(d["tstream"])
             self._pull_overlapped(marks, marks[2])
         elif self.kernel_times is None:
             rc = L.sph_engine_substeps(E, half, full, nsub, d["stream"])
             _native.check(rc, "engine_substeps")
+            self._deliver_tail()
         else:   # per-kernel CUDA-event timing (bench.py roofline pass)
             ms = (ctypes.c_float * 5)()
             rc = L.sph_engine_substeps_timed(E, half, full, nsub, ms, d["stream"])
             _native.check(rc, "engine_substeps_timed")
+            self._deliver_tail()
             for k, name in enumerate(SUBSTEP_KERNELS):   # per sub-step average
                 self.kernel_times.setdefault(name, []).append(ms[k] / nsub)
         self._call("sph_engine_stats", ctypes.c_int32(_native.STATS_NORMS))

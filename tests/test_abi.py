@@ -26,7 +26,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_native.EXPORTED)
-    assert lib.sph_abi_version() == _native.ABI_VERSION == 15
+    assert lib.sph_abi_version() == _native.ABI_VERSION == 16
 
 
 def test_struct_layouts_match_header(tmp_path):
