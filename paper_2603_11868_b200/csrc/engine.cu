@@ -823,6 +823,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         // kept candidates' ids appended in any order (warp-aggregated), then
         // sorted by a network that never touches the slots past them
         int r = 0;   // k only grows: each thread's run search resumes where it stopped
+        uint32_t nb = nruns > 1 ? run_pre[1] : 0xffffffffu;   // run r ends at nb
         const CellReach<T, D> reach(cc, g, cs2);
         // SPH_SKIN_BLOCKED: thread t takes candidates [t per, t per + per), so
         // its run search moves past few run boundaries; else k = t + NT i
@@ -832,7 +833,10 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
             bool keep = false;
             uint32_t key = 0;
             if (k < M) {
-                while (r + 1 < nruns && run_pre[r + 1] <= (uint32_t)k) r++;
+                while ((uint32_t)k >= nb) {
+                    r++;
+                    nb = r + 1 < nruns ? run_pre[r + 1] : 0xffffffffu;
+                }
                 const uint32_t ph = run_start[r] + ((uint32_t)k - run_pre[r]);
                 keep = true;
                 if (SPH_SKIN_PRUNE) {
