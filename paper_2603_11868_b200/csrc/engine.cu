@@ -87,6 +87,9 @@
 #ifndef SPH_SKIN_DYN
 #define SPH_SKIN_DYN 1          // skin tile: cells handed out by an atomic counter
 #endif
+#ifndef SPH_SKIN_BBOX
+#define SPH_SKIN_BBOX 1         // skin tile: prune against the cell's particles' bounding box
+#endif
 #ifndef SPH_SKIN_STAGE
 #define SPH_SKIN_STAGE 1        // k_skin_tile: survivors staged in shared memory, int4 stores
 #endif
@@ -355,6 +358,19 @@ struct CellReach {
             lo[k] = cc[k] > 0 ? a - w : -inf;
             hi[k] = cc[k] < g.s[k] - 1 ? a + g.cs + w : inf;
 #endif
+        }
+        r2 = cs2 * T(1.0002);
+    }
+    // the box spanned by the cell's own particles (bounded grids): every
+    // candidate within reach of a particle is within reach of this box
+    __device__ __forceinline__ CellReach(const T (&bl)[3], const T (&bh)[3], const GridP<T>& g,
+                                         T cs2)
+    {
+        const T w = T(1e-4) * g.cs;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            lo[k] = bl[k] - w;
+            hi[k] = bh[k] + w;
         }
         r2 = cs2 * T(1.0002);
     }
@@ -723,6 +739,7 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
     // (*work counts the cells claimed beyond the first gridDim.x), so cells of
     // uneven cost spread over the CTAs; else a static grid stride
     __shared__ uint32_t s_next;
+    __shared__ T s_bb[NW][6];   // per-warp bounding boxes of the cell's particles
     auto next_cell = [&](uint32_t cur) -> uint32_t {
         if (!SPH_SKIN_DYN) return cur + gridDim.x;
         if (tid == 0) s_next = gridDim.x + atomicAdd(work, 1u);
@@ -824,7 +841,50 @@ k_skin_tile(const EngAcc<T> acc, const GridP<T> g, T cs2, Eng<T> E,
         // sorted by a network that never touches the slots past them
         int r = 0;   // k only grows: each thread's run search resumes where it stopped
         uint32_t nb = nruns > 1 ? run_pre[1] : 0xffffffffu;   // run r ends at nb
+#if SPH_SKIN_BBOX && SPH_SKIN_PRUNE
+        // the cell's particles' bounding box (block min / max reduction)
+        T bl[3] = {inf, inf, inf}, bh[3] = {-inf, -inf, -inf};
+        for (int t = (int)tid; t < nt; t += NT) {
+            const int64_t i = t < ntf ? (int64_t)f0 + t : nf + w0 + (t - ntf);
+            T x[3];
+            to3<T>(E.pos[i], x);
+#pragma unroll
+            for (int k = 0; k < D; k++) {
+                bl[k] = fmin(bl[k], x[k]);
+                bh[k] = fmax(bh[k], x[k]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < D; k++) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                bl[k] = fmin(bl[k], __shfl_xor_sync(0xffffffffu, bl[k], o));
+                bh[k] = fmax(bh[k], __shfl_xor_sync(0xffffffffu, bh[k], o));
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < D; k++) {
+                s_bb[warp][k] = bl[k];
+                s_bb[warp][3 + k] = bh[k];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < D; k++) {
+            bl[k] = s_bb[0][k];
+            bh[k] = s_bb[0][3 + k];
+#pragma unroll
+            for (int w = 1; w < NW; w++) {
+                bl[k] = fmin(bl[k], s_bb[w][k]);
+                bh[k] = fmax(bh[k], s_bb[w][3 + k]);
+            }
+        }
+        if (D == 2) { bl[2] = T(0); bh[2] = T(0); }
+        const CellReach<T, D> reach(bl, bh, g, cs2);
+#else
         const CellReach<T, D> reach(cc, g, cs2);
+#endif
         // SPH_SKIN_BLOCKED: thread t takes candidates [t per, t per + per), so
         // its run search moves past few run boundaries; else k = t + NT i
         const int per = SPH_SKIN_BLOCKED ? (M + NT - 1) / NT : 1;
