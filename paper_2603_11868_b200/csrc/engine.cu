@@ -62,13 +62,9 @@
 #ifndef SPH_SKIN_FLUID_PASS
 #define SPH_SKIN_FLUID_PASS 1   // k_skin_tile: fluid-pair passes without wall tests
 #endif
-#ifndef SPH_SKIN_PRUNE          // drop block candidates beyond the cell box's skin reach
-#if SPH_PERIODIC                // (3D 4M skin build -4%; Taylor-Green +2%: bounded only)
-#define SPH_SKIN_PRUNE 0
-#else
-#define SPH_SKIN_PRUNE 1
-#endif
-#endif
+#ifndef SPH_SKIN_PRUNE          // drop block candidates beyond the cell's skin reach (against
+#define SPH_SKIN_PRUNE 1        // the cell box: 3D 4M -4%, Taylor-Green +2%; against the
+#endif                          // particles' box, SPH_SKIN_BBOX: -14% / -8%)
 #ifndef SPH_SKIN_FMA
 #define SPH_SKIN_FMA 1          // skin test r2 with FMAs (not rounded like the reference)
 #endif
